@@ -1,0 +1,695 @@
+"""Benchmark driver for the B200 SU(3) hot path (contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload nn-weak|nn-strong|nn32|link|routine:<name>] [--dtype f32|f64]
+
+Default workload = BASELINE configs[4], weak-scaling variant: the periodic
+nearest-neighbour sweep on a 64^3 x 16*N lattice, t sharded into one 64^3x16
+slab per GPU (one-site halos over NCCL), complex64; one step = 10 repeated
+applications v <- D v on device-resident fields.  `value` is whole-job
+site-ops/s (sites x applications / s, max over ranks); `e2e` is the same
+metric through the reference-facing path with host (AoS, pinned) buffers
+and the H2D/D2H copies inside the timed region; `roofline` is the NN-sweep
+kernel's algorithmic HBM bytes / CUDA-event duration against the measured
+copy bandwidth in MEASURED_PEAKS.json.
+
+--impl reference times the reference's own algorithm on the host CPU (the
+pinned numpy restatement in oracle/, parallelised over t-slabs with all host
+threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SU(3) site-ops/s and HBM GB/s as % of peak (fp32/fp64), 1–8 GPUs"
+UNIT = "site-ops/s"
+FALLBACK_HBM_GBS = 6650.0
+
+# algorithmic (compulsory) HBM bytes per site: read each input object once, write each output once
+NN_BYTES = {"f32": 336, "f64": 672}        # U 72 reals + v 6 + out 6
+LINK_BYTES = {"f32": 360, "f64": 720}      # U 72 + acc 18
+ROUTINE_REALS = {                           # (in reals, out reals) per site
+    "mult_su3_mat_vec": (24, 6),
+    "mult_adj_su3_mat_vec": (24, 6),
+    "mult_su3_nn": (36, 18),
+    "mult_su3_na": (36, 18),
+    "mult_su3_an": (36, 18),
+    "scalar_mult_add_su3_matrix": (36, 18),
+    "mult_su3_mat_vec_sum_4dir": (96, 6),
+    "mult_adj_su3_mat_vec_4dir": (78, 24),
+}
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--workload", default="nn-weak")
+    p.add_argument("--dtype", choices=["f32", "f64"], default=None)
+    p.add_argument("--applications", type=int, default=10)
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e measurement")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--sites", type=int, default=64**4, help="sites for routine:<name> workloads")
+    args = p.parse_args(argv)
+    if args.warmup < 3:
+        p.error("--warmup must be >= 3")
+    if args.dtype is None:
+        args.dtype = "f64" if args.workload == "link" else "f32"
+    return args
+
+
+# ----------------------------------------------------------------------------
+# workload geometry
+# ----------------------------------------------------------------------------
+
+def workload_config(args, world):
+    w = args.workload
+    if w == "nn-weak":
+        return dict(kind="nn", global_dims=(64, 64, 64, 16 * world), apps=args.applications,
+                    name=f"config5-weak: periodic NN sweep 64^3x16*N t-slabs, {args.applications} applications/step")
+    if w == "nn-strong":
+        return dict(kind="nn", global_dims=(64, 64, 64, 128), apps=args.applications,
+                    name=f"config5-strong: periodic NN sweep 64^3x128 t-slabs, {args.applications} applications/step")
+    if w == "nn32":
+        return dict(kind="nn", global_dims=(32, 32, 32, 32), apps=1, name="config2: periodic NN sweep 32^4, 1 application/step")
+    if w == "link":
+        return dict(kind="link", global_dims=(48, 48, 48, 48), apps=1, name="config3: link-product sweep 48^4, 1 sweep/step")
+    if w.startswith("routine:"):
+        r = w.split(":", 1)[1]
+        if r not in ROUTINE_REALS:
+            raise SystemExit(f"unknown routine {r!r}")
+        return dict(kind="routine", routine=r, nsites=args.sites, apps=1,
+                    name=f"{r} streaming batch of {args.sites} sites (roofline run for configs[0]/[1])")
+    raise SystemExit(f"unknown workload {w!r}")
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region (NVML)
+# ----------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001
+            self.ok = False
+        self.period = period_s
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            time.sleep(self.period)
+
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        except Exception:  # noqa: BLE001
+            pass
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self.ok and self._t is not None:
+            self._sample()
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        names = [n for n, bit in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:  # noqa: BLE001
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(workload: str, dtype: str):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(f"{workload}/{dtype}")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing
+# ----------------------------------------------------------------------------
+
+def init_dist(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus > 1 must be launched with torch.distributed.run (one rank per GPU)")
+    if args.impl == "b200" or world > 1:
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        if args.impl == "b200":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return rank, world, local
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world, device=None):
+    if world > 1:
+        import torch.distributed as dist
+
+        if device is not None:
+            dist.barrier(device_ids=[device.index])
+        else:
+            dist.barrier()
+
+
+# ----------------------------------------------------------------------------
+# the B200 arm
+# ----------------------------------------------------------------------------
+
+def run_b200(args, rank, world, local):
+    import torch
+
+    from paper_1309_0551_b200 import inputs, kernels, sweeps
+    from paper_1309_0551_b200.lattice import Field, Lattice4D
+    from paper_1309_0551_b200.slab import SlabSweep
+
+    cfg = workload_config(args, world)
+    dev = torch.device("cuda", local)
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(inputs.SEED + 7919 * rank)
+    stream = torch.cuda.current_stream(dev)
+    launches_per_step = 0
+    dominant_events = []  # (start, end) pairs around the dominant kernel
+
+    if cfg["kind"] == "nn":
+        gd = cfg["global_dims"]
+        glat = Lattice4D(*gd)
+        lat = glat.slab(world, rank)
+        U_aos = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen)
+        v_aos = inputs.random_vectors_torch(lat.volume, None, tdt, dev, gen)
+        U = Field.from_aos(lat, "mat4", U_aos)
+        v0 = Field.from_aos(lat, "vec", v_aos)
+        va, vb = v0.empty_like(), v0.empty_like()
+        va.data.copy_(v0.data)
+        slab = SlabSweep(U)
+        ntl = lat.nt
+        if world == 1:
+            per_launch_sites = lat.volume
+            launches_per_app = 1
+        else:
+            per_launch_sites = max(ntl - 2, 0) * lat.slice_sites
+            launches_per_app = 2 + (1 if ntl > 2 else 0) + 1  # interior + 2 boundary + halo pack
+        bytes_per_launch = per_launch_sites * NN_BYTES[args.dtype]
+        apps = cfg["apps"]
+
+        def step(record=False):
+            nonlocal va, vb
+            for _ in range(apps):
+                if record:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                if world == 1:
+                    if record:
+                        e0.record(stream)
+                    sweeps.nn_sweep(U, va, out=vb)
+                    if record:
+                        e1.record(stream)
+                        dominant_events.append((e0, e1))
+                else:
+                    _apply_sharded(slab, va, vb, record, dominant_events, stream)
+                va, vb = vb, va
+
+        launches_per_step = apps * launches_per_app
+        sites_per_step = lat.volume * apps  # per rank
+        del U_aos
+    elif cfg["kind"] == "link":
+        lat = Lattice4D(*cfg["global_dims"])
+        if world > 1:
+            raise SystemExit("the link-product workload is single-GPU (replicas only)")
+        U_aos = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen)
+        U = Field.from_aos(lat, "mat4", U_aos)
+        del U_aos
+        acc = Field(lat, "mat", tdt, dev)
+        bytes_per_launch = lat.volume * LINK_BYTES[args.dtype]
+        mode = os.environ.get("SU3G_LINK_MODE", "fma")
+
+        def step(record=False):
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            sweeps.link_product(U, 1.0 / 6.0, mode=mode, out=acc)
+            if record:
+                e1.record(stream)
+                dominant_events.append((e0, e1))
+
+        launches_per_step = 1
+        sites_per_step = lat.volume
+        cfg["name"] += f", {mode} arithmetic"
+    else:  # routine streaming batch
+        r = cfg["routine"]
+        n = cfg["nsites"]
+        rin, rout = ROUTINE_REALS[r]
+        from paper_1309_0551_b200 import _lib
+
+        kinds = {"mult_su3_mat_vec_sum_4dir": (72, 24), "mult_adj_su3_mat_vec_4dir": (72, 6)}.get(r, (18, rin - 18))
+        a = torch.randn(n * kinds[0], dtype=tdt, device=dev, generator=gen)
+        b = torch.randn(n * kinds[1], dtype=tdt, device=dev, generator=gen)
+        c = torch.empty(n * rout, dtype=tdt, device=dev)
+        sfx = args.dtype
+        bytes_per_launch = n * (rin + rout) * (4 if sfx == "f32" else 8)
+
+        def launch():
+            if r == "scalar_mult_add_su3_matrix":
+                _lib.call(f"su3g_{r}_{sfx}", a.data_ptr(), b.data_ptr(), 0.5, None, c.data_ptr(), n, stream.cuda_stream)
+            else:
+                _lib.call(f"su3g_{r}_{sfx}", a.data_ptr(), b.data_ptr(), c.data_ptr(), n, stream.cuda_stream)
+
+        def step(record=False):
+            if record:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            launch()
+            if record:
+                e1.record(stream)
+                dominant_events.append((e0, e1))
+
+        launches_per_step = 1
+        sites_per_step = n
+
+    # ---- warm-up, then the timed region ---------------------------------
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    barrier(world, dev)
+    torch.cuda.synchronize(dev)
+    clocks.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks.stop()
+    barrier(world, dev)
+    elapsed_ms = max_over_ranks(t0.elapsed_time(t1), world, dev)
+    kern_ms = [a.elapsed_time(b) for a, b in dominant_events]
+    kern_avg_ms = max_over_ranks(float(np.mean(kern_ms)) if kern_ms else float("nan"), world, dev)
+
+    total_sites = sites_per_step * world * args.steps
+    value = total_sites / (elapsed_ms / 1e3)
+    peak, peak_src = peak_hbm()
+    achieved = bytes_per_launch / (kern_avg_ms / 1e3) / 1e9 if kern_ms else None
+
+    # ---- e2e through the host-buffer path ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(args, cfg, rank, world, dev, tdt, stream)
+
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak" if args.workload == "nn-weak" else ("strong" if args.workload == "nn-strong" else "weak"),
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic (seeded SU(3) Gram-Schmidt links + complex-Gaussian vectors, generated on device)",
+        "config": {
+            "workload": cfg["name"],
+            "lattice": list(cfg.get("global_dims", [])) or None,
+            "sites_per_gpu": sites_per_step // max(cfg["apps"], 1),
+            "applications_per_step": cfg["apps"],
+            "parallelism": f"t-slab x{world}" if cfg["kind"] == "nn" else f"replicas x{world}",
+            "l2": "inputs larger than L2 (U alone > 1 GB/GPU); no flush needed",
+        },
+        "impl": "b200",
+        "hbm_gbs": achieved,
+        "roofline": {
+            "bound": "hbm",
+            "kernel": {"nn": "k_nn_sweep", "link": "k_link_product"}.get(cfg["kind"], "k_stream"),
+            "achieved": achieved,
+            "peak": peak,
+            "peak_source": peak_src,
+            "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic_for(args.workload, args.dtype),
+            "algorithmic_bytes_per_launch": bytes_per_launch,
+            "kernel_avg_ms": kern_avg_ms,
+        },
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+    }
+    if rank == 0 and not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args, cfg, threads=1)
+    return line
+
+
+def _apply_sharded(slab, v, out, record, events, stream):
+    """slab.apply with CUDA events around the interior (dominant) kernel."""
+    import torch
+
+    from paper_1309_0551_b200.slab import boundary_ranges
+
+    k = slab.k
+    w_send, v_hi, w_lo = slab._buffers(v)
+    k.halo_w(slab.U, v, w_send)
+    reqs = slab.exchange(v, w_send, v_hi, w_lo)
+    interior, edges = boundary_ranges(k.nt(v))
+    if interior is not None:
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        k.sweep(slab.U, v, out, interior, v_hi, w_lo)
+        if record:
+            e1.record(stream)
+            events.append((e0, e1))
+    for r in reqs:
+        r.wait()
+    for rng in edges:
+        k.sweep(slab.U, v, out, rng, v_hi, w_lo)
+
+
+def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
+    """Same metric through the reference-facing path: pinned host AoS in, host AoS out, copies timed."""
+    import torch
+
+    from paper_1309_0551_b200 import inputs, sweeps
+    from paper_1309_0551_b200.lattice import Field, Lattice4D
+    from paper_1309_0551_b200.slab import SlabSweep
+
+    steps = max(3, min(args.steps, 10))
+    if cfg["kind"] == "nn":
+        lat = Lattice4D(*cfg["global_dims"]).slab(world, rank)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(99 + rank)
+        U_h = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen).cpu().pin_memory()
+        v_h = inputs.random_vectors_torch(lat.volume, None, tdt, dev, gen).cpu().pin_memory()
+        out_h = torch.empty_like(v_h).pin_memory()
+        U_d = torch.empty_like(U_h, device=dev)
+        v_d = torch.empty_like(v_h, device=dev)
+        Uf = Field(lat, "mat4", tdt, dev)
+        va, vb = Field(lat, "vec", tdt, dev), Field(lat, "vec", tdt, dev)
+        slab = SlabSweep(Uf)
+
+        def step():
+            U_d.copy_(U_h, non_blocking=True)
+            v_d.copy_(v_h, non_blocking=True)
+            Field.from_aos(lat, "mat4", U_d, out=Uf)
+            Field.from_aos(lat, "vec", v_d, out=va)
+            res = slab.apply_n(va, vb, cfg["apps"])
+            res.to_aos(out=v_d)
+            out_h.copy_(v_d, non_blocking=True)
+
+        h2d = U_h.numel() * U_h.element_size() + v_h.numel() * v_h.element_size()
+        d2h = out_h.numel() * out_h.element_size()
+        sites = lat.volume * cfg["apps"]
+    elif cfg["kind"] == "link":
+        lat = Lattice4D(*cfg["global_dims"])
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(99)
+        U_h = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen).cpu().pin_memory()
+        out_h = torch.empty((lat.volume, 3, 3, 2), dtype=tdt).pin_memory()
+        U_d = torch.empty_like(U_h, device=dev)
+        o_d = torch.empty_like(out_h, device=dev)
+        Uf = Field(lat, "mat4", tdt, dev)
+        mode = os.environ.get("SU3G_LINK_MODE", "fma")
+
+        def step():
+            U_d.copy_(U_h, non_blocking=True)
+            Field.from_aos(lat, "mat4", U_d, out=Uf)
+            sweeps.link_product(Uf, 1.0 / 6.0, mode=mode).to_aos(out=o_d)
+            out_h.copy_(o_d, non_blocking=True)
+
+        h2d = U_h.numel() * U_h.element_size()
+        d2h = out_h.numel() * out_h.element_size()
+        sites = lat.volume
+    else:
+        from paper_1309_0551_b200 import kernels
+
+        r = cfg["routine"]
+        n = cfg["nsites"]
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(99)
+        shapes = {
+            "mult_su3_mat_vec": ((3, 3, 2), (3, 2)), "mult_adj_su3_mat_vec": ((3, 3, 2), (3, 2)),
+            "mult_su3_mat_vec_sum_4dir": ((4, 3, 3, 2), (4, 3, 2)), "mult_adj_su3_mat_vec_4dir": ((4, 3, 3, 2), (3, 2)),
+        }.get(r, ((3, 3, 2), (3, 3, 2)))
+        a_h = torch.randn((n,) + shapes[0], dtype=tdt, generator=gen, device=dev).cpu().pin_memory()
+        b_h = torch.randn((n,) + shapes[1], dtype=tdt, generator=gen, device=dev).cpu().pin_memory()
+        a_d, b_d = torch.empty_like(a_h, device=dev), torch.empty_like(b_h, device=dev)
+        res_shape = {"mult_su3_mat_vec": (3, 2), "mult_adj_su3_mat_vec": (3, 2), "mult_su3_mat_vec_sum_4dir": (3, 2),
+                     "mult_adj_su3_mat_vec_4dir": (4, 3, 2)}.get(r, (3, 3, 2))
+        c_d = torch.empty((n,) + res_shape, dtype=tdt, device=dev)
+        out_h = torch.empty((n,) + res_shape, dtype=tdt).pin_memory()
+        fn = kernels.KERNELS[r]
+
+        def step():
+            a_d.copy_(a_h, non_blocking=True)
+            b_d.copy_(b_h, non_blocking=True)
+            if r == "scalar_mult_add_su3_matrix":
+                fn(a_d, b_d, 0.5, out=c_d)
+            else:
+                fn(a_d, b_d, out=c_d)
+            out_h.copy_(c_d, non_blocking=True)
+
+        h2d = (a_h.numel() + b_h.numel()) * a_h.element_size()
+        d2h = out_h.numel() * out_h.element_size()
+        sites = n
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize(dev)
+    barrier(world, dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world, dev)
+    ms = max_over_ranks(e0.elapsed_time(e1), world, dev)
+    return {
+        "value": sites * world * steps / (ms / 1e3),
+        "unit": UNIT,
+        "h2d_bytes_per_step": int(h2d),
+        "d2h_bytes_per_step": int(d2h),
+        "steps": steps,
+        "path": "pinned host AoS -> H2D -> AoS->SoA -> kernels (+NCCL halos) -> SoA->AoS -> D2H",
+    }
+
+
+# ----------------------------------------------------------------------------
+# CPU side: the reference algorithm (pinned numpy port in oracle/) on host cores
+# ----------------------------------------------------------------------------
+
+def _cpu_sample(cfg, dtype, small=False):
+    """A bounded sample of the workload for the host CPU: (callable, site-ops per call, state, description)."""
+    from oracle import routines as R
+    from oracle import sweeps as S
+    from paper_1309_0551_b200 import inputs
+
+    dt = np.float32 if dtype == "f32" else np.float64
+    rng = inputs.config_rng(424242)
+    if cfg["kind"] == "nn":
+        nx, ny, nz = cfg["global_dims"][:3]
+        if small:
+            nx, ny, nz = min(nx, 32), min(ny, 32), min(nz, 32)
+        dims = (nx, ny, nz, 4)
+        V = nx * ny * nz * 4
+        U = inputs.random_links(rng, V, 4, dtype=dt)
+        v = inputs.random_vectors(rng, V, None, dtype=dt)
+        return (lambda: S.nn_sweep(U, v, dims)), V, (dims, U, v), f"composed reference NN sweep on a {nx}x{ny}x{nz}x4 sample, 1 application"
+    if cfg["kind"] == "link":
+        dims = (48, 48, 8, 4)
+        V = int(np.prod(dims))
+        U = inputs.random_links(rng, V, 4, dtype=dt)
+        return (lambda: S.link_product(U, dims, 1 / 6)), V, (dims, U, None), "composed reference link product on a 48x48x8x4 sample"
+    r = cfg["routine"]
+    n = 1 << 18
+    if r in ("mult_su3_mat_vec_sum_4dir",):
+        ops = [inputs.random_links(rng, n, 4, dtype=dt), inputs.random_vectors(rng, n, 4, dtype=dt)]
+    elif r == "mult_adj_su3_mat_vec_4dir":
+        ops = [inputs.random_links(rng, n, 4, dtype=dt), inputs.random_vectors(rng, n, None, dtype=dt)]
+    elif r in ("mult_su3_mat_vec", "mult_adj_su3_mat_vec"):
+        ops = [inputs.random_links(rng, n, None, dtype=dt), inputs.random_vectors(rng, n, None, dtype=dt)]
+    elif r == "scalar_mult_add_su3_matrix":
+        ops = [inputs.random_links(rng, n, None, dtype=dt), inputs.random_links(rng, n, None, dtype=dt), dt(0.5)]
+    else:
+        ops = [inputs.random_links(rng, n, None, dtype=dt), inputs.random_links(rng, n, None, dtype=dt)]
+    fn = R.ROUTINES[r]
+    return (lambda: fn(*ops)), n, None, f"reference {r} (numpy restatement) on {n} sites"
+
+
+def _parallel_nn(state, threads):
+    """The composed reference sweep split into t-slabs with explicit halos, one slab per host thread."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import routines as R
+    from oracle import sweeps as S
+
+    dims, U, v = state
+    nx, ny, nz, nt = dims
+    F = nx * ny * nz
+    parts = min(threads, nt)
+    while nt % parts:
+        parts -= 1
+
+    def one(r):
+        t0, t1 = S.slab_bounds(nt, parts, r)
+        nxt, prv = (t1 % nt) * F, ((t0 - 1) % nt) * F
+        w_lo = R.mult_adj_su3_mat_vec(U[prv : prv + F, 3], v[prv : prv + F])
+        return S.nn_sweep_slab(U[t0 * F : t1 * F], v[t0 * F : t1 * F], (nx, ny, nz, t1 - t0), v[nxt : nxt + F], w_lo)
+
+    with ThreadPoolExecutor(parts) as ex:
+        return list(ex.map(one, range(parts)))
+
+
+def cpu_baseline(args, cfg, threads=1, budget_s=10.0):
+    fn, sites, state, desc = _cpu_sample(cfg, args.dtype)
+    if threads > 1 and cfg["kind"] == "nn":
+        def call():
+            return _parallel_nn(state, threads)
+    else:
+        threads = 1
+        call = fn
+    call()  # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        call()
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or n >= 50:
+            break
+    return {
+        "value": sites * n / el,
+        "unit": UNIT,
+        "cores": threads,
+        "kind": "port",
+        "sample": f"{desc}; {n} calls in {el:.2f} s",
+        "host_cpus": os.cpu_count(),
+    }
+
+
+def run_reference(args, rank, world):
+    cfg = workload_config(args, world)
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    fn, sites, state, desc = _cpu_sample(cfg, args.dtype, small=True)
+    call = (lambda: _parallel_nn(state, threads)) if cfg["kind"] == "nn" else fn
+    if cfg["kind"] != "nn":
+        threads = 1
+    for _ in range(args.warmup):
+        call()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    el = time.perf_counter() - t0
+    value = sites * args.steps / el
+    return {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": el * 1e3 / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak" if args.workload == "nn-weak" else "strong",
+        "vs_baseline": None,
+        "dtype": args.dtype,
+        "data": "synthetic (seeded SU(3) links + complex-Gaussian vectors)",
+        "config": {"workload": cfg["name"], "lattice": list(cfg.get("global_dims", [])) or None},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{desc} per step; reference association (numpy restatement pinned bitwise to su3bench)",
+                         "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    rank, world, local = init_dist(args)
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_b200(args, rank, world, local)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/* libsu3g -- B200 (sm_100a) SU(3) lattice hot path, C ABI.
+ *
+ * Drop-in boundary for the per-site routines of the reference package su3bench
+ * (arXiv 1309.0551; /root/reference/pkg/src/su3bench).  The reference exposes
+ * them as Python functions fn(a, b, out=None) on site-major (re, im) pair arrays
+ * (simd.py:80-230) behind the plugin registry Backend(kind, apply, batch_apply,
+ * kernels) (backends.py:11-31).  Each entry point below replaces one of those
+ * kernels for a batch of `nsites` independent operand sets; the Python layer
+ * (paper_1309_0551_b200.kernels / .backends) restores the reference signatures.
+ *
+ * Conventions
+ *   - Pointers are DEVICE pointers.  Per-site routine operands are dense in the
+ *     reference AoS order: matrix (3,3,2), vector (3,2), mat4 (4,3,3,2), vec4
+ *     (4,3,2) per site, sites contiguous (types.py:1-13, OPERAND_SHAPES).
+ *   - Work is enqueued on `stream` (a cudaStream_t) and the call returns after
+ *     enqueue.  No allocation, no host synchronisation.
+ *   - Arithmetic follows the reference association (separated sums, combine
+ *     once, no FMA; scalar.py:8-14), so results are bit-identical to su3bench.
+ *   - Return value: 0 = ok, <0 = invalid argument (SU3G_EINVAL), >0 = a
+ *     cudaError_t.  su3g_last_error() returns the calling thread's message.
+ *   - Result storage must not alias an input (the reference's contract,
+ *     validation.py:25-34); it is the caller's responsibility, as there.
+ */
+#ifndef SU3G_H
+#define SU3G_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SU3G_API __attribute__((visibility("default")))
+#else
+#define SU3G_API
+#endif
+
+typedef struct CUstream_st *su3g_stream_t; /* == cudaStream_t */
+
+#define SU3G_OK 0
+#define SU3G_EINVAL (-1)
+
+#define SU3G_ABI_VERSION 1
+
+/* link-product arithmetic: exact reference association, or FMA chains */
+#define SU3G_EXACT 0
+#define SU3G_FMA 1
+
+SU3G_API int su3g_abi_version(void);
+SU3G_API const char *su3g_last_error(void);
+/* number of SMs / L2 bytes of the current device (0 on failure) */
+SU3G_API int su3g_device_sm_count(void);
+SU3G_API int64_t su3g_device_l2_bytes(void);
+
+/* ---- per-site routines (8 hot routines x {f32, f64}) ---------------------
+ * c = routine(a, b) for every site.                                            */
+
+/* replaces su3bench.simd.mult_su3_mat_vec (simd.py:80-91; scalar.py:49-60) */
+SU3G_API int su3g_mult_su3_mat_vec_f32(const float *a, const float *b, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_su3_mat_vec_f64(const double *a, const double *b, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_adj_su3_mat_vec (simd.py:94-105; scalar.py:63-74) */
+SU3G_API int su3g_mult_adj_su3_mat_vec_f32(const float *a, const float *b, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_adj_su3_mat_vec_f64(const double *a, const double *b, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_su3_nn (simd.py:108-119; scalar.py:77-89) */
+SU3G_API int su3g_mult_su3_nn_f32(const float *a, const float *b, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_su3_nn_f64(const double *a, const double *b, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_su3_na (simd.py:136-149; scalar.py:92-104) */
+SU3G_API int su3g_mult_su3_na_f32(const float *a, const float *b, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_su3_na_f64(const double *a, const double *b, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_su3_an (simd.py:122-133; scalar.py:107-119) */
+SU3G_API int su3g_mult_su3_an_f32(const float *a, const float *b, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_su3_an_f64(const double *a, const double *b, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_adj_su3_mat_vec_4dir (simd.py:172-179; scalar.py:140-146)
+ * a4: mat4 per site, b: vec per site, c: vec4 per site */
+SU3G_API int su3g_mult_adj_su3_mat_vec_4dir_f32(const float *a4, const float *b, float *c4, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_adj_su3_mat_vec_4dir_f64(const double *a4, const double *b, double *c4, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_su3_mat_vec_sum_4dir (simd.py:197-214; scalar.py:168-194)
+ * c = sum_d adj(a4[d]) b4[d]  -- the ADJOINT form the reference code implements */
+SU3G_API int su3g_mult_su3_mat_vec_sum_4dir_f32(const float *a4, const float *b4, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_su3_mat_vec_sum_4dir_f64(const double *a4, const double *b4, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.scalar_mult_add_su3_matrix (simd.py:224-230; scalar.py:197-205)
+ * c = a + s*b; s_per_site (nsites reals) overrides s when non-NULL (simd.py:217-221) */
+SU3G_API int su3g_scalar_mult_add_su3_matrix_f32(const float *a, const float *b, float s, const float *s_per_site, float *c,
+                                        int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_scalar_mult_add_su3_matrix_f64(const double *a, const double *b, double s, const double *s_per_site,
+                                        double *c, int64_t nsites, su3g_stream_t stream);
+
+/* ---- layout transforms ---------------------------------------------------
+ * AoS (reference site-major, `reals_per_site` reals per site, sites x-fastest;
+ * lattice.py:155-187 SiteBuffer) <-> GPU-internal t-sliced SoA:
+ *     soa[(t * reals_per_site + c) * sites_per_slice + s3]
+ * where a slice is one fixed-t block of sites_per_slice = nx*ny*nz sites (a
+ * t-face is contiguous in the reference numbering, lattice.py:3-6).
+ * nslices = 1 gives plain SoA.  reals_per_site <= 72.                        */
+SU3G_API int su3g_aos_to_soa_f32(const float *aos, float *soa, int64_t sites_per_slice, int64_t nslices, int32_t reals_per_site,
+                        su3g_stream_t stream);
+SU3G_API int su3g_aos_to_soa_f64(const double *aos, double *soa, int64_t sites_per_slice, int64_t nslices,
+                        int32_t reals_per_site, su3g_stream_t stream);
+SU3G_API int su3g_soa_to_aos_f32(const float *soa, float *aos, int64_t sites_per_slice, int64_t nslices, int32_t reals_per_site,
+                        su3g_stream_t stream);
+SU3G_API int su3g_soa_to_aos_f64(const double *soa, double *aos, int64_t sites_per_slice, int64_t nslices,
+                        int32_t reals_per_site, su3g_stream_t stream);
+
+/* ---- periodic nearest-neighbour sweep (BASELINE configs[2], configs[4]) ----
+ *   out(x) = sum_mu U_mu(x) v(x+mu) - sum_mu U_mu(x-mu)^dag v(x-mu)
+ * in the association of the composed reference oracle:
+ *   ((((fw0+fw1)+fw2)+fw3) - bw0 - bw1 - bw2 - bw3), fw = mult_su3_mat_vec,
+ *   bw = mult_adj_su3_mat_vec.
+ * Fields are t-sliced SoA on a local lattice nx*ny*nz*nt: U has 72 reals per
+ * site (mu-major, 18 each), v/out 6.  x, y, z are periodic.  Along t:
+ *   v_hi (6*F reals, SoA face) = v on the slice after the last local one, or
+ *        NULL -> periodic (slice 0);
+ *   w_lo (6*F reals)           = U_t(x)^dag v(x) on the slice before slice 0
+ *        (computed by its owner with su3g_nn_halo_w), or NULL -> periodic.
+ * Only slices t in [t_begin, t_end) of `out` are written (interior/boundary
+ * split for overlapping a halo exchange).                                   */
+SU3G_API int su3g_nn_sweep_f32(const float *U, const float *v, float *out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                      int32_t t_begin, int32_t t_end, const float *v_hi, const float *w_lo, su3g_stream_t stream);
+SU3G_API int su3g_nn_sweep_f64(const double *U, const double *v, double *out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                      int32_t t_begin, int32_t t_end, const double *v_hi, const double *w_lo, su3g_stream_t stream);
+/* w_face = U_t(x)^dag v(x) on the LAST local t-slice (the halo a t-slab sends
+ * to its +t neighbour; 6*F reals, SoA face) */
+SU3G_API int su3g_nn_halo_w_f32(const float *U, const float *v, float *w_face, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                       su3g_stream_t stream);
+SU3G_API int su3g_nn_halo_w_f64(const double *U, const double *v, double *w_face, int32_t nx, int32_t ny, int32_t nz,
+                       int32_t nt, su3g_stream_t stream);
+
+/* ---- link-product sweep (BASELINE configs[3]) ------------------------------
+ * acc(x) = sum over (mu,nu) in (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) of
+ *          s * U_mu(x) U_nu(x+mu) U_mu(x+nu)^dag, accumulated in that order
+ *          via mult_su3_nn -> mult_su3_na -> scalar_mult_add_su3_matrix,
+ *          starting from acc = 0; periodic lattice.
+ * U: t-sliced SoA, 72 reals/site; acc: t-sliced SoA, 18 reals/site.
+ * mode SU3G_EXACT = reference association (bitwise), SU3G_FMA = FMA chains.  */
+SU3G_API int su3g_link_product_f32(const float *U, float *acc, int32_t nx, int32_t ny, int32_t nz, int32_t nt, float s,
+                          int32_t mode, su3g_stream_t stream);
+SU3G_API int su3g_link_product_f64(const double *U, double *acc, int32_t nx, int32_t ny, int32_t nz, int32_t nt, double s,
+                          int32_t mode, su3g_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SU3G_H */

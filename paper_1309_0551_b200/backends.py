@@ -1,0 +1,58 @@
+"""The "b200" backend behind the reference's plugin API.
+
+su3bench selects kernels through ``Backend(kind, apply, batch_apply, kernels)``
+records looked up by name (backends.py:11-31); its harnesses (verify._route,
+verify.py:67-70; bench.run_hot / run_streaming, bench.py:186,234) only ever
+touch that record.  This module provides the same record for the GPU path and
+a shim that inserts it into a live su3bench registry, so the reference's own
+parity sweep and timing harness drive the B200 kernels unchanged:
+
+    import su3bench
+    from paper_1309_0551_b200 import backends
+    backends.register_with_su3bench()
+    su3bench.verify.check_routine("mult_su3_nn", candidate="b200")
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from types import MappingProxyType
+from typing import Callable, Mapping
+
+from . import kernels
+
+
+@dataclass(frozen=True)
+class Backend:
+    kind: str
+    apply: Callable
+    batch_apply: Callable
+    kernels: Mapping[str, Callable] = field(repr=False)
+
+
+B200 = Backend("b200", kernels.apply, kernels.batch_apply, MappingProxyType(kernels.KERNELS))
+
+_BACKENDS = {"b200": B200}
+BACKEND_NAMES = tuple(_BACKENDS)
+
+
+def get_backend(kind: str) -> Backend:
+    try:
+        return _BACKENDS[kind]
+    except KeyError:
+        raise ValueError(f"unknown backend {kind!r}; expected one of {BACKEND_NAMES}") from None
+
+
+def register_with_su3bench(name: str = "b200"):
+    """Insert the GPU backend into su3bench.backends._BACKENDS (the reference has no register call).
+
+    The reference registry holds su3bench.backends.Backend records; a record of
+    that class is built so isinstance checks in the reference keep working.
+    Only the eight hot-path routines are provided; asking the registered
+    backend for another routine raises KeyError, as a missing kernel would.
+    """
+    import su3bench.backends as ref_backends
+
+    rec = ref_backends.Backend(name, kernels.apply, kernels.batch_apply, MappingProxyType(kernels.KERNELS))
+    ref_backends._BACKENDS[name] = rec
+    ref_backends.BACKEND_NAMES = tuple(ref_backends._BACKENDS)
+    return rec

@@ -1,0 +1,273 @@
+// Per-site SU(3) routines on the reference AoS layout, sm_100a.
+//
+// Design: every routine is a pure stream --
+// each site's operands are read once and its result written once, arithmetic
+// intensity 0.08-0.9 flop/B -- so the kernel is built to move bytes at HBM
+// speed, not to do math:
+//   * persistent CTAs (grid = resident CTAs per SM x 148 SMs) walk tiles of TS
+//     consecutive sites;
+//   * a tile's operand bytes are contiguous in the AoS layout, so one elected
+//     thread moves each operand tile with a single TMA bulk copy
+//     (cp.async.bulk ... mbarrier::complete_tx, SASS UBLKCP) into a STAGES-deep
+//     shared-memory ring, evict-first in L2;
+//   * one thread per site loads its record from shared memory with 8/16-byte
+//     vector loads (AoS 72-byte f32 matrices are not 16-byte aligned per site,
+//     which is why global loads are not done per thread), computes in
+//     registers, writes the result record to a double-buffered smem tile;
+//   * the result tile goes back with one bulk store (cp.async.bulk.global).
+// Sites that do not fill a whole tile are handled by plain per-thread loads
+// in the last CTA; misaligned (non-16-byte) base pointers take a direct
+// per-thread kernel.  Both paths share the same per-site arithmetic, which is
+// the reference association (su3_math.cuh), so every path is bit-identical to
+// su3bench.
+#include <algorithm>
+
+#include "su3_math.cuh"
+
+namespace su3g {
+
+// ---------------------------------------------------------------------------
+// routine descriptors: reals per site of a, b, c; optional per-site scalar
+// ---------------------------------------------------------------------------
+template <typename T_>
+struct OpMatVec {
+    using T = T_;
+    static constexpr int NA = 18, NB = 6, NC = 6;
+    static constexpr bool SCALAR = false;
+    static constexpr const char* name = "mult_su3_mat_vec";
+    __device__ static void apply(const T* a, const T* b, T, T* c) { mat_vec<T>(a, b, c); }
+};
+template <typename T_>
+struct OpAdjMatVec {
+    using T = T_;
+    static constexpr int NA = 18, NB = 6, NC = 6;
+    static constexpr bool SCALAR = false;
+    static constexpr const char* name = "mult_adj_su3_mat_vec";
+    __device__ static void apply(const T* a, const T* b, T, T* c) { adj_mat_vec<T>(a, b, c); }
+};
+template <typename T_>
+struct OpNN {
+    using T = T_;
+    static constexpr int NA = 18, NB = 18, NC = 18;
+    static constexpr bool SCALAR = false;
+    static constexpr const char* name = "mult_su3_nn";
+    __device__ static void apply(const T* a, const T* b, T, T* c) { mat_nn<T>(a, b, c); }
+};
+template <typename T_>
+struct OpNA {
+    using T = T_;
+    static constexpr int NA = 18, NB = 18, NC = 18;
+    static constexpr bool SCALAR = false;
+    static constexpr const char* name = "mult_su3_na";
+    __device__ static void apply(const T* a, const T* b, T, T* c) { mat_na<T>(a, b, c); }
+};
+template <typename T_>
+struct OpAN {
+    using T = T_;
+    static constexpr int NA = 18, NB = 18, NC = 18;
+    static constexpr bool SCALAR = false;
+    static constexpr const char* name = "mult_su3_an";
+    __device__ static void apply(const T* a, const T* b, T, T* c) { mat_an<T>(a, b, c); }
+};
+template <typename T_>
+struct OpAdj4Dir {
+    using T = T_;
+    static constexpr int NA = 72, NB = 6, NC = 24;
+    static constexpr bool SCALAR = false;
+    static constexpr const char* name = "mult_adj_su3_mat_vec_4dir";
+    __device__ static void apply(const T* a, const T* b, T, T* c) { adj_mat_vec_4dir<T>(a, b, c); }
+};
+template <typename T_>
+struct OpSum4Dir {
+    using T = T_;
+    static constexpr int NA = 72, NB = 24, NC = 6;
+    static constexpr bool SCALAR = false;
+    static constexpr const char* name = "mult_su3_mat_vec_sum_4dir";
+    __device__ static void apply(const T* a, const T* b, T, T* c) { mat_vec_sum_4dir<T>(a, b, c); }
+};
+template <typename T_>
+struct OpSmadd {
+    using T = T_;
+    static constexpr int NA = 18, NB = 18, NC = 18;
+    static constexpr bool SCALAR = true;
+    static constexpr const char* name = "scalar_mult_add_su3_matrix";
+    __device__ static void apply(const T* a, const T* b, T s, T* c) { scalar_mult_add<T, 18>(a, b, s, c); }
+};
+
+// tile geometry per routine: ~12-24 KiB of operands per stage
+template <class Op>
+struct Geometry {
+    using T = typename Op::T;
+    static constexpr int IN_BYTES = (Op::NA + Op::NB + (Op::SCALAR ? 1 : 0)) * int(sizeof(T));
+    static constexpr int TS = IN_BYTES <= 160 ? 128 : (IN_BYTES <= 320 ? 64 : 32);
+    static constexpr int STAGES = 4;
+    static constexpr uint32_t A_BYTES = TS * Op::NA * sizeof(T);
+    static constexpr uint32_t B_BYTES = TS * Op::NB * sizeof(T);
+    static constexpr uint32_t S_BYTES = Op::SCALAR ? TS * sizeof(T) : 0;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES + S_BYTES;
+    static constexpr uint32_t C_BYTES = TS * Op::NC * sizeof(T);
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 2 * C_BYTES + STAGES * 8;
+    static_assert(A_BYTES % 16 == 0 && B_BYTES % 16 == 0 && S_BYTES % 16 == 0 && C_BYTES % 16 == 0, "bulk sizes");
+};
+
+// one site through global memory (tail / misaligned path); identical arithmetic
+template <class Op>
+__device__ __forceinline__ void site_direct(const typename Op::T* __restrict__ A, const typename Op::T* __restrict__ B,
+                                            const typename Op::T* __restrict__ S, typename Op::T s,
+                                            typename Op::T* __restrict__ C, int64_t x) {
+    using T = typename Op::T;
+    T a[Op::NA], b[Op::NB], c[Op::NC];
+#pragma unroll
+    for (int k = 0; k < Op::NA; ++k) a[k] = A[x * Op::NA + k];
+#pragma unroll
+    for (int k = 0; k < Op::NB; ++k) b[k] = B[x * Op::NB + k];
+    if (Op::SCALAR && S != nullptr) s = S[x];
+    Op::apply(a, b, s, c);
+#pragma unroll
+    for (int k = 0; k < Op::NC; ++k) C[x * Op::NC + k] = c[k];
+}
+
+template <class Op>
+__global__ void __launch_bounds__(Geometry<Op>::TS)
+    k_stream(const typename Op::T* __restrict__ A, const typename Op::T* __restrict__ B,
+             const typename Op::T* __restrict__ S, typename Op::T s_scalar, typename Op::T* __restrict__ C, int64_t n) {
+    using T = typename Op::T;
+    using G = Geometry<Op>;
+    constexpr int TS = G::TS, STAGES = G::STAGES;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* stages = smem;
+    T* obuf = reinterpret_cast<T*>(smem + STAGES * G::STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_BYTES + 2 * G::C_BYTES);
+
+    const int tid = threadIdx.x;
+    const int64_t ntiles = n / TS;
+    const bool has_s = Op::SCALAR && S != nullptr;
+    const uint32_t tx_bytes = G::A_BYTES + G::B_BYTES + (has_s ? G::S_BYTES : 0u);
+    const int64_t first = blockIdx.x, stride = gridDim.x;
+    const int64_t count = ntiles > first ? (ntiles - first + stride - 1) / stride : 0;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    uint64_t pol = 0;
+    if (tid == 0) pol = policy_evict_first();
+    auto issue = [&](int64_t tile, int st) {
+        unsigned char* base = stages + st * G::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[st], tx_bytes);
+        bulk_g2s(base, A + tile * TS * Op::NA, G::A_BYTES, &full[st], pol);
+        bulk_g2s(base + G::A_BYTES, B + tile * TS * Op::NB, G::B_BYTES, &full[st], pol);
+        if (has_s) bulk_g2s(base + G::A_BYTES + G::B_BYTES, S + tile * TS, G::S_BYTES, &full[st], pol);
+    };
+    if (tid == 0) {
+        for (int k = 0; k < STAGES && k < count; ++k) issue(first + k * stride, k);
+    }
+
+    for (int64_t k = 0; k < count; ++k) {
+        const int st = static_cast<int>(k % STAGES);
+        const uint32_t parity = static_cast<uint32_t>((k / STAGES) & 1);
+        const int64_t tile = first + k * stride;
+        mbar_wait(&full[st], parity);
+
+        const unsigned char* base = stages + st * G::STAGE_BYTES;
+        T a[Op::NA], b[Op::NB], c[Op::NC];
+        T s = s_scalar;
+        load_rec<Op::NA>(reinterpret_cast<const T*>(base) + tid * Op::NA, a);
+        load_rec<Op::NB>(reinterpret_cast<const T*>(base + G::A_BYTES) + tid * Op::NB, b);
+        if (has_s) s = reinterpret_cast<const T*>(base + G::A_BYTES + G::B_BYTES)[tid];
+
+        if (tid == 0) bulk_wait_read<1>();  // result buffer (k & 1) released by the store of tile k-2
+        __syncthreads();                     // stage st fully consumed; obuf (k & 1) free
+        if (tid == 0 && k + STAGES < count) issue(first + (k + STAGES) * stride, st);
+
+        Op::apply(a, b, s, c);
+        T* ob = obuf + (k & 1) * TS * Op::NC;
+        store_rec<Op::NC>(ob + tid * Op::NC, c);
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            bulk_s2g(C + tile * TS * Op::NC, ob, G::C_BYTES);
+            bulk_commit();
+        }
+    }
+
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t x = ntiles * TS + tid; x < n; x += TS) site_direct<Op>(A, B, S, s_scalar, C, x);
+    }
+    if (tid == 0) bulk_wait<0>();
+}
+
+template <class Op>
+__global__ void __launch_bounds__(256)
+    k_direct(const typename Op::T* __restrict__ A, const typename Op::T* __restrict__ B,
+             const typename Op::T* __restrict__ S, typename Op::T s_scalar, typename Op::T* __restrict__ C, int64_t n) {
+    for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < n; x += int64_t(gridDim.x) * blockDim.x)
+        site_direct<Op>(A, B, S, s_scalar, C, x);
+}
+
+template <class Op>
+struct LaunchCache {
+    int blocks_per_sm[64] = {0};
+};
+
+template <class Op>
+int launch(const typename Op::T* a, const typename Op::T* b, const typename Op::T* s_site, typename Op::T s,
+           typename Op::T* c, int64_t n, cudaStream_t stream) {
+    using G = Geometry<Op>;
+    if (n < 0) return fail_invalid(std::string(Op::name) + ": negative site count");
+    if (n == 0) return SU3G_OK;
+    if (a == nullptr || b == nullptr || c == nullptr) return fail_invalid(std::string(Op::name) + ": null pointer");
+    const DeviceInfo& di = device_info();
+    if (di.num_sms <= 0) return fail_invalid(std::string(Op::name) + ": no CUDA device");
+    const bool aligned = aligned16(a) && aligned16(b) && aligned16(c) && (s_site == nullptr || aligned16(s_site));
+    if (!aligned) {
+        const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(di.num_sms) * 8);
+        k_direct<Op><<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, b, s_site, s, c, n);
+        return check_launch(Op::name);
+    }
+    static LaunchCache<Op> cache;
+    int& per_sm = cache.blocks_per_sm[di.device & 63];
+    if (per_sm == 0) {
+        cudaFuncSetAttribute(k_stream<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM));
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_stream<Op>, G::TS, G::SMEM);
+        per_sm = std::max(b, 1);
+    }
+    const int64_t ntiles = n / G::TS;
+    int64_t grid = std::min<int64_t>(ntiles, int64_t(per_sm) * di.num_sms);
+    if (grid < 1) grid = 1;
+    k_stream<Op><<<static_cast<unsigned>(grid), G::TS, G::SMEM, stream>>>(a, b, s_site, s, c, n);
+    return check_launch(Op::name);
+}
+
+}  // namespace su3g
+
+using namespace su3g;
+
+#define SU3G_ROUTINE(NAME, OP)                                                                                      \
+    extern "C" int su3g_##NAME##_f32(const float* a, const float* b, float* c, int64_t n, su3g_stream_t st) {      \
+        return launch<OP<float>>(a, b, nullptr, 0.0f, c, n, reinterpret_cast<cudaStream_t>(st));                 \
+    }                                                                                                              \
+    extern "C" int su3g_##NAME##_f64(const double* a, const double* b, double* c, int64_t n, su3g_stream_t st) {   \
+        return launch<OP<double>>(a, b, nullptr, 0.0, c, n, reinterpret_cast<cudaStream_t>(st));                  \
+    }
+
+SU3G_ROUTINE(mult_su3_mat_vec, OpMatVec)
+SU3G_ROUTINE(mult_adj_su3_mat_vec, OpAdjMatVec)
+SU3G_ROUTINE(mult_su3_nn, OpNN)
+SU3G_ROUTINE(mult_su3_na, OpNA)
+SU3G_ROUTINE(mult_su3_an, OpAN)
+SU3G_ROUTINE(mult_adj_su3_mat_vec_4dir, OpAdj4Dir)
+SU3G_ROUTINE(mult_su3_mat_vec_sum_4dir, OpSum4Dir)
+
+extern "C" int su3g_scalar_mult_add_su3_matrix_f32(const float* a, const float* b, float s, const float* s_site,
+                                                   float* c, int64_t n, su3g_stream_t st) {
+    return launch<OpSmadd<float>>(a, b, s_site, s, c, n, reinterpret_cast<cudaStream_t>(st));
+}
+extern "C" int su3g_scalar_mult_add_su3_matrix_f64(const double* a, const double* b, double s, const double* s_site,
+                                                   double* c, int64_t n, su3g_stream_t st) {
+    return launch<OpSmadd<double>>(a, b, s_site, s, c, n, reinterpret_cast<cudaStream_t>(st));
+}

@@ -1,0 +1,252 @@
+"""Drop-in SU(3) routines backed by the sm_100a kernels of libsu3g.
+
+Each function keeps the reference signature and semantics of su3bench's
+vector backend (simd.py:80-230):
+
+    fn(a, b, out=None)                      -> result
+    scalar_mult_add_su3_matrix(a, b, s, out=None)
+
+* operands carry any shared leading batch shape in front of the per-object
+  shape (simd.py:59-68); a wrong per-object shape or disagreeing batch shapes
+  raise ValueError, as does an ``out`` of the wrong shape (simd.py:51-56);
+* the result lands in ``out`` when given (and ``out`` is returned), else in a
+  fresh array of the operands' dtype;
+* inputs are never modified;
+* numpy operands (what the reference harness passes, verify.py:67-70) are
+  copied to the GPU and the result copied back as numpy; CUDA torch tensors
+  stay on the device and the kernel runs on the current torch stream;
+  complex64/complex128 inputs are accepted as pair views.
+
+Deliberate tightening (documented in DESIGN.md): operands of different
+precisions raise ValueError instead of being silently promoted.
+
+There is no CPU fallback: without libsu3g.so or a CUDA device every call raises.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib, validation
+from .types import OPERAND_SHAPES, ROUTINE_NAMES, batch_count, routine_spec
+
+_TORCH_REAL = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+_SFX = {torch.float32: "f32", torch.float64: "f64"}
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1309_0551_b200 needs a CUDA device (B200, sm_100a); there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+class _Arg:
+    """One array operand normalised to a contiguous real-pair device tensor."""
+
+    __slots__ = ("src", "kind", "is_torch", "is_complex", "dev", "shape", "rdtype")
+
+    def __init__(self, src, kind: str):
+        self.src = src
+        self.kind = kind
+        self.is_torch = isinstance(src, torch.Tensor)
+        if self.is_torch:
+            t = src
+            self.is_complex = t.is_complex()
+            if self.is_complex:
+                t = torch.view_as_real(t.resolve_conj())
+            if t.dtype not in _SFX:
+                raise ValueError(f"unsupported dtype {t.dtype}; expected float32/float64 (or complex64/complex128)")
+            self.rdtype = t.dtype
+            self.shape = tuple(t.shape)
+            self.dev = t
+        else:
+            a = np.asarray(src)
+            self.is_complex = np.iscomplexobj(a)
+            if self.is_complex:
+                a = np.stack([a.real, a.imag], axis=-1)
+            if a.dtype not in _TORCH_REAL:
+                raise ValueError(f"unsupported dtype {a.dtype}; expected float32/float64 (or complex64/complex128)")
+            self.rdtype = _TORCH_REAL[a.dtype]
+            self.shape = a.shape
+            self.dev = a  # moved to the device after validation
+
+    def to_device(self, device) -> torch.Tensor:
+        if self.is_torch:
+            t = self.dev
+            if t.device != device:
+                t = t.to(device)
+            self.dev = t.contiguous()
+        else:
+            self.dev = torch.from_numpy(np.ascontiguousarray(self.dev)).to(device)
+        return self.dev
+
+
+def _check_shapes(name: str, args) -> tuple:
+    prefixes = set()
+    for label, arg in args:
+        obj = OPERAND_SHAPES[arg.kind]
+        nd = len(obj)
+        if len(arg.shape) < nd or tuple(arg.shape[len(arg.shape) - nd:]) != obj:
+            raise ValueError(f"{name}: operand {label} has shape {arg.shape}, expected (...,) + {obj}")
+        prefixes.add(tuple(arg.shape[: len(arg.shape) - nd]))
+    if len(prefixes) > 1:
+        raise ValueError(f"{name}: operands disagree on batch shape: {sorted(prefixes)}")
+    return prefixes.pop()
+
+
+def _run(name: str, labelled, result_kind: str, like: "_Arg", out, scalar=None):
+    """Validate, stage, launch and deliver one routine call."""
+    spec = routine_spec(name)
+    args = [_Arg(x, kind) for (x, kind) in labelled]
+    prefix = _check_shapes(name, list(zip("ab", args)))
+    rdtype = args[0].rdtype
+    for arg in args[1:]:
+        if arg.rdtype != rdtype:
+            raise ValueError(f"{name}: operands mix {rdtype} and {arg.rdtype}; pass one precision")
+    result_shape = prefix + OPERAND_SHAPES[result_kind]
+    if out is not None:
+        out_shape = tuple(out.shape)
+        if isinstance(out, torch.Tensor) and out.is_complex():
+            out_shape = out_shape + (2,)
+        elif isinstance(out, np.ndarray) and np.iscomplexobj(out):
+            out_shape = out_shape + (2,)
+        if out_shape != result_shape:
+            raise ValueError(f"result array has shape {tuple(out.shape)}, expected {result_shape}")
+    validation.check_no_alias(out, *(a.src for a in args))
+
+    device = _device()
+    n = int(np.prod(prefix, dtype=np.int64)) if prefix else 1
+    devs = [arg.to_device(device) for arg in args]
+    sfx = _SFX[rdtype]
+
+    # destination: write straight into a contiguous CUDA `out`, else a scratch tensor
+    direct = (
+        isinstance(out, torch.Tensor)
+        and out.is_cuda
+        and out.device == device
+        and not out.is_complex()
+        and out.dtype == rdtype
+        and out.is_contiguous()
+    )
+    dst = out if direct else torch.empty(result_shape, dtype=rdtype, device=device)
+
+    stream = _stream()
+    if n > 0:
+        if spec.name == "scalar_mult_add_su3_matrix":
+            s_scalar, s_site = scalar
+            _lib.call(
+                f"su3g_scalar_mult_add_su3_matrix_{sfx}",
+                devs[0].data_ptr(), devs[1].data_ptr(), s_scalar,
+                None if s_site is None else s_site.data_ptr(), dst.data_ptr(), n, stream,
+            )
+        else:
+            _lib.call(f"su3g_{spec.name}_{sfx}", devs[0].data_ptr(), devs[1].data_ptr(), dst.data_ptr(), n, stream)
+
+    return _deliver(dst, out, like, direct)
+
+
+def _deliver(dst: torch.Tensor, out, like: "_Arg", direct: bool):
+    if out is not None:
+        if direct:
+            return out
+        if isinstance(out, torch.Tensor):
+            if out.is_complex():
+                out.copy_(torch.view_as_complex(dst))
+            else:
+                out.copy_(dst)
+            return out
+        host = dst.cpu().numpy()
+        if np.iscomplexobj(out):
+            out[...] = host[..., 0] + 1j * host[..., 1]
+        else:
+            out[...] = host
+        return out
+    if like.is_torch:
+        res = dst if like.src.is_cuda else dst.cpu()
+        return torch.view_as_complex(res) if like.is_complex else res
+    host = dst.cpu().numpy()
+    if like.is_complex:
+        return host[..., 0] + 1j * host[..., 1]
+    return host
+
+
+def _scalar_operand(s, rdtype, prefix, device):
+    """(host scalar, per-site device tensor or None) -- s cast to the operand dtype (simd.py:217-221)."""
+    if isinstance(s, torch.Tensor):
+        s_arr = s.detach().to(torch.float64 if rdtype == torch.float64 else torch.float32)
+        if s_arr.ndim == 0:
+            return float(s_arr.item()), None
+        s_dev = s_arr.to(device).expand(prefix).contiguous().reshape(-1)
+        return 0.0, s_dev
+    np_dt = np.float64 if rdtype == torch.float64 else np.float32
+    s_arr = np.asarray(s, dtype=np_dt)
+    if s_arr.ndim == 0:
+        return float(s_arr), None
+    s_arr = np.broadcast_to(s_arr, prefix)
+    return 0.0, torch.from_numpy(np.ascontiguousarray(s_arr).reshape(-1)).to(device)
+
+
+def _make(name: str):
+    spec = routine_spec(name)
+    kinds = spec.operands
+    # the reference allocates its result like operand b for mat-vec families, a for mat-mat
+    like_index = 1 if spec.result in ("vec", "vec4") else 0
+
+    def routine(a, b, out=None):
+        labelled = [(a, kinds[0]), (b, kinds[1])]
+        probe = [_Arg(a, kinds[0]), _Arg(b, kinds[1])]
+        return _run(name, labelled, spec.result, probe[like_index], out)
+
+    routine.__name__ = name
+    routine.__qualname__ = name
+    routine.__doc__ = f"Drop-in for su3bench.simd.{name} on the B200 (libsu3g su3g_{name}_f32/_f64)."
+    return routine
+
+
+mult_su3_mat_vec = _make("mult_su3_mat_vec")
+mult_adj_su3_mat_vec = _make("mult_adj_su3_mat_vec")
+mult_su3_nn = _make("mult_su3_nn")
+mult_su3_na = _make("mult_su3_na")
+mult_su3_an = _make("mult_su3_an")
+mult_adj_su3_mat_vec_4dir = _make("mult_adj_su3_mat_vec_4dir")
+mult_su3_mat_vec_sum_4dir = _make("mult_su3_mat_vec_sum_4dir")
+
+
+def scalar_mult_add_su3_matrix(a, b, s, out=None):
+    """c = a + s*b for real s, 0-d or per-site (drop-in for su3bench.simd.scalar_mult_add_su3_matrix)."""
+    name = "scalar_mult_add_su3_matrix"
+    probe_a = _Arg(a, "mat")
+    prefix = tuple(probe_a.shape[:-3]) if len(probe_a.shape) >= 3 else ()
+    device = _device()
+    scalar = _scalar_operand(s, probe_a.rdtype, prefix, device)
+    return _run(name, [(a, "mat"), (b, "mat")], "mat", probe_a, out, scalar=scalar)
+
+
+KERNELS = {
+    "mult_adj_su3_mat_vec": mult_adj_su3_mat_vec,
+    "mult_adj_su3_mat_vec_4dir": mult_adj_su3_mat_vec_4dir,
+    "mult_su3_an": mult_su3_an,
+    "mult_su3_na": mult_su3_na,
+    "mult_su3_nn": mult_su3_nn,
+    "mult_su3_mat_vec": mult_su3_mat_vec,
+    "mult_su3_mat_vec_sum_4dir": mult_su3_mat_vec_sum_4dir,
+    "scalar_mult_add_su3_matrix": scalar_mult_add_su3_matrix,
+}
+assert set(KERNELS) == set(ROUTINE_NAMES)
+
+
+def apply(routine: str, *operands, out=None):
+    """Invoke one kernel by name on a single operand set (simd.py:281-287)."""
+    routine_spec(routine)
+    return KERNELS[routine](*operands, out=out)
+
+
+def batch_apply(routine: str, operands, count: int | None = None, out=None):
+    """Apply one kernel to `count` stacked operand sets in one launch (simd.py:304-314)."""
+    spec = routine_spec(routine)
+    batch_count(spec, operands, count)
+    return KERNELS[routine](*operands, out=out)

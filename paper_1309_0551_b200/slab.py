@@ -1,0 +1,126 @@
+"""t-slab domain decomposition of the NN sweep across GPUs (BASELINE configs[4]).
+
+The global lattice nx*ny*nz*nt is cut along t into G equal slabs, one per
+rank (one process per GPU, torch.distributed over NCCL).  A fixed-t slice is
+a contiguous block of sites in the reference numbering (lattice.py:3-6), so a
+rank's fields are contiguous sub-arrays and its t-faces are contiguous SoA
+blocks.
+
+Per application of D, rank r needs two one-site halos:
+  * v on the first t-slice of rank r+1  (forward +t term of its last slice);
+  * w = U_t(x)^dag v(x) on the last t-slice of rank r-1 (backward -t term of
+    its first slice).  The owner computes w with the same arithmetic the
+    unsharded kernel uses, so the sharded result is BIT-IDENTICAL to the
+    single-GPU sweep; 6 reals cross the link per face site instead of 24.
+
+Schedule per application (compute stream C, NCCL's stream N):
+  C: pack w_last                        (su3g_nn_halo_w)
+  N: send v_first -> r-1, recv v_hi <- r+1, send w_last -> r+1, recv w_lo <- r-1
+  C: interior slices t in [1, nt_local-1)    -- overlaps the exchange
+  C: wait(N); boundary slices t = 0 and t = nt_local-1
+
+The compute is pluggable (``kernels``) so the exchange logic can be exercised
+on CPU ranks over gloo in the tests; the product default is the CUDA kernels.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import sweeps
+from .lattice import Field
+
+TAG_V = 11
+TAG_W = 12
+
+
+class CudaSlabKernels:
+    """Device compute for one slab: libsu3g kernels on t-sliced SoA fields."""
+
+    def alloc_face(self, v: Field) -> torch.Tensor:
+        return torch.empty((6, v.lattice.slice_sites), dtype=v.dtype, device=v.device)
+
+    def first_face(self, v: Field) -> torch.Tensor:
+        return v.face(0)
+
+    def halo_w(self, U: Field, v: Field, w: torch.Tensor) -> None:
+        sweeps.nn_halo_w(U, v, w)
+
+    def sweep(self, U: Field, v: Field, out: Field, t_range, v_hi, w_lo) -> None:
+        sweeps.nn_sweep(U, v, out=out, t_range=t_range, v_hi=v_hi, w_lo=w_lo)
+
+    def nt(self, v: Field) -> int:
+        return v.lattice.nt
+
+
+def boundary_ranges(nt_local: int):
+    """(interior range, boundary ranges) of local t-slices; halos only touch the boundary."""
+    if nt_local <= 2:
+        return None, [(t, t + 1) for t in range(nt_local)]
+    return (1, nt_local - 1), [(0, 1), (nt_local - 1, nt_local)]
+
+
+class SlabSweep:
+    """Applies D on this rank's t-slab, exchanging halos with the t-neighbour ranks."""
+
+    def __init__(self, U, kernels=None, group=None):
+        self.U = U
+        self.k = kernels if kernels is not None else CudaSlabKernels()
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(group)
+            self.world = dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        self._faces = None
+
+    @property
+    def up(self) -> int:
+        return (self.rank + 1) % self.world
+
+    @property
+    def down(self) -> int:
+        return (self.rank - 1) % self.world
+
+    def _buffers(self, v):
+        if self._faces is None:
+            self._faces = (self.k.alloc_face(v), self.k.alloc_face(v), self.k.alloc_face(v))
+        return self._faces
+
+    def _peer(self, r: int) -> int:
+        return r if self.group is None else dist.get_global_rank(self.group, r)
+
+    def exchange(self, v, w_send, v_hi, w_lo):
+        """Post the four halo transfers; returns the pending requests."""
+        ops = [
+            dist.P2POp(dist.isend, self.k.first_face(v), self._peer(self.down), self.group, TAG_V),
+            dist.P2POp(dist.irecv, v_hi, self._peer(self.up), self.group, TAG_V),
+            dist.P2POp(dist.isend, w_send, self._peer(self.up), self.group, TAG_W),
+            dist.P2POp(dist.irecv, w_lo, self._peer(self.down), self.group, TAG_W),
+        ]
+        return dist.batch_isend_irecv(ops)
+
+    def apply(self, v, out):
+        """out = D v on this slab (periodic in t across the ranks)."""
+        if self.world == 1:
+            self.k.sweep(self.U, v, out, (0, self.k.nt(v)), None, None)
+            return out
+        w_send, v_hi, w_lo = self._buffers(v)
+        self.k.halo_w(self.U, v, w_send)
+        reqs = self.exchange(v, w_send, v_hi, w_lo)
+        interior, edges = boundary_ranges(self.k.nt(v))
+        if interior is not None:
+            self.k.sweep(self.U, v, out, interior, v_hi, w_lo)
+        for r in reqs:
+            r.wait()
+        for rng in edges:
+            self.k.sweep(self.U, v, out, rng, v_hi, w_lo)
+        return out
+
+    def apply_n(self, v, scratch, applications: int):
+        """v <- D v `applications` times (ping-pong); returns the buffer holding the result."""
+        a, b = v, scratch
+        for _ in range(applications):
+            self.apply(a, b)
+            a, b = b, a
+        return a

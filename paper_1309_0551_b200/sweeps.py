@@ -1,0 +1,117 @@
+"""Lattice sweeps on device-resident fields (BASELINE configs[2]-[4]).
+
+* ``nn_sweep``      out = D v, D the periodic nearest-neighbour operator
+                    out(x) = sum_mu U_mu(x) v(x+mu) - U_mu(x-mu)^dag v(x-mu)
+                    (SURVEY.md 8(a) a13), bit-identical to the composition of
+                    the reference routines in the order of SURVEY.md 8(c).
+* ``nn_apply``      v <- D v repeated (configs[4]: 10 applications).
+* ``link_product``  acc = sum_planes s U_mu U_nu(x+mu) U_mu(x+nu)^dag (a14).
+
+The reference has no sweep routine; these are built from its
+per-site routines' arithmetic.  ``*_aos`` helpers take/return the reference
+AoS layout for callers that hold su3bench-style arrays.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .lattice import Field, Lattice4D
+
+_SFX = {torch.float32: "f32", torch.float64: "f64"}
+MODES = {"exact": _lib.SU3G_EXACT, "fma": _lib.SU3G_FMA}
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=None, w_lo=None) -> Field:
+    """One application of D on the slices t in t_range (default: all).
+
+    v_hi / w_lo: (6, F) SoA halo faces for a t-slab (see include/su3g.h); None
+    closes t periodically on the local lattice.
+    """
+    if U.kind != "mat4" or v.kind != "vec":
+        raise ValueError("nn_sweep needs U of kind 'mat4' and v of kind 'vec'")
+    if U.lattice != v.lattice or U.dtype != v.dtype:
+        raise ValueError("U and v must share lattice and dtype")
+    if out is None:
+        out = v.empty_like()
+    lat = U.lattice
+    t0, t1 = (0, lat.nt) if t_range is None else t_range
+    _lib.call(
+        f"su3g_nn_sweep_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
+        lat.nx, lat.ny, lat.nz, lat.nt, t0, t1, _ptr(v_hi), _ptr(w_lo), _stream(U.device),
+    )
+    return out
+
+
+def nn_halo_w(U: Field, v: Field, w_face: torch.Tensor) -> torch.Tensor:
+    """w = U_t^dag v on the last local t-slice -> (6, F) SoA face (sent to the +t neighbour)."""
+    lat = U.lattice
+    _lib.call(
+        f"su3g_nn_halo_w_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), w_face.data_ptr(),
+        lat.nx, lat.ny, lat.nz, lat.nt, _stream(U.device),
+    )
+    return w_face
+
+
+def nn_apply(U: Field, v: Field, applications: int, scratch: Field | None = None) -> Field:
+    """v <- D v, `applications` times, ping-ponging between two buffers; returns the final field."""
+    a = v
+    b = scratch if scratch is not None else v.empty_like()
+    for _ in range(applications):
+        nn_sweep(U, a, out=b)
+        a, b = b, a
+    return a
+
+
+def link_product(U: Field, s: float = 1.0 / 6.0, mode: str = "exact", out: Field | None = None) -> Field:
+    if U.kind != "mat4":
+        raise ValueError("link_product needs U of kind 'mat4'")
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {sorted(MODES)}")
+    lat = U.lattice
+    if out is None:
+        out = Field(lat, "mat", U.dtype, U.device)
+    _lib.call(
+        f"su3g_link_product_{_SFX[U.dtype]}", U.data.data_ptr(), out.data.data_ptr(),
+        lat.nx, lat.ny, lat.nz, lat.nt, float(np.dtype(np.float32 if U.dtype == torch.float32 else np.float64).type(s)),
+        MODES[mode], _stream(U.device),
+    )
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference-layout convenience wrappers
+# ---------------------------------------------------------------------------
+
+def _family(x):
+    return "torch" if isinstance(x, torch.Tensor) else "numpy"
+
+
+def _back(t: torch.Tensor, like):
+    if _family(like) == "numpy":
+        return t.cpu().numpy()
+    return t if like.is_cuda else t.cpu()
+
+
+def nn_sweep_aos(U, v, dims, applications: int = 1):
+    """D^applications v for reference-layout U (V,4,3,3,2) and v (V,3,2); returns v's array family."""
+    lat = Lattice4D.from_dims(dims)
+    Uf = Field.from_aos(lat, "mat4", U)
+    vf = Field.from_aos(lat, "vec", v)
+    res = nn_apply(Uf, vf, applications)
+    return _back(res.to_aos(), v)
+
+
+def link_product_aos(U, dims, s: float = 1.0 / 6.0, mode: str = "exact"):
+    lat = Lattice4D.from_dims(dims)
+    Uf = Field.from_aos(lat, "mat4", U)
+    return _back(link_product(Uf, s, mode).to_aos(), U)

@@ -1,0 +1,163 @@
+"""Host-side tests that need no GPU: the C ABI library, the registry, shapes, errors."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1309_0551_b200 import _lib, lattice, types, validation
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "su3g.h")).read()
+    return sorted(set(re.findall(r"SU3G_API[^;(]*?\b(su3g_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_full_abi():
+    syms = header_symbols()
+    for r in _lib.HOT_ROUTINES + ("scalar_mult_add_su3_matrix",):
+        for sfx in ("f32", "f64"):
+            assert f"su3g_{r}_{sfx}" in syms
+    assert "su3g_nn_sweep_f32" in syms and "su3g_link_product_f64" in syms
+    assert len(syms) == len(_lib.SIGNATURES)
+    assert set(syms) == set(_lib.SIGNATURES)
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    lib = _lib.load()
+    for name in header_symbols():
+        assert isinstance(getattr(lib, name), ctypes._CFuncPtr), name
+    assert lib.su3g_abi_version() == 1
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_invalid_arguments_rejected_without_touching_the_device():
+    lib = _lib.load()
+    # negative site count, null pointers -> SU3G_EINVAL before any CUDA call
+    assert lib.su3g_mult_su3_mat_vec_f32(None, None, None, -1, None) == _lib.SU3G_EINVAL
+    assert b"negative" in lib.su3g_last_error()
+    assert lib.su3g_nn_sweep_f32(None, None, None, 0, 4, 4, 4, 0, 4, None, None, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_link_product_f64(None, None, 4, 4, 4, 4, 0.5, 7, None) == _lib.SU3G_EINVAL
+    with pytest.raises(ValueError):
+        _lib.check(_lib.SU3G_EINVAL, "x")
+    # zero sites is a valid no-op
+    assert lib.su3g_mult_su3_nn_f64(None, None, None, 0, None) == _lib.SU3G_OK
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_no_cpu_fallback():
+    from paper_1309_0551_b200 import kernels
+
+    a = np.zeros((2, 3, 3, 2), np.float32)
+    b = np.zeros((2, 3, 2), np.float32)
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        kernels.mult_su3_mat_vec(a, b)
+
+
+def test_shape_errors_match_reference_conventions():
+    from paper_1309_0551_b200 import kernels
+
+    a = np.zeros((4, 3, 3, 2), np.float32)
+    b = np.zeros((4, 3, 2), np.float32)
+    with pytest.raises(ValueError):
+        kernels.mult_su3_mat_vec(b, b)  # wrong per-object shape
+    with pytest.raises(ValueError):
+        kernels.mult_su3_nn(a, b)
+    with pytest.raises(ValueError):
+        kernels.mult_su3_mat_vec(a, b[:3])  # batch shapes disagree
+    with pytest.raises(ValueError):
+        kernels.mult_su3_mat_vec(a, b.astype(np.float64))  # mixed precision (deliberate tightening)
+    with pytest.raises(ValueError):
+        kernels.mult_su3_mat_vec(a, b, out=np.zeros((4, 3, 3, 2), np.float32))
+    with pytest.raises(ValueError):
+        kernels.apply("mult_su3_zz", a, b)
+    with pytest.raises(ValueError):
+        kernels.batch_apply("mult_su3_nn", [a, a[:3]])
+    with pytest.raises(ValueError):
+        kernels.batch_apply("mult_su3_nn", [a, a], count=9)
+
+
+def test_alias_check_under_debug_validation():
+    from paper_1309_0551_b200 import kernels
+
+    a = np.zeros((4, 3, 3, 2), np.float32)
+    b = np.zeros((4, 3, 2), np.float32)
+    validation.debug_validation(True)
+    try:
+        with pytest.raises(ValueError, match="aliases"):
+            kernels.mult_su3_mat_vec(a, b, out=b)
+        t = torch.zeros(10)
+        with pytest.raises(ValueError, match="aliases"):
+            validation.check_no_alias(t[2:6], t[4:8])
+        validation.check_no_alias(t[0:4], t[4:8])
+    finally:
+        validation.debug_validation(False)
+
+
+def test_registry_and_batch_count():
+    assert set(types.ROUTINE_NAMES) == set(_lib.HOT_ROUTINES) | {"scalar_mult_add_su3_matrix"}
+    spec = types.routine_spec("scalar_mult_add_su3_matrix")
+    a = np.zeros((5, 3, 3, 2))
+    assert types.batch_count(spec, [a, a, 0.5]) == 5
+    assert types.batch_count(spec, [a, a, np.zeros(5)]) == 5
+    assert types.batch_count(types.routine_spec("mult_su3_nn"), [a[:0], a[:0]]) == 0
+    with pytest.raises(ValueError):
+        types.routine_spec("nope")
+    assert types.dtype_for("single") == np.float32
+    with pytest.raises(ValueError):
+        types.dtype_for(np.int32)
+
+
+def test_lattice_matches_reference_numbering():
+    lat = lattice.Lattice4D(4, 4, 4, 4)
+    assert lat.site_index((1, 0, 0, 0)) == 1
+    assert lat.site_index((0, 1, 0, 0)) == 4
+    assert lat.site_index((0, 0, 1, 0)) == 16
+    assert lat.site_index((0, 0, 0, 1)) == 64
+    assert lat.neighbor(lat.site_index((3, 0, 0, 0)), "+x") == 0
+    assert lat.neighbor(0, "-t") == lat.site_index((0, 0, 0, 3))
+    lat2 = lattice.Lattice4D(2, 3, 4, 5)
+    for s in range(lat2.volume):
+        assert lat2.site_index(lat2.site_coord(s)) == s
+        for d in lattice.DIRECTIONS:
+            opp = ("-" if d[0] == "+" else "+") + d[1]
+            assert lat2.neighbor(lat2.neighbor(s, d), opp) == s
+    assert lattice.Lattice4D(8, 8, 8, 16).slab(4, 1).dims == (8, 8, 8, 4)
+    with pytest.raises(ValueError):
+        lattice.Lattice4D(8, 8, 8, 6).slab(4, 0)
+    with pytest.raises(ValueError):
+        lattice.Lattice4D(0, 1, 1, 1)
+
+
+def test_lattice_numbering_agrees_with_oracle_shift():
+    from oracle import sweeps as S
+
+    dims = (3, 4, 5, 6)
+    lat = lattice.Lattice4D(*dims)
+    idx = np.arange(lat.volume).reshape(-1, 1)
+    for mu, axis in enumerate("xyzt"):
+        up = S.shift(idx, dims, mu, +1)[:, 0]
+        assert all(up[s] == lat.neighbor(s, "+" + axis) for s in range(0, lat.volume, 7))
+
+
+def test_input_generators_are_special_unitary():
+    from paper_1309_0551_b200 import inputs
+
+    U = inputs.random_links(inputs.config_rng(1), 300, 4)
+    u = U[..., 0] + 1j * U[..., 1]
+    eye = np.einsum("...ij,...kj->...ik", u, u.conj())
+    assert np.abs(eye - np.eye(3)).max() < 1e-13
+    assert np.abs(np.linalg.det(u) - 1).max() < 1e-13
+    # deterministic per seed
+    a = inputs.random_vectors(np.random.default_rng(5), 10, None)
+    b = inputs.random_vectors(np.random.default_rng(5), 10, None)
+    assert np.array_equal(a, b)
