@@ -52,6 +52,10 @@ SU3G_API const char *su3g_last_error(void);
 /* number of SMs / L2 bytes of the current device (0 on failure) */
 SU3G_API int su3g_device_sm_count(void);
 SU3G_API int64_t su3g_device_l2_bytes(void);
+/* process-wide tuning/debug knobs (not needed for normal use):
+ *   "nn_variant": 0 = auto (t-walk kernel when the lattice allows, else generic),
+ *                 1 = always the generic one-thread-per-site kernel, 2 = require the t-walk kernel */
+SU3G_API int su3g_set_option(const char *name, int64_t value);
 
 /* ---- per-site routines (8 hot routines x {f32, f64}) ---------------------
  * c = routine(a, b) for every site.                                            */
@@ -92,7 +96,7 @@ SU3G_API int su3g_scalar_mult_add_su3_matrix_f64(const double *a, const double *
  *     soa[(t * reals_per_site + c) * sites_per_slice + s3]
  * where a slice is one fixed-t block of sites_per_slice = nx*ny*nz sites (a
  * t-face is contiguous in the reference numbering, lattice.py:3-6).
- * nslices = 1 gives plain SoA.  reals_per_site <= 72.                        */
+ * nslices = 1 gives plain SoA.  reals_per_site in {2, 6, 12, 18, 24, 72}.                        */
 SU3G_API int su3g_aos_to_soa_f32(const float *aos, float *soa, int64_t sites_per_slice, int64_t nslices, int32_t reals_per_site,
                         su3g_stream_t stream);
 SU3G_API int su3g_aos_to_soa_f64(const double *aos, double *soa, int64_t sites_per_slice, int64_t nslices,

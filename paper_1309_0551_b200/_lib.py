@@ -41,6 +41,7 @@ def _signatures():
         "su3g_last_error": ([], ctypes.c_char_p),
         "su3g_device_sm_count": ([], ctypes.c_int),
         "su3g_device_l2_bytes": ([], ctypes.c_int64),
+        "su3g_set_option": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
     }
     for sfx, real in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
         for r in HOT_ROUTINES:
@@ -94,3 +95,7 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def set_option(name: str, value: int) -> None:
+    call("su3g_set_option", name.encode(), int(value))

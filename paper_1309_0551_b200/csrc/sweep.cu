@@ -9,6 +9,8 @@
 //
 // Field layout (layout.cu): f[(t * C + c) * F + s3], F = nx*ny*nz.
 #include <algorithm>
+#include <atomic>
+#include <cstring>
 
 #include "su3_math.cuh"
 
@@ -159,6 +161,232 @@ __global__ void __launch_bounds__(128)
     for (int k = 0; k < 18; ++k) acc_out[(int64_t(t) * 18 + k) * g.F + s3] = acc[k];
 }
 
+
+// ---------------------------------------------------------------------------
+// NN sweep, t-walk kernel (the fast path)
+//
+// A CTA owns a block of one t-slice, full x extent (x periodic inside the CTA)
+// times BY x BZ rows, one thread per (x, y, z) column, and walks t.  Per step:
+//   * each thread streams its own links U_mu(x,t) (72 reals, coalesced SoA)
+//     and v(x,t+1) from HBM -- the only compulsory traffic;
+//   * it forms the backward half-products w_mu(x) = U_mu(x)^dag v(x) for
+//     mu = x, y, z and publishes them with v(x) in shared memory, so every
+//     backward neighbour term is read from on-chip memory instead of
+//     re-fetching the neighbour's 18-real link;
+//   * w_t(x,t) stays in registers and is the -t term of step t+1; v(x,t+1)
+//     becomes v(x,t) of the next step -- t-neighbours never leave the SM;
+//   * y/z neighbours outside the block (halo rows) come from L2.
+// Work = (blocks x slices) steps split evenly over persistent CTAs; a CTA
+// crossing into a new block reloads the one-slice prologue.
+// The per-site arithmetic (and its order) is exactly that of k_nn_sweep, so
+// both paths -- and the composed reference -- agree bit for bit.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct WalkParams {
+    const T* __restrict__ U;
+    const T* __restrict__ v;
+    T* __restrict__ out;
+    const T* __restrict__ v_hi;
+    const T* __restrict__ w_lo;
+    int nx, ny, nz, nt;
+    int64_t F;
+    int BY, BZ, nby;
+    int t_begin, t_end;
+    int64_t total;  // blocks * (t_end - t_begin)
+};
+
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p, uint64_t pol) {
+    T r;
+    if constexpr (sizeof(T) == 4) {
+        float f;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(f) : "l"(p), "l"(pol));
+        r = f;
+    } else {
+        double d;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(d) : "l"(p), "l"(pol));
+        r = d;
+    }
+    return r;
+}
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw);
+    const int nthr = blockDim.x;
+    const int tid = threadIdx.x;
+    const int nx = p.nx;
+    const int lx = tid % nx;
+    const int rr = tid / nx;
+    const int ly = rr % p.BY;
+    const int lz = rr / p.BY;
+    const int64_t F = p.F;
+    const int steps = p.t_end - p.t_begin;
+
+    // in-block neighbour threads for the backward exchange (-1: halo row, via L2)
+    const int tx_dn = (lx == 0) ? tid + nx - 1 : tid - 1;
+    const int sy = nx, sz = nx * p.BY;
+    const int ty_dn = (ly > 0) ? tid - sy : (p.BY == p.ny ? tid + (p.BY - 1) * sy : -1);
+    const int tz_dn = (lz > 0) ? tid - sz : (p.BZ == p.nz ? tid + (p.BZ - 1) * sz : -1);
+
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+
+    const int64_t w0 = p.total * blockIdx.x / gridDim.x;
+    const int64_t w1 = p.total * (blockIdx.x + 1) / gridDim.x;
+
+    T vc[6], wt[6];
+    int64_t cur = -1;
+    int64_t s3 = 0, s3_up[3] = {0, 0, 0}, s3_ydn = 0, s3_zdn = 0;
+    int buf = 0;
+    for (int64_t w = w0; w < w1; ++w) {
+        const int64_t blk = w / steps;
+        const int t = p.t_begin + static_cast<int>(w - blk * steps);
+        if (blk != cur) {  // prologue: v(x,t) and the -t half-product w_t(x,t-1)
+            cur = blk;
+            const int y = static_cast<int>(blk % p.nby) * p.BY + ly;
+            const int z = static_cast<int>(blk / p.nby) * p.BZ + lz;
+            s3 = lx + int64_t(nx) * (y + int64_t(p.ny) * z);
+            s3_up[0] = (lx + 1) % nx + int64_t(nx) * (y + int64_t(p.ny) * z);
+            s3_up[1] = lx + int64_t(nx) * ((y + 1) % p.ny + int64_t(p.ny) * z);
+            s3_up[2] = lx + int64_t(nx) * (y + int64_t(p.ny) * ((z + 1) % p.nz));
+            s3_ydn = lx + int64_t(nx) * ((y + p.ny - 1) % p.ny + int64_t(p.ny) * z);
+            s3_zdn = lx + int64_t(nx) * (y + int64_t(p.ny) * ((z + p.nz - 1) % p.nz));
+            ld_soa<T, 6>(p.v + int64_t(t) * 6 * F, F, s3, vc);
+            if (t == 0 && p.w_lo != nullptr) {
+                ld_soa<T, 6>(p.w_lo, F, s3, wt);
+            } else {
+                const int tp = (t > 0) ? t - 1 : p.nt - 1;
+                T u[18], vp[6];
+                ld_soa<T, 18>(p.U + (int64_t(tp) * 72 + 54) * F, F, s3, u);
+                ld_soa<T, 6>(p.v + int64_t(tp) * 6 * F, F, s3, vp);
+                adj_mat_vec<T>(u, vp, wt);
+            }
+        }
+        T vn[6];
+        if (t + 1 < p.nt) ld_soa<T, 6>(p.v + int64_t(t + 1) * 6 * F, F, s3, vn);
+        else if (p.v_hi != nullptr) ld_soa<T, 6>(p.v_hi, F, s3, vn);
+        else ld_soa<T, 6>(p.v, F, s3, vn);
+
+        // ---- per direction: stream U_mu(x,t) once; publish w_mu; forward term ----
+        T* sb = sm + buf * 18 * nthr;
+        const T* Ut = p.U + int64_t(t) * 72 * F + s3;
+        const T* vt = p.v + int64_t(t) * 6 * F;
+        T acc[6], wt_next[6];
+#pragma unroll
+        for (int mu = 0; mu < 4; ++mu) {
+            T u[18], nb[6], f[6];
+#pragma unroll
+            for (int k = 0; k < 18; ++k) u[k] = ld_stream(Ut + (18 * mu + k) * F, pol);
+            if (mu < 3) {
+                T wm[6];
+                adj_mat_vec<T>(u, vc, wm);
+#pragma unroll
+                for (int k = 0; k < 6; ++k) sb[(6 * mu + k) * nthr + tid] = wm[k];
+                ld_soa<T, 6>(vt, F, s3_up[mu], nb);  // v(x+mu, t): L1 hit (this CTA read it as v(t+1) last step)
+                mat_vec<T>(u, nb, f);
+            } else {
+                adj_mat_vec<T>(u, vc, wt_next);
+                mat_vec<T>(u, vn, f);
+            }
+#pragma unroll
+            for (int k = 0; k < 6; ++k) acc[k] = (mu == 0) ? f[k] : xadd(acc[k], f[k]);
+        }
+        __syncthreads();
+
+        // ---- backward terms (sub_four_su3_vecs chain) ----
+#pragma unroll
+        for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], sb[k * nthr + tx_dn]);
+        if (ty_dn >= 0) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], sb[(6 + k) * nthr + ty_dn]);
+        } else {
+            T uh[18], vh[6], wh[6];
+            ld_soa<T, 18>(p.U + (int64_t(t) * 72 + 18) * F, F, s3_ydn, uh);
+            ld_soa<T, 6>(vt, F, s3_ydn, vh);
+            adj_mat_vec<T>(uh, vh, wh);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], wh[k]);
+        }
+        if (tz_dn >= 0) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], sb[(12 + k) * nthr + tz_dn]);
+        } else {
+            T uh[18], vh[6], wh[6];
+            ld_soa<T, 18>(p.U + (int64_t(t) * 72 + 36) * F, F, s3_zdn, uh);
+            ld_soa<T, 6>(vt, F, s3_zdn, vh);
+            adj_mat_vec<T>(uh, vh, wh);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], wh[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], wt[k]);
+
+        T* o = p.out + int64_t(t) * 6 * F + s3;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) o[k * F] = acc[k];
+
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            vc[k] = vn[k];
+            wt[k] = wt_next[k];
+        }
+        buf ^= 1;
+    }
+}
+
+// block shape (BY, BZ) for the walk kernel; false -> use the generic kernel
+static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ) {
+    if (nx > max_threads) return false;
+    int best = 0, by = 0, bz = 0;
+    double best_halo = 1e30;
+    for (int a = 1; a <= ny; ++a) {
+        if (ny % a) continue;
+        for (int b = 1; b <= nz; ++b) {
+            if (nz % b) continue;
+            const int n = nx * a * b;
+            if (n > max_threads) continue;
+            // halo rows read through L2 per block site (0 if the block spans the extent)
+            const double halo = (a == ny ? 0.0 : 1.0 / a) + (b == nz ? 0.0 : 1.0 / b);
+            if (n > best || (n == best && halo < best_halo)) {
+                best = n; by = a; bz = b; best_halo = halo;
+            }
+        }
+    }
+    if (best < 32) return false;
+    BY = by;
+    BZ = bz;
+    return true;
+}
+
+static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk
+
+template <typename T>
+static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
+                       const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st) {
+    constexpr int MINB = 2;
+    WalkParams<T> p{U, v, out, v_hi, w_lo, nx, ny, nz, nt, int64_t(nx) * ny * nz, BY, BZ, ny / BY, t_begin, t_end, 0};
+    const int64_t nblocks = int64_t(ny / BY) * (nz / BZ);
+    p.total = nblocks * (t_end - t_begin);
+    const int nthr = nx * BY * BZ;
+    const size_t smem = size_t(2) * 18 * nthr * sizeof(T);
+    static int per_sm_cache[64][2] = {};
+    const DeviceInfo& di = device_info();
+    int& per_sm = per_sm_cache[di.device & 63][sizeof(T) == 8];
+    if (per_sm == 0) {
+        cudaFuncSetAttribute(k_nn_walk<T, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 18 * 256 * int(sizeof(T)));
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_nn_walk<T, MINB>, 256, 2 * 18 * 256 * sizeof(T));
+        per_sm = b > 0 ? b : 1;
+    }
+    // blocks of fewer than 256 threads fit proportionally more CTAs per SM
+    const int64_t slots = int64_t(per_sm) * di.num_sms * std::max(1, 256 / nthr);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.total, slots));
+    k_nn_walk<T, MINB><<<static_cast<unsigned>(grid), nthr, smem, st>>>(p);
+    return check_launch("nn_sweep(walk)");
+}
+
 static int check_geom(const char* what, int nx, int ny, int nz, int nt) {
     if (nx < 1 || ny < 1 || nz < 1 || nt < 1) return fail_invalid(std::string(what) + ": lattice extents must be >= 1");
     return SU3G_OK;
@@ -171,6 +399,11 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     if (t_begin < 0 || t_end > nt || t_begin > t_end) return fail_invalid("nn_sweep: bad t range");
     if (!U || !v || !out) return fail_invalid("nn_sweep: null pointer");
     if (t_begin == t_end) return SU3G_OK;
+    int BY = 0, BZ = 0;
+    const int variant = g_nn_variant.load();
+    if (variant != 1 && walk_shape(nx, ny, nz, 256, BY, BZ))
+        return launch_walk<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+    if (variant == 2) return fail_invalid("nn_sweep: walk kernel not applicable to this lattice");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int64_t n = int64_t(t_end - t_begin) * g.F;
     k_nn_sweep<T><<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo);
@@ -204,6 +437,16 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
 using namespace su3g;
 
 extern "C" {
+
+int su3g_set_option(const char* name, int64_t value) {
+    if (name == nullptr) return fail_invalid("set_option: null name");
+    if (std::strcmp(name, "nn_variant") == 0) {
+        if (value < 0 || value > 2) return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk)");
+        g_nn_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    return fail_invalid(std::string("set_option: unknown option ") + name);
+}
 
 int su3g_nn_sweep_f32(const float* U, const float* v, float* out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
                       int32_t t_begin, int32_t t_end, const float* v_hi, const float* w_lo, su3g_stream_t st) {

@@ -162,3 +162,48 @@ def test_slab_halo_path_equals_periodic_sweep(ranks, precision):
     # and the halo face itself is the reference adj product on the last slice
     w0 = w_faces[0].cpu().numpy().T.reshape(F, 3, 2)
     assert np.array_equal(w0, R.mult_adj_su3_mat_vec(U[(ntl - 1) * F : ntl * F, 3], v[(ntl - 1) * F : ntl * F]))
+
+
+@pytest.fixture(params=[0, 1], ids=["auto-walk", "generic"])
+def nn_variant(request):
+    from paper_1309_0551_b200 import _lib
+
+    _lib.set_option("nn_variant", request.param)
+    yield request.param
+    _lib.set_option("nn_variant", 0)
+
+
+@pytest.mark.parametrize("dims", [(8, 8, 8, 8), (16, 4, 6, 3), (64, 4, 4, 4), (5, 7, 3, 4), (4, 8, 8, 2), (32, 16, 2, 1)])
+def test_nn_kernel_variants_bitwise(dims, precision, nn_variant):
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(7000 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    want = coracle.nn_sweep(U, v, dims)
+    assert np.array_equal(sweeps.nn_sweep_aos(U, v, dims), want)
+    # slice-range split (interior + boundaries) writes the same bytes
+    lat = Lattice4D(*dims)
+    Uf = Field.from_aos(lat, "mat4", U)
+    vf = Field.from_aos(lat, "vec", v)
+    out = vf.empty_like()
+    nt = dims[3]
+    for rng_t in ([(0, nt)] if nt < 3 else [(1, nt - 1), (0, 1), (nt - 1, nt)]):
+        sweeps.nn_sweep(Uf, vf, out=out, t_range=rng_t)
+    assert np.array_equal(out.numpy(), want)
+
+
+def test_walk_variant_required_fails_loudly_when_inapplicable():
+    from paper_1309_0551_b200 import _lib
+
+    _lib.set_option("nn_variant", 2)
+    try:
+        lat = Lattice4D(512, 1, 1, 2)  # x extent larger than a CTA
+        U = Field(lat, "mat4", torch.float32, torch.device("cuda"))
+        v = Field(lat, "vec", torch.float32, torch.device("cuda"))
+        with pytest.raises(ValueError, match="walk kernel not applicable"):
+            sweeps.nn_sweep(U, v)
+    finally:
+        _lib.set_option("nn_variant", 0)
+    with pytest.raises(ValueError):
+        _lib.set_option("no_such_option", 1)
