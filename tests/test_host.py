@@ -161,3 +161,30 @@ def test_input_generators_are_special_unitary():
     a = inputs.random_vectors(np.random.default_rng(5), 10, None)
     b = inputs.random_vectors(np.random.default_rng(5), 10, None)
     assert np.array_equal(a, b)
+
+
+def test_register_with_su3bench_plugin_registry():
+    """The b200 record slots into the reference's own registry (backends.py:19-31), harness config accepts it."""
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference package not present (GPU box)")
+    import sys
+
+    sys.path.insert(0, ref)
+    try:
+        import su3bench.backends as rb
+        from su3bench.bench import BenchConfig
+
+        from paper_1309_0551_b200 import backends, kernels
+
+        rec = backends.register_with_su3bench()
+        try:
+            assert rb.get_backend("b200") is rec
+            assert isinstance(rec, rb.Backend)
+            assert set(rec.kernels) == set(kernels.KERNELS)
+            BenchConfig(routine="mult_su3_nn", backend="b200")  # validated through get_backend (bench.py:66)
+        finally:
+            rb._BACKENDS.pop("b200", None)
+            rb.BACKEND_NAMES = tuple(rb._BACKENDS)
+    finally:
+        sys.path.remove(ref)
