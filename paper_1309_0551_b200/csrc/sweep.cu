@@ -12,28 +12,9 @@
 #include <atomic>
 #include <cstring>
 
-#include "su3_math.cuh"
+#include "sweep_common.cuh"
 
 namespace su3g {
-
-struct Geom {
-    int nx, ny, nz, nt;
-    int64_t F;  // sites per t-slice
-};
-
-template <typename T, int N>
-__device__ __forceinline__ void ld_soa(const T* __restrict__ p, int64_t F, int64_t s3, T* r) {
-#pragma unroll
-    for (int k = 0; k < N; ++k) r[k] = __ldg(p + k * F + s3);
-}
-
-// neighbour slice-local index one step along mu in {0, 1, 2} (periodic)
-__device__ __forceinline__ int64_t step3(const Geom& g, int x, int y, int z, int mu, int dir) {
-    if (mu == 0) x = (x + dir + g.nx) % g.nx;
-    else if (mu == 1) y = (y + dir + g.ny) % g.ny;
-    else z = (z + dir + g.nz) % g.nz;
-    return x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
-}
 
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
@@ -195,21 +176,6 @@ struct WalkParams {
     int64_t total;  // blocks * (t_end - t_begin)
 };
 
-template <typename T>
-__device__ __forceinline__ T ld_stream(const T* p, uint64_t pol) {
-    T r;
-    if constexpr (sizeof(T) == 4) {
-        float f;
-        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(f) : "l"(p), "l"(pol));
-        r = f;
-    } else {
-        double d;
-        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(d) : "l"(p), "l"(pol));
-        r = d;
-    }
-    return r;
-}
-
 template <typename T, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -360,7 +326,7 @@ static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ
     return true;
 }
 
-static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk
+static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk, 3 TMA walk
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
@@ -401,7 +367,12 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     if (t_begin == t_end) return SU3G_OK;
     int BY = 0, BZ = 0;
     const int variant = g_nn_variant.load();
-    if (variant != 1 && walk_shape(nx, ny, nz, 256, BY, BZ))
+    if (variant == 0 || variant == 3) {
+        const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+        if (rc != 1) return rc;
+        if (variant == 3) return fail_invalid("nn_sweep: TMA kernel not applicable to this lattice");
+    }
+    if ((variant == 0 || variant == 2) && walk_shape(nx, ny, nz, 256, BY, BZ))
         return launch_walk<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
     if (variant == 2) return fail_invalid("nn_sweep: walk kernel not applicable to this lattice");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
@@ -441,7 +412,8 @@ extern "C" {
 int su3g_set_option(const char* name, int64_t value) {
     if (name == nullptr) return fail_invalid("set_option: null name");
     if (std::strcmp(name, "nn_variant") == 0) {
-        if (value < 0 || value > 2) return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk)");
+        if (value < 0 || value > 3)
+            return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk)");
         g_nn_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -1,0 +1,49 @@
+// Shared pieces of the lattice-sweep kernels (t-sliced SoA fields, see layout.cu).
+#pragma once
+
+#include "su3_math.cuh"
+
+namespace su3g {
+
+struct Geom {
+    int nx, ny, nz, nt;
+    int64_t F;  // sites per t-slice
+};
+
+template <typename T, int N>
+__device__ __forceinline__ void ld_soa(const T* __restrict__ p, int64_t F, int64_t s3, T* r) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) r[k] = __ldg(p + k * F + s3);
+}
+
+// neighbour slice-local index one step along mu in {0, 1, 2} (periodic)
+__device__ __forceinline__ int64_t step3(const Geom& g, int x, int y, int z, int mu, int dir) {
+    if (mu == 0) x = (x + dir + g.nx) % g.nx;
+    else if (mu == 1) y = (y + dir + g.ny) % g.ny;
+    else z = (z + dir + g.nz) % g.nz;
+    return x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
+}
+
+
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p, uint64_t pol) {
+    T r;
+    if constexpr (sizeof(T) == 4) {
+        float f;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(f) : "l"(p), "l"(pol));
+        r = f;
+    } else {
+        double d;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(d) : "l"(p), "l"(pol));
+        r = d;
+    }
+    return r;
+}
+
+// TMA-staged t-walk NN sweep (nn_tma.cu); returns SU3G_EINVAL-style status, or
+// 1 when the lattice does not meet its constraints (caller falls back).
+template <typename T>
+int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
+                  const T* v_hi, const T* w_lo, cudaStream_t st);
+
+}  // namespace su3g
