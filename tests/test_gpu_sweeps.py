@@ -153,9 +153,11 @@ def test_slab_halo_path_equals_periodic_sweep(ranks, precision, dims=(8, 4, 4, 8
         v_hi = vf[(r + 1) % ranks].face(0).contiguous()
         w_lo = w_faces[(r - 1) % ranks]
         out = vf[r].empty_like()
-        sweeps.nn_sweep(Uf[r], vf[r], out=out, t_range=(1, ntl - 1), v_hi=v_hi, w_lo=w_lo)
-        sweeps.nn_sweep(Uf[r], vf[r], out=out, t_range=(0, 1), v_hi=v_hi, w_lo=w_lo)
-        sweeps.nn_sweep(Uf[r], vf[r], out=out, t_range=(ntl - 1, ntl), v_hi=v_hi, w_lo=w_lo)
+        from paper_1309_0551_b200.slab import boundary_ranges
+
+        interior, edges = boundary_ranges(ntl)
+        for rng_t in ([interior] if interior else []) + edges:
+            sweeps.nn_sweep(Uf[r], vf[r], out=out, t_range=rng_t, v_hi=v_hi, w_lo=w_lo)
         parts.append(out.numpy())
     assert np.array_equal(np.concatenate(parts), want)
     # and the halo face itself is the reference adj product on the last slice

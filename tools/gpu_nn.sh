@@ -8,5 +8,5 @@ python tools/suite.py sweeps > gpurun_out/suite_sweeps.jsonl 2> gpurun_out/suite
 python bench.py --steps 50 --warmup 5 > gpurun_out/bench_default.log 2>&1
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k_nn_walk -s 30 -c 1 -o gpurun_out/prof_walk $CMD > gpurun_out/ncu_walk.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:k_nn_tma -s 30 -c 1 -o gpurun_out/prof_tma $CMD > gpurun_out/ncu_tma.log 2>&1
 echo done
