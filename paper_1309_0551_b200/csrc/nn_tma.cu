@@ -106,38 +106,47 @@ __device__ __forceinline__ void item_range(const TmaParams& p, int64_t item, int
 
 }  // namespace
 
-// exchange buffer geometry (per buffer, runtime halo widths HY = nx*BZ, HZ = nx*BY):
-//   WX [6][N]           w_x of the block's sites
-//   WY [6][N + HY]      w_y, plus the -y halo row
-//   WZ [6][N + HZ]      w_z, plus the -z halo row
-//   VV [6][N + HY + HZ] v(x,t), plus the +y and +z halo rows
-struct XLayout {
+// Shared-memory geometry (runtime halo widths HY = nx*BZ, HZ = nx*BY; 0 when the
+// block spans that extent and the direction wraps inside the CTA).
+// Stage (filled by TMA, STAGES deep):
+//   SU  [54][N]   U_x, U_y, U_z of the block's sites
+//   SV  [6][N]    v(x,t+1) of the block
+//   HUy [18][HY]  U_y on the -y halo row      HVyd [6][HY] v on the -y row   HVyu [6][HY] v on the +y row
+//   HUz [18][HZ]  U_z on the -z halo plane    HVzd [6][HZ] v on the -z row   HVzu [6][HZ] v on the +z row
+// Exchange (single buffer, rewritten every step):
+//   XW [18][N] w_x, w_y, w_z of the block   XV [6][N] v(x,t)   XHy [6][HY] / XHz [6][HZ] halo w_y / w_z
+struct Geo {
     int N, HY, HZ;
-    __device__ __forceinline__ int wx() const { return 0; }
-    __device__ __forceinline__ int wy() const { return 6 * N; }
-    __device__ __forceinline__ int wz() const { return 6 * N + 6 * (N + HY); }
-    __device__ __forceinline__ int vv() const { return 6 * N + 6 * (N + HY) + 6 * (N + HZ); }
-    __device__ __forceinline__ int py() const { return N + HY; }
-    __device__ __forceinline__ int pz() const { return N + HZ; }
-    __device__ __forceinline__ int pv() const { return N + HY + HZ; }
-    __device__ __forceinline__ int size() const { return vv() + 6 * (N + HY + HZ); }
+    __device__ __forceinline__ int stage_size() const { return 60 * N + 30 * HY + 30 * HZ; }
+    __device__ __forceinline__ int su() const { return 0; }
+    __device__ __forceinline__ int sv() const { return 54 * N; }
+    __device__ __forceinline__ int huy() const { return 60 * N; }
+    __device__ __forceinline__ int hvyd() const { return 60 * N + 18 * HY; }
+    __device__ __forceinline__ int hvyu() const { return 60 * N + 24 * HY; }
+    __device__ __forceinline__ int huz() const { return 60 * N + 30 * HY; }
+    __device__ __forceinline__ int hvzd() const { return 60 * N + 30 * HY + 18 * HZ; }
+    __device__ __forceinline__ int hvzu() const { return 60 * N + 30 * HY + 24 * HZ; }
+    __device__ __forceinline__ int xw() const { return 0; }
+    __device__ __forceinline__ int xv() const { return 18 * N; }
+    __device__ __forceinline__ int xhy() const { return 24 * N; }
+    __device__ __forceinline__ int xhz() const { return 24 * N + 6 * HY; }
+    __device__ __forceinline__ int xsize() const { return 24 * N + 6 * HY + 6 * HZ; }
 };
 
-template <typename T, int NTHR, int NHALO, int STAGES>
-__global__ void __launch_bounds__(NTHR + 32 + NHALO, 1)
+template <typename T, int NTHR, int STAGES>
+__global__ void __launch_bounds__(NTHR + 32, 1)
     k_nn_tma(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
-             const __grid_constant__ CUtensorMap mapVhi, const T* __restrict__ U, const T* __restrict__ v,
+             const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
+             const __grid_constant__ CUtensorMap mapUzH, const __grid_constant__ CUtensorMap mapVyH,
+             const __grid_constant__ CUtensorMap mapVzH, const T* __restrict__ U, const T* __restrict__ v,
              T* __restrict__ out, const T* __restrict__ w_lo, TmaParams p) {
-    constexpr int NU = 54 * NTHR;  // U_x, U_y, U_z of the block per stage (U_t goes straight to registers)
-    constexpr int NV = 6 * NTHR;   // v(t+1) of the block per stage
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    T* stU = reinterpret_cast<T*>(smem_raw);  // [STAGES][54][NTHR]
-    T* stV = stU + STAGES * NU;                // [STAGES][6][NTHR]
-    T* xb = stV + STAGES * NV;                 // [2][XLayout]
     const int nx = p.nx;
-    const XLayout L{NTHR, p.BY == p.ny ? 0 : nx * p.BZ, p.BZ == p.nz ? 0 : nx * p.BY};
-    const int XS = L.size();
-    uint64_t* full = reinterpret_cast<uint64_t*>(xb + 2 * XS);
+    const Geo g{NTHR, p.BY == p.ny ? 0 : nx * p.BZ, p.BZ == p.nz ? 0 : nx * p.BY};
+    const int SS = g.stage_size();
+    T* stage0 = reinterpret_cast<T*>(smem_raw);
+    T* xb = stage0 + STAGES * SS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(xb + g.xsize());
     uint64_t* empty = full + STAGES;
 
     const int tid = threadIdx.x;
@@ -153,67 +162,15 @@ __global__ void __launch_bounds__(NTHR + 32 + NHALO, 1)
     const int G = gridDim.x;
     const int64_t F = p.F;
 
-    if (tid >= NTHR + 32) {
-        // ------------------------------------------------------------------
-        // halo warps: the -y/-z half-products and +y/+z vectors of the rows just
-        // outside the block, from L2 (the neighbouring blocks are streamed by
-        // other CTAs at the same time), straight into the exchange buffer.
-        // ------------------------------------------------------------------
-        const int h = tid - NTHR - 32;
-        int b = 0;
-        for (int64_t item = blockIdx.x; item < p.nitems; item += G) {
-            int64_t blk;
-            int t0, t1;
-            item_range(p, item, blk, t0, t1);
-            const int y0 = static_cast<int>(blk % p.nby) * p.BY;
-            const int z0 = static_cast<int>(blk / p.nby) * p.BZ;
-            for (int t = t0; t < t1; ++t) {
-                T* sx = xb + b * XS;
-                const T* Ut = U + int64_t(t) * 72 * F;
-                const T* vt = v + int64_t(t) * 6 * F;
-                for (int j = h; j < L.HY + L.HZ; j += NHALO) {
-                    int64_t dn, up;
-                    int mu, wbase, wpitch, vslot;
-                    if (j < L.HY) {
-                        const int lx = j % nx, lz = j / nx;
-                        const int64_t zr = int64_t(p.ny) * (z0 + lz);
-                        dn = lx + int64_t(nx) * ((y0 + p.ny - 1) % p.ny + zr);
-                        up = lx + int64_t(nx) * ((y0 + p.BY) % p.ny + zr);
-                        mu = 1; wbase = L.wy(); wpitch = L.py(); vslot = NTHR + j;
-                    } else {
-                        const int jj = j - L.HY, lx = jj % nx, ly = jj / nx;
-                        dn = lx + int64_t(nx) * (y0 + ly + int64_t(p.ny) * ((z0 + p.nz - 1) % p.nz));
-                        up = lx + int64_t(nx) * (y0 + ly + int64_t(p.ny) * ((z0 + p.BZ) % p.nz));
-                        mu = 2; wbase = L.wz(); wpitch = L.pz(); vslot = NTHR + L.HY + jj;
-                    }
-                    T uh[18], vh[6], vu[6], wh[6];
-                    ld_soa<T, 18>(Ut + int64_t(mu) * 18 * F, F, dn, uh);
-                    ld_soa<T, 6>(vt, F, dn, vh);
-                    ld_soa<T, 6>(vt, F, up, vu);
-                    adj_mat_vec<T>(uh, vh, wh);
-                    const int slot = NTHR + (j < L.HY ? j : j - L.HY);
-#pragma unroll
-                    for (int q = 0; q < 6; ++q) {
-                        sx[wbase + q * wpitch + slot] = wh[q];
-                        sx[L.vv() + q * L.pv() + vslot] = vu[q];
-                    }
-                }
-                named_sync<NTHR + NHALO>();
-                b ^= 1;
-            }
-        }
-        return;
-    }
-
     if (tid >= NTHR) {
         // ------------------------------------------------------------------
-        // producer warp: one elected lane streams every step's operands by TMA
+        // producer warp: one elected lane streams each step's block + halo rows
         // ------------------------------------------------------------------
         if (tid != NTHR) return;
         uint64_t pol_first, pol_normal;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_normal));
-        constexpr uint32_t bytes = (54 + 6) * NTHR * sizeof(T);
+        const uint32_t bytes = uint32_t(SS) * sizeof(T);
         int64_t k = 0;
         for (int64_t item = blockIdx.x; item < p.nitems; item += G) {
             int64_t blk;
@@ -221,26 +178,37 @@ __global__ void __launch_bounds__(NTHR + 32 + NHALO, 1)
             item_range(p, item, blk, t0, t1);
             const int y0 = static_cast<int>(blk % p.nby) * p.BY;
             const int z0 = static_cast<int>(blk / p.nby) * p.BZ;
+            const int ydn = (y0 + p.ny - 1) % p.ny, yup = (y0 + p.BY) % p.ny;
+            const int zdn = (z0 + p.nz - 1) % p.nz, zup = (z0 + p.BZ) % p.nz;
             for (int t = t0; t < t1; ++t, ++k) {
                 const int s = static_cast<int>(k % STAGES);
                 if (k >= STAGES) mbar_wait(&empty[s], static_cast<uint32_t>(((k / STAGES) - 1) & 1));
                 mbar_arrive_expect_tx(&full[s], bytes);
-                T* dU = stU + s * NU;
-                // U_y / U_z rows are re-read as halos by neighbouring blocks: normal priority
-                tma_load_4d(dU, &mapU, 0, y0, z0, t * 72, &full[s], pol_first);
-                tma_load_4d(dU + 18 * NTHR, &mapU, 0, y0, z0, t * 72 + 18, &full[s], pol_normal);
-                tma_load_4d(dU + 36 * NTHR, &mapU, 0, y0, z0, t * 72 + 36, &full[s], pol_normal);
-                T* dV = stV + s * NV;
-                if (t + 1 < p.nt) tma_load_4d(dV, &mapV, 0, y0, z0, (t + 1) * 6, &full[s], pol_normal);
-                else if (p.has_vhi) tma_load_4d(dV, &mapVhi, 0, y0, z0, 0, &full[s], pol_normal);
-                else tma_load_4d(dV, &mapV, 0, y0, z0, 0, &full[s], pol_normal);
+                T* st = stage0 + s * SS;
+                // U_y / U_z are re-read as halo rows by neighbouring blocks in flight: normal priority
+                tma_load_4d(st + g.su(), &mapU, 0, y0, z0, t * 72, &full[s], pol_first);
+                tma_load_4d(st + g.su() + 18 * NTHR, &mapU, 0, y0, z0, t * 72 + 18, &full[s], pol_normal);
+                tma_load_4d(st + g.su() + 36 * NTHR, &mapU, 0, y0, z0, t * 72 + 36, &full[s], pol_normal);
+                if (t + 1 < p.nt) tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, (t + 1) * 6, &full[s], pol_normal);
+                else if (p.has_vhi) tma_load_4d(st + g.sv(), &mapVhi, 0, y0, z0, 0, &full[s], pol_normal);
+                else tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, 0, &full[s], pol_normal);
+                if (g.HY) {
+                    tma_load_4d(st + g.huy(), &mapUyH, 0, ydn, z0, t * 72 + 18, &full[s], pol_normal);
+                    tma_load_4d(st + g.hvyd(), &mapVyH, 0, ydn, z0, t * 6, &full[s], pol_normal);
+                    tma_load_4d(st + g.hvyu(), &mapVyH, 0, yup, z0, t * 6, &full[s], pol_normal);
+                }
+                if (g.HZ) {
+                    tma_load_4d(st + g.huz(), &mapUzH, 0, y0, zdn, t * 72 + 36, &full[s], pol_normal);
+                    tma_load_4d(st + g.hvzd(), &mapVzH, 0, y0, zdn, t * 6, &full[s], pol_normal);
+                    tma_load_4d(st + g.hvzu(), &mapVzH, 0, y0, zup, t * 6, &full[s], pol_normal);
+                }
             }
         }
         return;
     }
 
     // ----------------------------------------------------------------------
-    // compute threads: one site each
+    // compute threads: one site each (+ one halo-row half-product)
     // ----------------------------------------------------------------------
     const int lx = tid % nx;
     const int rr = tid / nx;
@@ -249,10 +217,11 @@ __global__ void __launch_bounds__(NTHR + 32 + NHALO, 1)
     const int sy = nx, sz = nx * p.BY;
     const int ix_up = (lx + 1 == nx) ? tid - lx : tid + 1;
     const int ix_dn = (lx == 0) ? tid + nx - 1 : tid - 1;
-    const int iy_up = (ly + 1 < p.BY) ? tid + sy : (L.HY == 0 ? tid - (p.BY - 1) * sy : NTHR + lx + nx * lz);
-    const int iy_dn = (ly > 0) ? tid - sy : (L.HY == 0 ? tid + (p.BY - 1) * sy : NTHR + lx + nx * lz);
-    const int iz_up = (lz + 1 < p.BZ) ? tid + sz : (L.HZ == 0 ? tid - (p.BZ - 1) * sz : NTHR + L.HY + lx + nx * ly);
-    const int iz_dn = (lz > 0) ? tid - sz : (L.HZ == 0 ? tid + (p.BZ - 1) * sz : NTHR + lx + nx * ly);
+    // neighbour sources: >= 0 -> block slot in the exchange; < 0 -> halo row slot (-1 - j)
+    const int iy_up = (ly + 1 < p.BY) ? tid + sy : (g.HY == 0 ? tid - (p.BY - 1) * sy : -1 - (lx + nx * lz));
+    const int iy_dn = (ly > 0) ? tid - sy : (g.HY == 0 ? tid + (p.BY - 1) * sy : -1 - (lx + nx * lz));
+    const int iz_up = (lz + 1 < p.BZ) ? tid + sz : (g.HZ == 0 ? tid - (p.BZ - 1) * sz : -1 - (lx + nx * ly));
+    const int iz_dn = (lz > 0) ? tid - sz : (g.HZ == 0 ? tid + (p.BZ - 1) * sz : -1 - (lx + nx * ly));
 
     auto site_of = [&](int64_t blk) {
         const int y = static_cast<int>(blk % p.nby) * p.BY + ly;
@@ -262,18 +231,16 @@ __global__ void __launch_bounds__(NTHR + 32 + NHALO, 1)
 
     T vc[6], wt[6], ut[18];
     int64_t k = 0;
-    int b = 0;
     int64_t item = blockIdx.x;
     int64_t blk = 0;
     int t0 = 0, t1 = 0;
     if (item < p.nitems) {
         item_range(p, item, blk, t0, t1);
-        ld_soa<T, 18>(U + (int64_t(t0) * 72 + 54) * F, F, site_of(blk), ut);  // U_t of the first step
+        ld_soa<T, 18>(U + (int64_t(t0) * 72 + 54) * F, F, site_of(blk), ut);
     }
     for (; item < p.nitems; item += G) {
         if (k > 0) item_range(p, item, blk, t0, t1);
         const int64_t s3 = site_of(blk);
-        // prologue: v(x,t0) and the -t half-product w_t(x,t0-1)
         ld_soa<T, 6>(v + int64_t(t0) * 6 * F, F, s3, vc);
         if (t0 == 0 && w_lo != nullptr) {
             ld_soa<T, 6>(w_lo, F, s3, wt);
@@ -289,77 +256,109 @@ __global__ void __launch_bounds__(NTHR + 32 + NHALO, 1)
             // prefetch U_t of the next step (this item's t+1, or the next item's first slice)
             T ut_next[18];
             {
-                int64_t nb_blk = blk;
-                int nt_ = t + 1;
-                if (nt_ >= t1 && item + G < p.nitems) {
-                    int a0, a1;
-                    item_range(p, item + G, nb_blk, a0, a1);
-                    nt_ = a0;
+                int64_t nblk = blk;
+                int tn = t + 1;
+                bool have = tn < t1;
+                if (!have && item + G < p.nitems) {
+                    int a1;
+                    item_range(p, item + G, nblk, tn, a1);
+                    have = true;
                 }
-                if (nt_ < p.nt && (nt_ < t1 || item + G < p.nitems))
-                    ld_soa<T, 18>(U + (int64_t(nt_) * 72 + 54) * F, F, site_of(nb_blk), ut_next);
+                if (have) ld_soa<T, 18>(U + (int64_t(tn) * 72 + 54) * F, F, site_of(nblk), ut_next);
             }
             const int s = static_cast<int>(k % STAGES);
             mbar_wait(&full[s], static_cast<uint32_t>((k / STAGES) & 1));
-            const T* su = stU + s * NU + tid;
-            const T* sv = stV + s * NV + tid;
-            T* sx = xb + b * XS;
+            const T* st = stage0 + s * SS;
 
-            // stage -> registers, then hand the stage back to the producer at once
             T u[54], vnext[6];
 #pragma unroll
-            for (int q = 0; q < 54; ++q) u[q] = su[q * NTHR];
+            for (int q = 0; q < 54; ++q) u[q] = st[g.su() + q * NTHR + tid];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) vnext[q] = sv[q * NTHR];
-            mbar_arrive(&empty[s]);
+            for (int q = 0; q < 6; ++q) vnext[q] = st[g.sv() + q * NTHR + tid];
 
-            // publish w_mu(x,t) (mu = x, y, z) and v(x,t); w_t(x,t) is the -t term of step t+1
+            // halo-row half-products: thread j computes halo site j
+            for (int j = tid; j < g.HY + g.HZ; j += NTHR) {
+                T uh[18], vh[6], wh[6];
+                const bool isy = j < g.HY;
+                const int jj = isy ? j : j - g.HY;
+                const int hp = isy ? g.HY : g.HZ;
+                const int ub = isy ? g.huy() : g.huz();
+                const int vb = isy ? g.hvyd() : g.hvzd();
+#pragma unroll
+                for (int q = 0; q < 18; ++q) uh[q] = st[ub + q * hp + jj];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) vh[q] = st[vb + q * hp + jj];
+                adj_mat_vec<T>(uh, vh, wh);
+                const int xo = isy ? g.xhy() : g.xhz();
+#pragma unroll
+                for (int q = 0; q < 6; ++q) xb[xo + q * hp + jj] = wh[q];
+            }
+            // this site's half-products w_x, w_y, w_z and v(x,t) for the neighbours
             {
                 T w[6];
-                adj_mat_vec<T>(u, vc, w);
 #pragma unroll
-                for (int q = 0; q < 6; ++q) sx[L.wx() + q * NTHR + tid] = w[q];
-                adj_mat_vec<T>(u + 18, vc, w);
+                for (int mu = 0; mu < 3; ++mu) {
+                    adj_mat_vec<T>(u + 18 * mu, vc, w);
 #pragma unroll
-                for (int q = 0; q < 6; ++q) sx[L.wy() + q * L.py() + tid] = w[q];
-                adj_mat_vec<T>(u + 36, vc, w);
+                    for (int q = 0; q < 6; ++q) xb[g.xw() + (6 * mu + q) * NTHR + tid] = w[q];
+                }
 #pragma unroll
-                for (int q = 0; q < 6; ++q) sx[L.wz() + q * L.pz() + tid] = w[q];
-#pragma unroll
-                for (int q = 0; q < 6; ++q) sx[L.vv() + q * L.pv() + tid] = vc[q];
+                for (int q = 0; q < 6; ++q) xb[g.xv() + q * NTHR + tid] = vc[q];
             }
             T wt_next[6], f3[6];
             adj_mat_vec<T>(ut, vc, wt_next);
             mat_vec<T>(ut, vnext, f3);  // forward +t term, summed last
-            named_sync<NTHR + NHALO>();
+            named_sync<NTHR>();
 
             // forward terms (add_su3_vector chain: ((f0 + f1) + f2) + f3)
             T acc[6];
             {
                 T nb[6], f[6];
 #pragma unroll
-                for (int q = 0; q < 6; ++q) nb[q] = sx[L.vv() + q * L.pv() + ix_up];
+                for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + ix_up];
                 mat_vec<T>(u, nb, acc);
+                if (iy_up >= 0) {
 #pragma unroll
-                for (int q = 0; q < 6; ++q) nb[q] = sx[L.vv() + q * L.pv() + iy_up];
+                    for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + iy_up];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) nb[q] = st[g.hvyu() + q * g.HY + (-1 - iy_up)];
+                }
                 mat_vec<T>(u + 18, nb, f);
 #pragma unroll
                 for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
+                if (iz_up >= 0) {
 #pragma unroll
-                for (int q = 0; q < 6; ++q) nb[q] = sx[L.vv() + q * L.pv() + iz_up];
+                    for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + iz_up];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) nb[q] = st[g.hvzu() + q * g.HZ + (-1 - iz_up)];
+                }
                 mat_vec<T>(u + 36, nb, f);
 #pragma unroll
                 for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
 #pragma unroll
                 for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f3[q]);
             }
+            mbar_arrive(&empty[s]);  // stage s fully read
+
             // backward terms (sub_four_su3_vecs chain)
 #pragma unroll
-            for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], sx[L.wx() + q * NTHR + ix_dn]);
+            for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + q * NTHR + ix_dn]);
+            if (iy_dn >= 0) {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], sx[L.wy() + q * L.py() + iy_dn]);
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + (6 + q) * NTHR + iy_dn]);
+            } else {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], sx[L.wz() + q * L.pz() + iz_dn]);
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xhy() + q * g.HY + (-1 - iy_dn)]);
+            }
+            if (iz_dn >= 0) {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + (12 + q) * NTHR + iz_dn]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xhz() + q * g.HZ + (-1 - iz_dn)]);
+            }
 #pragma unroll
             for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], wt[q]);
 
@@ -373,7 +372,7 @@ __global__ void __launch_bounds__(NTHR + 32 + NHALO, 1)
             }
 #pragma unroll
             for (int q = 0; q < 18; ++q) ut[q] = ut_next[q];
-            b ^= 1;
+            named_sync<NTHR>();  // exchange buffer free for the next step
         }
     }
 }
@@ -421,10 +420,11 @@ int pick_chunk(int64_t nblocks, int nt_range, int G) {
 
 }  // namespace
 
-template <typename T, int NTHR, int NHALO, int STAGES>
+template <typename T, int NTHR, int STAGES>
 static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                    const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st) {
-    CUtensorMap mU, mV, mVhi;
+    const int HY = (BY == ny) ? 0 : nx * BZ, HZ = (BZ == nz) ? 0 : nx * BY;
+    CUtensorMap mU, mV, mVhi, mUy, mUz, mVy, mVz;
     if (!make_map<T>(&mU, U, nx, ny, nz, int64_t(nt) * 72, BY, BZ, 18)) return 1;
     if (!make_map<T>(&mV, v, nx, ny, nz, int64_t(nt) * 6, BY, BZ, 6)) return 1;
     if (v_hi != nullptr) {
@@ -432,19 +432,19 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     } else {
         mVhi = mV;
     }
-    const int HY = (BY == ny) ? 0 : nx * BZ, HZ = (BZ == nz) ? 0 : nx * BY;
-    const size_t xs = size_t(6) * (4 * NTHR + 2 * HY + 2 * HZ);
-    const size_t smem = size_t(STAGES) * (54 + 6) * NTHR * sizeof(T) + 2 * xs * sizeof(T) + 2 * STAGES * sizeof(uint64_t);
+    mUy = mU; mVy = mV; mUz = mU; mVz = mV;
+    if (HY && (!make_map<T>(&mUy, U, nx, ny, nz, int64_t(nt) * 72, 1, BZ, 18) ||
+               !make_map<T>(&mVy, v, nx, ny, nz, int64_t(nt) * 6, 1, BZ, 6)))
+        return 1;
+    if (HZ && (!make_map<T>(&mUz, U, nx, ny, nz, int64_t(nt) * 72, BY, 1, 18) ||
+               !make_map<T>(&mVz, v, nx, ny, nz, int64_t(nt) * 6, BY, 1, 6)))
+        return 1;
+    const size_t stage = size_t(60) * NTHR + 30 * size_t(HY) + 30 * size_t(HZ);
+    const size_t xsize = size_t(24) * NTHR + 6 * size_t(HY) + 6 * size_t(HZ);
+    const size_t smem = (STAGES * stage + xsize) * sizeof(T) + 2 * STAGES * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    static int configured[64] = {0};
-    if (!configured[di.device & 63]) {
-        const size_t worst = size_t(STAGES) * (54 + 6) * NTHR * sizeof(T) + 2 * size_t(6) * (8 * NTHR) * sizeof(T) +
-                             2 * STAGES * sizeof(uint64_t);
-        cudaFuncSetAttribute(k_nn_tma<T, NTHR, NHALO, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(std::min<size_t>(worst, size_t(di.max_smem_optin))));
-        configured[di.device & 63] = 1;
-    }
+    cudaFuncSetAttribute(k_nn_tma<T, NTHR, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     TmaParams p{};
     p.nx = nx; p.ny = ny; p.nz = nz; p.nt = nt;
     p.F = int64_t(nx) * ny * nz;
@@ -457,7 +457,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
-    k_nn_tma<T, NTHR, NHALO, STAGES><<<grid, NTHR + 32 + NHALO, smem, st>>>(mU, mV, mVhi, U, v, out, w_lo, p);
+    k_nn_tma<T, NTHR, STAGES><<<grid, NTHR + 32, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     return check_launch("nn_sweep(tma)");
 }
 
@@ -469,7 +469,7 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
     int BY = 0, BZ = 0;
     if (!tma_shape(nx, ny, nz, NTHR, BY, BZ)) return 1;
-    return run_tma<T, NTHR, 64, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+    return run_tma<T, NTHR, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
 }
 
 template int launch_nn_tma<float>(const float*, const float*, float*, int, int, int, int, int, int, const float*,

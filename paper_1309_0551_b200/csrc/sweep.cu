@@ -372,7 +372,8 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
         if (rc != 1) return rc;
         if (variant == 3) return fail_invalid("nn_sweep: TMA kernel not applicable to this lattice");
     }
-    if ((variant == 0 || variant == 2) && walk_shape(nx, ny, nz, 256, BY, BZ))
+    // auto: f64 skips the register-walk kernel (the generic kernel measured faster for f64)
+    if (((variant == 0 && sizeof(T) == 4) || variant == 2) && walk_shape(nx, ny, nz, 256, BY, BZ))
         return launch_walk<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
     if (variant == 2) return fail_invalid("nn_sweep: walk kernel not applicable to this lattice");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
