@@ -134,7 +134,7 @@ struct Geo {
 };
 
 template <typename T, int NTHR, int STAGES>
-__global__ void __launch_bounds__(NTHR + 32, 1)
+__global__ void __maxnreg__(NTHR >= 256 ? 224 : 255)
     k_nn_tma(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
              const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
              const __grid_constant__ CUtensorMap mapUzH, const __grid_constant__ CUtensorMap mapVyH,
@@ -229,17 +229,48 @@ __global__ void __launch_bounds__(NTHR + 32, 1)
         return lx + int64_t(nx) * (y + int64_t(p.ny) * z);
     };
 
-    T vc[6], wt[6], ut[18];
+    // U_t of step k is loaded two steps ahead (registers ut -> ut1 -> ut2 pipeline)
+    struct Cursor {
+        int64_t item, blk;
+        int t, t1;
+        bool valid;
+    };
+    auto advance = [&](Cursor c) {
+        if (!c.valid) return c;
+        if (c.t + 1 < c.t1) {
+            ++c.t;
+            return c;
+        }
+        c.item += G;
+        if (c.item >= p.nitems) {
+            c.valid = false;
+            return c;
+        }
+        int a0, a1;
+        item_range(p, c.item, c.blk, a0, a1);
+        c.t = a0;
+        c.t1 = a1;
+        return c;
+    };
+    auto load_ut = [&](const Cursor& c, T* r) {
+        if (c.valid) ld_soa<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, site_of(c.blk), r);
+    };
+
+    T vc[6], wt[6], ut[18], ut1[18];
     int64_t k = 0;
     int64_t item = blockIdx.x;
     int64_t blk = 0;
     int t0 = 0, t1 = 0;
-    if (item < p.nitems) {
-        item_range(p, item, blk, t0, t1);
-        ld_soa<T, 18>(U + (int64_t(t0) * 72 + 54) * F, F, site_of(blk), ut);
+    Cursor ahead{item, 0, 0, 0, item < p.nitems};
+    if (ahead.valid) {
+        item_range(p, item, ahead.blk, ahead.t, ahead.t1);
+        load_ut(ahead, ut);
+        ahead = advance(ahead);
+        load_ut(ahead, ut1);
+        ahead = advance(ahead);  // -> step 2
     }
     for (; item < p.nitems; item += G) {
-        if (k > 0) item_range(p, item, blk, t0, t1);
+        item_range(p, item, blk, t0, t1);
         const int64_t s3 = site_of(blk);
         ld_soa<T, 6>(v + int64_t(t0) * 6 * F, F, s3, vc);
         if (t0 == 0 && w_lo != nullptr) {
@@ -253,19 +284,9 @@ __global__ void __launch_bounds__(NTHR + 32, 1)
         }
 
         for (int t = t0; t < t1; ++t, ++k) {
-            // prefetch U_t of the next step (this item's t+1, or the next item's first slice)
-            T ut_next[18];
-            {
-                int64_t nblk = blk;
-                int tn = t + 1;
-                bool have = tn < t1;
-                if (!have && item + G < p.nitems) {
-                    int a1;
-                    item_range(p, item + G, nblk, tn, a1);
-                    have = true;
-                }
-                if (have) ld_soa<T, 18>(U + (int64_t(tn) * 72 + 54) * F, F, site_of(nblk), ut_next);
-            }
+            T ut2[18];
+            load_ut(ahead, ut2);  // U_t of step k+2
+            ahead = advance(ahead);
             const int s = static_cast<int>(k % STAGES);
             mbar_wait(&full[s], static_cast<uint32_t>((k / STAGES) & 1));
             const T* st = stage0 + s * SS;
@@ -371,7 +392,10 @@ __global__ void __launch_bounds__(NTHR + 32, 1)
                 wt[q] = wt_next[q];
             }
 #pragma unroll
-            for (int q = 0; q < 18; ++q) ut[q] = ut_next[q];
+            for (int q = 0; q < 18; ++q) {
+                ut[q] = ut1[q];
+                ut1[q] = ut2[q];
+            }
             named_sync<NTHR>();  // exchange buffer free for the next step
         }
     }
