@@ -134,12 +134,13 @@ struct Geo {
 };
 
 template <typename T, int NTHR, int STAGES>
-__global__ void __maxnreg__(NTHR >= 256 ? 224 : 255)
+__global__ void __launch_bounds__(NTHR, 1)
     k_nn_tma(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
              const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
              const __grid_constant__ CUtensorMap mapUzH, const __grid_constant__ CUtensorMap mapVyH,
              const __grid_constant__ CUtensorMap mapVzH, const T* __restrict__ U, const T* __restrict__ v,
              T* __restrict__ out, const T* __restrict__ w_lo, TmaParams p) {
+    static_assert(STAGES == 2, "the refill of stage k%2 is step k+2 (two-step lookahead)");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int nx = p.nx;
     const Geo g{NTHR, p.BY == p.ny ? 0 : nx * p.BZ, p.BZ == p.nz ? 0 : nx * p.BY};
@@ -161,51 +162,38 @@ __global__ void __maxnreg__(NTHR >= 256 ? 224 : 255)
 
     const int G = gridDim.x;
     const int64_t F = p.F;
-
-    if (tid >= NTHR) {
-        // ------------------------------------------------------------------
-        // producer warp: one elected lane streams each step's block + halo rows
-        // ------------------------------------------------------------------
-        if (tid != NTHR) return;
-        uint64_t pol_first, pol_normal;
+    uint64_t pol_first = 0, pol_normal = 0;
+    if (tid == 0) {
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_normal));
-        const uint32_t bytes = uint32_t(SS) * sizeof(T);
-        int64_t k = 0;
-        for (int64_t item = blockIdx.x; item < p.nitems; item += G) {
-            int64_t blk;
-            int t0, t1;
-            item_range(p, item, blk, t0, t1);
-            const int y0 = static_cast<int>(blk % p.nby) * p.BY;
-            const int z0 = static_cast<int>(blk / p.nby) * p.BZ;
-            const int ydn = (y0 + p.ny - 1) % p.ny, yup = (y0 + p.BY) % p.ny;
-            const int zdn = (z0 + p.nz - 1) % p.nz, zup = (z0 + p.BZ) % p.nz;
-            for (int t = t0; t < t1; ++t, ++k) {
-                const int s = static_cast<int>(k % STAGES);
-                if (k >= STAGES) mbar_wait(&empty[s], static_cast<uint32_t>(((k / STAGES) - 1) & 1));
-                mbar_arrive_expect_tx(&full[s], bytes);
-                T* st = stage0 + s * SS;
-                // U_y / U_z are re-read as halo rows by neighbouring blocks in flight: normal priority
-                tma_load_4d(st + g.su(), &mapU, 0, y0, z0, t * 72, &full[s], pol_first);
-                tma_load_4d(st + g.su() + 18 * NTHR, &mapU, 0, y0, z0, t * 72 + 18, &full[s], pol_normal);
-                tma_load_4d(st + g.su() + 36 * NTHR, &mapU, 0, y0, z0, t * 72 + 36, &full[s], pol_normal);
-                if (t + 1 < p.nt) tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, (t + 1) * 6, &full[s], pol_normal);
-                else if (p.has_vhi) tma_load_4d(st + g.sv(), &mapVhi, 0, y0, z0, 0, &full[s], pol_normal);
-                else tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, 0, &full[s], pol_normal);
-                if (g.HY) {
-                    tma_load_4d(st + g.huy(), &mapUyH, 0, ydn, z0, t * 72 + 18, &full[s], pol_normal);
-                    tma_load_4d(st + g.hvyd(), &mapVyH, 0, ydn, z0, t * 6, &full[s], pol_normal);
-                    tma_load_4d(st + g.hvyu(), &mapVyH, 0, yup, z0, t * 6, &full[s], pol_normal);
-                }
-                if (g.HZ) {
-                    tma_load_4d(st + g.huz(), &mapUzH, 0, y0, zdn, t * 72 + 36, &full[s], pol_normal);
-                    tma_load_4d(st + g.hvzd(), &mapVzH, 0, y0, zdn, t * 6, &full[s], pol_normal);
-                    tma_load_4d(st + g.hvzu(), &mapVzH, 0, y0, zup, t * 6, &full[s], pol_normal);
-                }
-            }
-        }
-        return;
     }
+    // TMA issue of one step's operands (thread 0 only): the block's U_x, U_y, U_z, v(t+1)
+    // and the halo rows; U_y / U_z stay at normal L2 priority because neighbouring
+    // blocks in flight re-read them as their halo rows.
+    auto issue = [&](int s, int64_t blk, int t) {
+        const int y0 = static_cast<int>(blk % p.nby) * p.BY;
+        const int z0 = static_cast<int>(blk / p.nby) * p.BZ;
+        mbar_arrive_expect_tx(&full[s], uint32_t(SS) * sizeof(T));
+        T* st = stage0 + s * SS;
+        tma_load_4d(st + g.su(), &mapU, 0, y0, z0, t * 72, &full[s], pol_first);
+        tma_load_4d(st + g.su() + 18 * NTHR, &mapU, 0, y0, z0, t * 72 + 18, &full[s], pol_normal);
+        tma_load_4d(st + g.su() + 36 * NTHR, &mapU, 0, y0, z0, t * 72 + 36, &full[s], pol_normal);
+        if (t + 1 < p.nt) tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, (t + 1) * 6, &full[s], pol_normal);
+        else if (p.has_vhi) tma_load_4d(st + g.sv(), &mapVhi, 0, y0, z0, 0, &full[s], pol_normal);
+        else tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, 0, &full[s], pol_normal);
+        if (g.HY) {
+            const int ydn = (y0 + p.ny - 1) % p.ny, yup = (y0 + p.BY) % p.ny;
+            tma_load_4d(st + g.huy(), &mapUyH, 0, ydn, z0, t * 72 + 18, &full[s], pol_normal);
+            tma_load_4d(st + g.hvyd(), &mapVyH, 0, ydn, z0, t * 6, &full[s], pol_normal);
+            tma_load_4d(st + g.hvyu(), &mapVyH, 0, yup, z0, t * 6, &full[s], pol_normal);
+        }
+        if (g.HZ) {
+            const int zdn = (z0 + p.nz - 1) % p.nz, zup = (z0 + p.BZ) % p.nz;
+            tma_load_4d(st + g.huz(), &mapUzH, 0, y0, zdn, t * 72 + 36, &full[s], pol_normal);
+            tma_load_4d(st + g.hvzd(), &mapVzH, 0, y0, zdn, t * 6, &full[s], pol_normal);
+            tma_load_4d(st + g.hvzu(), &mapVzH, 0, y0, zup, t * 6, &full[s], pol_normal);
+        }
+    };
 
     // ----------------------------------------------------------------------
     // compute threads: one site each (+ one halo-row half-product)
@@ -264,8 +252,10 @@ __global__ void __maxnreg__(NTHR >= 256 ? 224 : 255)
     Cursor ahead{item, 0, 0, 0, item < p.nitems};
     if (ahead.valid) {
         item_range(p, item, ahead.blk, ahead.t, ahead.t1);
+        if (tid == 0) issue(0, ahead.blk, ahead.t);
         load_ut(ahead, ut);
         ahead = advance(ahead);
+        if (tid == 0 && ahead.valid && STAGES > 1) issue(1, ahead.blk, ahead.t);
         load_ut(ahead, ut1);
         ahead = advance(ahead);  // -> step 2
     }
@@ -285,7 +275,8 @@ __global__ void __maxnreg__(NTHR >= 256 ? 224 : 255)
 
         for (int t = t0; t < t1; ++t, ++k) {
             T ut2[18];
-            load_ut(ahead, ut2);  // U_t of step k+2
+            const Cursor c2 = ahead;  // step k + 2
+            load_ut(c2, ut2);
             ahead = advance(ahead);
             const int s = static_cast<int>(k % STAGES);
             mbar_wait(&full[s], static_cast<uint32_t>((k / STAGES) & 1));
@@ -361,7 +352,11 @@ __global__ void __maxnreg__(NTHR >= 256 ? 224 : 255)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f3[q]);
             }
-            mbar_arrive(&empty[s]);  // stage s fully read
+            mbar_arrive(&empty[s]);  // stage s fully read by this thread
+            if (tid == 0 && c2.valid) {  // refill it with step k + 2 once every thread is done
+                mbar_wait(&empty[s], static_cast<uint32_t>((k / STAGES) & 1));
+                issue(s, c2.blk, c2.t);
+            }
 
             // backward terms (sub_four_su3_vecs chain)
 #pragma unroll
@@ -481,7 +476,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
-    k_nn_tma<T, NTHR, STAGES><<<grid, NTHR + 32, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
+    k_nn_tma<T, NTHR, STAGES><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     return check_launch("nn_sweep(tma)");
 }
 
