@@ -173,7 +173,9 @@ struct WalkParams {
     int64_t F;
     int BY, BZ, nby;
     int t_begin, t_end;
-    int64_t total;  // blocks * (t_end - t_begin)
+    int64_t nblocks;
+    int chunk;       // t-chunk length of one work item
+    int64_t nitems;  // nblocks * ceil((t_end - t_begin) / chunk), chunk-major
 };
 
 template <typename T, int MINB>
@@ -199,18 +201,17 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 
-    const int64_t w0 = p.total * blockIdx.x / gridDim.x;
-    const int64_t w1 = p.total * (blockIdx.x + 1) / gridDim.x;
-
     T vc[6], wt[6];
-    int64_t cur = -1;
     int64_t s3 = 0, s3_up[3] = {0, 0, 0}, s3_ydn = 0, s3_zdn = 0;
     int buf = 0;
-    for (int64_t w = w0; w < w1; ++w) {
-        const int64_t blk = w / steps;
-        const int t = p.t_begin + static_cast<int>(w - blk * steps);
-        if (blk != cur) {  // prologue: v(x,t) and the -t half-product w_t(x,t-1)
-            cur = blk;
+    // items (block, t-chunk), chunk-major: CTAs in flight hold neighbouring blocks of the same
+    // t-range, so the halo rows they read from each other are L2 hits
+    for (int64_t item = blockIdx.x; item < p.nitems; item += gridDim.x) {
+        const int64_t ch = item / p.nblocks;
+        const int64_t blk = item - ch * p.nblocks;
+        const int t0 = p.t_begin + static_cast<int>(ch) * p.chunk;
+        const int t1 = min(t0 + p.chunk, p.t_end);
+        {  // prologue: v(x,t0) and the -t half-product w_t(x,t0-1)
             const int y = static_cast<int>(blk % p.nby) * p.BY + ly;
             const int z = static_cast<int>(blk / p.nby) * p.BZ + lz;
             s3 = lx + int64_t(nx) * (y + int64_t(p.ny) * z);
@@ -219,17 +220,18 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
             s3_up[2] = lx + int64_t(nx) * (y + int64_t(p.ny) * ((z + 1) % p.nz));
             s3_ydn = lx + int64_t(nx) * ((y + p.ny - 1) % p.ny + int64_t(p.ny) * z);
             s3_zdn = lx + int64_t(nx) * (y + int64_t(p.ny) * ((z + p.nz - 1) % p.nz));
-            ld_soa<T, 6>(p.v + int64_t(t) * 6 * F, F, s3, vc);
-            if (t == 0 && p.w_lo != nullptr) {
+            ld_soa<T, 6>(p.v + int64_t(t0) * 6 * F, F, s3, vc);
+            if (t0 == 0 && p.w_lo != nullptr) {
                 ld_soa<T, 6>(p.w_lo, F, s3, wt);
             } else {
-                const int tp = (t > 0) ? t - 1 : p.nt - 1;
+                const int tp = (t0 > 0) ? t0 - 1 : p.nt - 1;
                 T u[18], vp[6];
                 ld_soa<T, 18>(p.U + (int64_t(tp) * 72 + 54) * F, F, s3, u);
                 ld_soa<T, 6>(p.v + int64_t(tp) * 6 * F, F, s3, vp);
                 adj_mat_vec<T>(u, vp, wt);
             }
         }
+      for (int t = t0; t < t1; ++t) {
         T vn[6];
         if (t + 1 < p.nt) ld_soa<T, 6>(p.v + int64_t(t + 1) * 6 * F, F, s3, vn);
         else if (p.v_hi != nullptr) ld_soa<T, 6>(p.v_hi, F, s3, vn);
@@ -244,7 +246,8 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
         for (int mu = 0; mu < 4; ++mu) {
             T u[18], nb[6], f[6];
 #pragma unroll
-            for (int k = 0; k < 18; ++k) u[k] = ld_stream(Ut + (18 * mu + k) * F, pol);
+            for (int k = 0; k < 18; ++k)  // U_y / U_z rows are re-read as halos by neighbouring blocks
+                u[k] = (mu == 1 || mu == 2) ? __ldg(Ut + (18 * mu + k) * F) : ld_stream(Ut + (18 * mu + k) * F, pol);
             if (mu < 3) {
                 T wm[6];
                 adj_mat_vec<T>(u, vc, wm);
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
             wt[k] = wt_next[k];
         }
         buf ^= 1;
+      }
     }
 }
 
@@ -332,9 +336,9 @@ template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                        const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st) {
     constexpr int MINB = 2;
-    WalkParams<T> p{U, v, out, v_hi, w_lo, nx, ny, nz, nt, int64_t(nx) * ny * nz, BY, BZ, ny / BY, t_begin, t_end, 0};
-    const int64_t nblocks = int64_t(ny / BY) * (nz / BZ);
-    p.total = nblocks * (t_end - t_begin);
+    WalkParams<T> p{U, v, out, v_hi, w_lo, nx, ny, nz, nt, int64_t(nx) * ny * nz, BY, BZ, ny / BY, t_begin, t_end,
+                    0, 0, 0};
+    p.nblocks = int64_t(ny / BY) * (nz / BZ);
     const int nthr = nx * BY * BZ;
     const size_t smem = size_t(2) * 18 * nthr * sizeof(T);
     static int per_sm_cache[64][2] = {};
@@ -348,7 +352,9 @@ static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, i
     }
     // blocks of fewer than 256 threads fit proportionally more CTAs per SM
     const int64_t slots = int64_t(per_sm) * di.num_sms * std::max(1, 256 / nthr);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.total, slots));
+    p.chunk = pick_chunk(p.nblocks, t_end - t_begin, static_cast<int>(std::min<int64_t>(slots, 1 << 20)));
+    p.nitems = p.nblocks * ((t_end - t_begin + p.chunk - 1) / p.chunk);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.nitems, slots));
     k_nn_walk<T, MINB><<<static_cast<unsigned>(grid), nthr, smem, st>>>(p);
     return check_launch("nn_sweep(walk)");
 }

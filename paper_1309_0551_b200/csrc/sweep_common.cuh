@@ -40,6 +40,25 @@ __device__ __forceinline__ T ld_stream(const T* p, uint64_t pol) {
     return r;
 }
 
+// chunk length that best balances the single wave of G CTAs (prologue = ~0.3 slice)
+inline int pick_chunk(int64_t nblocks, int nt_range, int G) {
+    int best_L = nt_range;
+    double best_eff = -1;
+    for (int L = nt_range; L >= 1; --L) {
+        const int64_t nchunks = (nt_range + L - 1) / L;
+        const int64_t items = nblocks * nchunks;
+        const int64_t per = (items + G - 1) / G;
+        const double work = double(nblocks) * nt_range;
+        const double eff = work / (double(per) * G * L) * (L / (L + 0.3));
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best_L = L;
+        }
+    }
+    return best_L;
+}
+
+
 // TMA-staged t-walk NN sweep (nn_tma.cu); returns SU3G_EINVAL-style status, or
 // 1 when the lattice does not meet its constraints (caller falls back).
 template <typename T>
