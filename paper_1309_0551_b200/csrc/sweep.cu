@@ -373,13 +373,16 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     if (t_begin == t_end) return SU3G_OK;
     int BY = 0, BZ = 0;
     const int variant = g_nn_variant.load();
-    if (variant == 0 || variant == 3) {
+    // auto policy (measured on B200, profiles/r01): f32 with full-width 64+ x rows -> TMA walk;
+    // other f32 lattices -> register walk; f64 -> generic (fewest registers, best occupancy)
+    const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 64;
+    const bool auto_walk = variant == 0 && sizeof(T) == 4;
+    if (auto_tma || variant == 3) {
         const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
         if (rc != 1) return rc;
         if (variant == 3) return fail_invalid("nn_sweep: TMA kernel not applicable to this lattice");
     }
-    // auto: f64 skips the register-walk kernel (the generic kernel measured faster for f64)
-    if (((variant == 0 && sizeof(T) == 4) || variant == 2) && walk_shape(nx, ny, nz, 256, BY, BZ))
+    if ((auto_walk || variant == 2) && walk_shape(nx, ny, nz, 256, BY, BZ))
         return launch_walk<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
     if (variant == 2) return fail_invalid("nn_sweep: walk kernel not applicable to this lattice");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
