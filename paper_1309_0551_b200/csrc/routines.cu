@@ -21,6 +21,7 @@
 // the reference association (su3_math.cuh), so every path is bit-identical to
 // su3bench.
 #include <algorithm>
+#include <type_traits>
 
 #include "su3_math.cuh"
 
@@ -76,6 +77,15 @@ struct OpAdj4Dir {
     static constexpr bool SCALAR = false;
     static constexpr const char* name = "mult_adj_su3_mat_vec_4dir";
     __device__ static void apply(const T* a, const T* b, T, T* c) { adj_mat_vec_4dir<T>(a, b, c); }
+    // 4 threads per site: part d computes c[d] = adj(a4[d]) b
+    static constexpr int PARTS = 4;
+    __device__ static void apply_part(int d, const T* a, const T* b, T, T* c) {
+        T m[18], v[6], r[6];
+        load_rec<18>(a + 18 * d, m);
+        load_rec<6>(b, v);
+        adj_mat_vec<T>(m, v, r);
+        store_rec<6>(c + 6 * d, r);
+    }
 };
 template <typename T_>
 struct OpSum4Dir {
@@ -84,6 +94,20 @@ struct OpSum4Dir {
     static constexpr bool SCALAR = false;
     static constexpr const char* name = "mult_su3_mat_vec_sum_4dir";
     __device__ static void apply(const T* a, const T* b, T, T* c) { mat_vec_sum_4dir<T>(a, b, c); }
+    // 4 threads per site: part i < 3 computes row i (the 12-term sum keeps its d-major order); part 3 idles
+    static constexpr int PARTS = 4;
+    __device__ static void apply_part(int i, const T* a4, const T* b4, T, T* c) {
+        if (i >= 3) return;
+        T col[24], v[24];
+#pragma unroll
+        for (int n = 0; n < 12; ++n) {  // a4[d][j][i], n = 3d + j
+            col[2 * n] = a4[18 * (n / 3) + (3 * (n % 3) + i) * 2];
+            col[2 * n + 1] = a4[18 * (n / 3) + (3 * (n % 3) + i) * 2 + 1];
+        }
+        load_rec<24>(b4, v);
+        cdot<T, CONJ_P, 12>([&](int n, int r) { return col[2 * n + r]; }, [&](int n, int r) { return v[2 * n + r]; },
+                            c[2 * i], c[2 * i + 1]);
+    }
 };
 template <typename T_>
 struct OpSmadd {
@@ -213,6 +237,107 @@ struct LaunchCache {
     int blocks_per_sm[64] = {0};
 };
 
+// Variant for wide records (mat4 / vec4 per site): PARTS threads per site read their
+// share of the record straight from the staged tile (conflict-free: lanes of a site hit
+// disjoint banks), so no thread holds the whole 96-real record in registers.
+template <class Op>
+struct PartsGeometry {
+    using T = typename Op::T;
+    static constexpr int IN_BYTES = (Op::NA + Op::NB) * int(sizeof(T));
+    static constexpr int TS = IN_BYTES <= 400 ? 64 : 32;
+    static constexpr int THREADS = TS * Op::PARTS;
+    static constexpr int STAGES = 4;
+    static constexpr uint32_t A_BYTES = TS * Op::NA * sizeof(T);
+    static constexpr uint32_t B_BYTES = TS * Op::NB * sizeof(T);
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t C_BYTES = TS * Op::NC * sizeof(T);
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 2 * C_BYTES + STAGES * 8;
+};
+
+template <class Op>
+__global__ void __launch_bounds__(PartsGeometry<Op>::THREADS)
+    k_stream_parts(const typename Op::T* __restrict__ A, const typename Op::T* __restrict__ B,
+                   typename Op::T* __restrict__ C, int64_t n) {
+    using T = typename Op::T;
+    using G = PartsGeometry<Op>;
+    constexpr int TS = G::TS, STAGES = G::STAGES;
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* stages = smem;
+    T* obuf = reinterpret_cast<T*>(smem + STAGES * G::STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_BYTES + 2 * G::C_BYTES);
+
+    const int tid = threadIdx.x;
+    const int site = tid / Op::PARTS, part = tid % Op::PARTS;
+    const int64_t ntiles = n / TS;
+    const int64_t first = blockIdx.x, stride = gridDim.x;
+    const int64_t count = ntiles > first ? (ntiles - first + stride - 1) / stride : 0;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int st = 0; st < STAGES; ++st) mbar_init(&full[st], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint64_t pol = 0;
+    if (tid == 0) pol = policy_evict_first();
+    auto issue = [&](int64_t tile, int st) {
+        unsigned char* base = stages + st * G::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[st], G::STAGE_BYTES);
+        bulk_g2s(base, A + tile * TS * Op::NA, G::A_BYTES, &full[st], pol);
+        bulk_g2s(base + G::A_BYTES, B + tile * TS * Op::NB, G::B_BYTES, &full[st], pol);
+    };
+    if (tid == 0) {
+        for (int k = 0; k < STAGES && k < count; ++k) issue(first + k * stride, k);
+    }
+    for (int64_t k = 0; k < count; ++k) {
+        const int st = static_cast<int>(k % STAGES);
+        const int64_t tile = first + k * stride;
+        mbar_wait(&full[st], static_cast<uint32_t>((k / STAGES) & 1));
+        const unsigned char* base = stages + st * G::STAGE_BYTES;
+        if (tid == 0) bulk_wait_read<1>();  // result buffer (k & 1) released by the store of tile k-2
+        __syncthreads();
+        T* ob = obuf + (k & 1) * TS * Op::NC;
+        Op::apply_part(part, reinterpret_cast<const T*>(base) + site * Op::NA,
+                       reinterpret_cast<const T*>(base + G::A_BYTES) + site * Op::NB, T(0), ob + site * Op::NC);
+        fence_proxy_async_smem();
+        __syncthreads();  // tile consumed and results written
+        if (tid == 0) {
+            bulk_s2g(C + tile * TS * Op::NC, ob, G::C_BYTES);
+            bulk_commit();
+            if (k + STAGES < count) issue(first + (k + STAGES) * stride, st);
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1) {
+        for (int64_t x = ntiles * TS + tid; x < n; x += G::THREADS) site_direct<Op>(A, B, nullptr, T(0), C, x);
+    }
+    if (tid == 0) bulk_wait<0>();
+}
+
+template <class Op>
+int launch_parts(const typename Op::T* a, const typename Op::T* b, typename Op::T* c, int64_t n, cudaStream_t stream) {
+    using G = PartsGeometry<Op>;
+    const DeviceInfo& di = device_info();
+    static LaunchCache<Op> cache;
+    int& per_sm = cache.blocks_per_sm[di.device & 63];
+    if (per_sm == 0) {
+        cudaFuncSetAttribute(k_stream_parts<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(G::SMEM));
+        int bl = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, k_stream_parts<Op>, G::THREADS, G::SMEM);
+        per_sm = std::max(bl, 1);
+    }
+    const int64_t ntiles = n / G::TS;
+    int64_t grid = std::min<int64_t>(ntiles, int64_t(per_sm) * di.num_sms);
+    if (grid < 1) grid = 1;
+    k_stream_parts<Op><<<static_cast<unsigned>(grid), G::THREADS, G::SMEM, stream>>>(a, b, c, n);
+    return check_launch(Op::name);
+}
+
+
+template <class Op, class = void>
+struct HasParts : std::false_type {};
+template <class Op>
+struct HasParts<Op, std::void_t<decltype(Op::PARTS)>> : std::true_type {};
+
 template <class Op>
 int launch(const typename Op::T* a, const typename Op::T* b, const typename Op::T* s_site, typename Op::T s,
            typename Op::T* c, int64_t n, cudaStream_t stream) {
@@ -228,6 +353,7 @@ int launch(const typename Op::T* a, const typename Op::T* b, const typename Op::
         k_direct<Op><<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, b, s_site, s, c, n);
         return check_launch(Op::name);
     }
+    if constexpr (HasParts<Op>::value) return launch_parts<Op>(a, b, c, n, stream);
     static LaunchCache<Op> cache;
     int& per_sm = cache.blocks_per_sm[di.device & 63];
     if (per_sm == 0) {
