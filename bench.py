@@ -235,6 +235,10 @@ def run_b200(args, rank, world, local):
         from paper_1309_0551_b200 import _lib as _l
 
         _l.set_option("nn_variant", int(os.environ["SU3G_NN_VARIANT"]))
+    if os.environ.get("SU3G_LINK_VARIANT"):
+        from paper_1309_0551_b200 import _lib as _l
+
+        _l.set_option("link_variant", int(os.environ["SU3G_LINK_VARIANT"]))
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     gen = torch.Generator(device=dev)
     gen.manual_seed(inputs.SEED + 7919 * rank)

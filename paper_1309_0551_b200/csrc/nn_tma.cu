@@ -133,7 +133,9 @@ struct Geo {
     __device__ __forceinline__ int xsize() const { return 24 * N + 6 * HY + 6 * HZ; }
 };
 
-template <typename T, int NTHR, int STAGES>
+// CNX/CBY/CBZ > 0: block geometry fixed at compile time (halos present in y and z),
+// so every shared-memory offset is an immediate; 0: runtime geometry.
+template <typename T, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
 __global__ void __launch_bounds__(NTHR, 1)
     k_nn_tma(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
              const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
@@ -142,8 +144,12 @@ __global__ void __launch_bounds__(NTHR, 1)
              T* __restrict__ out, const T* __restrict__ w_lo, TmaParams p) {
     static_assert(STAGES == 2, "the refill of stage k%2 is step k+2 (two-step lookahead)");
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int nx = p.nx;
-    const Geo g{NTHR, p.BY == p.ny ? 0 : nx * p.BZ, p.BZ == p.nz ? 0 : nx * p.BY};
+    constexpr bool FIXED = CNX > 0;
+    const int nx = FIXED ? CNX : p.nx;
+    const int BY = FIXED ? CBY : p.BY;
+    const int BZ = FIXED ? CBZ : p.BZ;
+    const Geo g{NTHR, FIXED ? CNX * CBZ : (p.BY == p.ny ? 0 : nx * p.BZ),
+                FIXED ? CNX * CBY : (p.BZ == p.nz ? 0 : nx * p.BY)};
     const int SS = g.stage_size();
     T* stage0 = reinterpret_cast<T*>(smem_raw);
     T* xb = stage0 + STAGES * SS;
@@ -171,8 +177,8 @@ __global__ void __launch_bounds__(NTHR, 1)
     // and the halo rows; U_y / U_z stay at normal L2 priority because neighbouring
     // blocks in flight re-read them as their halo rows.
     auto issue = [&](int s, int64_t blk, int t) {
-        const int y0 = static_cast<int>(blk % p.nby) * p.BY;
-        const int z0 = static_cast<int>(blk / p.nby) * p.BZ;
+        const int y0 = static_cast<int>(blk % p.nby) * BY;
+        const int z0 = static_cast<int>(blk / p.nby) * BZ;
         mbar_arrive_expect_tx(&full[s], uint32_t(SS) * sizeof(T));
         T* st = stage0 + s * SS;
         tma_load_4d(st + g.su(), &mapU, 0, y0, z0, t * 72, &full[s], pol_first);
@@ -182,13 +188,13 @@ __global__ void __launch_bounds__(NTHR, 1)
         else if (p.has_vhi) tma_load_4d(st + g.sv(), &mapVhi, 0, y0, z0, 0, &full[s], pol_normal);
         else tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, 0, &full[s], pol_normal);
         if (g.HY) {
-            const int ydn = (y0 + p.ny - 1) % p.ny, yup = (y0 + p.BY) % p.ny;
+            const int ydn = (y0 + p.ny - 1) % p.ny, yup = (y0 + BY) % p.ny;
             tma_load_4d(st + g.huy(), &mapUyH, 0, ydn, z0, t * 72 + 18, &full[s], pol_normal);
             tma_load_4d(st + g.hvyd(), &mapVyH, 0, ydn, z0, t * 6, &full[s], pol_normal);
             tma_load_4d(st + g.hvyu(), &mapVyH, 0, yup, z0, t * 6, &full[s], pol_normal);
         }
         if (g.HZ) {
-            const int zdn = (z0 + p.nz - 1) % p.nz, zup = (z0 + p.BZ) % p.nz;
+            const int zdn = (z0 + p.nz - 1) % p.nz, zup = (z0 + BZ) % p.nz;
             tma_load_4d(st + g.huz(), &mapUzH, 0, y0, zdn, t * 72 + 36, &full[s], pol_normal);
             tma_load_4d(st + g.hvzd(), &mapVzH, 0, y0, zdn, t * 6, &full[s], pol_normal);
             tma_load_4d(st + g.hvzu(), &mapVzH, 0, y0, zup, t * 6, &full[s], pol_normal);
@@ -200,28 +206,36 @@ __global__ void __launch_bounds__(NTHR, 1)
     // ----------------------------------------------------------------------
     const int lx = tid % nx;
     const int rr = tid / nx;
-    const int ly = rr % p.BY;
-    const int lz = rr / p.BY;
-    const int sy = nx, sz = nx * p.BY;
+    const int ly = rr % BY;
+    const int lz = rr / BY;
+    const int sy = nx, sz = nx * BY;
     const int ix_up = (lx + 1 == nx) ? tid - lx : tid + 1;
     const int ix_dn = (lx == 0) ? tid + nx - 1 : tid - 1;
     // neighbour sources: >= 0 -> block slot in the exchange; < 0 -> halo row slot (-1 - j)
-    const int iy_up = (ly + 1 < p.BY) ? tid + sy : (g.HY == 0 ? tid - (p.BY - 1) * sy : -1 - (lx + nx * lz));
-    const int iy_dn = (ly > 0) ? tid - sy : (g.HY == 0 ? tid + (p.BY - 1) * sy : -1 - (lx + nx * lz));
-    const int iz_up = (lz + 1 < p.BZ) ? tid + sz : (g.HZ == 0 ? tid - (p.BZ - 1) * sz : -1 - (lx + nx * ly));
-    const int iz_dn = (lz > 0) ? tid - sz : (g.HZ == 0 ? tid + (p.BZ - 1) * sz : -1 - (lx + nx * ly));
+    const int iy_up = (ly + 1 < BY) ? tid + sy : (g.HY == 0 ? tid - (BY - 1) * sy : -1 - (lx + nx * lz));
+    const int iy_dn = (ly > 0) ? tid - sy : (g.HY == 0 ? tid + (BY - 1) * sy : -1 - (lx + nx * lz));
+    const int iz_up = (lz + 1 < BZ) ? tid + sz : (g.HZ == 0 ? tid - (BZ - 1) * sz : -1 - (lx + nx * ly));
+    const int iz_dn = (lz > 0) ? tid - sz : (g.HZ == 0 ? tid + (BZ - 1) * sz : -1 - (lx + nx * ly));
 
     auto site_of = [&](int64_t blk) {
-        const int y = static_cast<int>(blk % p.nby) * p.BY + ly;
-        const int z = static_cast<int>(blk / p.nby) * p.BZ + lz;
+        const int y = static_cast<int>(blk % p.nby) * BY + ly;
+        const int z = static_cast<int>(blk / p.nby) * BZ + lz;
         return lx + int64_t(nx) * (y + int64_t(p.ny) * z);
     };
 
-    // U_t of step k is loaded two steps ahead (registers ut -> ut1 -> ut2 pipeline)
+    // U_t of step k is loaded two steps ahead (registers ut -> ut1 -> ut2 pipeline); the
+    // cursor caches its site index so the per-step work has no 64-bit divisions
     struct Cursor {
-        int64_t item, blk;
+        int64_t item, blk, s3;
         int t, t1;
         bool valid;
+    };
+    auto enter = [&](Cursor& c) {
+        int a0, a1;
+        item_range(p, c.item, c.blk, a0, a1);
+        c.t = a0;
+        c.t1 = a1;
+        c.s3 = site_of(c.blk);
     };
     auto advance = [&](Cursor c) {
         if (!c.valid) return c;
@@ -234,14 +248,11 @@ __global__ void __launch_bounds__(NTHR, 1)
             c.valid = false;
             return c;
         }
-        int a0, a1;
-        item_range(p, c.item, c.blk, a0, a1);
-        c.t = a0;
-        c.t1 = a1;
+        enter(c);
         return c;
     };
     auto load_ut = [&](const Cursor& c, T* r) {
-        if (c.valid) ld_soa<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, site_of(c.blk), r);
+        if (c.valid) ld_soa<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, c.s3, r);
     };
 
     T vc[6], wt[6], ut[18], ut1[18];
@@ -249,9 +260,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     int64_t item = blockIdx.x;
     int64_t blk = 0;
     int t0 = 0, t1 = 0;
-    Cursor ahead{item, 0, 0, 0, item < p.nitems};
+    Cursor ahead{item, 0, 0, 0, 0, item < p.nitems};
     if (ahead.valid) {
-        item_range(p, item, ahead.blk, ahead.t, ahead.t1);
+        enter(ahead);
         if (tid == 0) issue(0, ahead.blk, ahead.t);
         load_ut(ahead, ut);
         ahead = advance(ahead);
@@ -421,7 +432,7 @@ bool tma_shape(int nx, int ny, int nz, int nthr, int& BY, int& BZ) {
 
 }  // namespace
 
-template <typename T, int NTHR, int STAGES>
+template <typename T, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
 static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                    const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st) {
     const int HY = (BY == ny) ? 0 : nx * BZ, HZ = (BZ == nz) ? 0 : nx * BY;
@@ -445,7 +456,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     const size_t smem = (STAGES * stage + xsize) * sizeof(T) + 2 * STAGES * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    cudaFuncSetAttribute(k_nn_tma<T, NTHR, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_nn_tma<T, NTHR, STAGES, CNX, CBY, CBZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     TmaParams p{};
     p.nx = nx; p.ny = ny; p.nz = nz; p.nt = nt;
     p.F = int64_t(nx) * ny * nz;
@@ -458,7 +469,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
-    k_nn_tma<T, NTHR, STAGES><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
+    k_nn_tma<T, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     return check_launch("nn_sweep(tma)");
 }
 
@@ -470,6 +481,10 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
     int BY = 0, BZ = 0;
     if (!tma_shape(nx, ny, nz, NTHR, BY, BZ)) return 1;
+    if constexpr (sizeof(T) == 4) {  // the 64-wide production geometry, specialised
+        if (nx == 64 && BY == 2 && BZ == 2 && ny > 2 && nz > 2)
+            return run_tma<T, NTHR, 2, 64, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+    }
     return run_tma<T, NTHR, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
 }
 

@@ -108,16 +108,12 @@ __device__ __forceinline__ void ld_link(const T* __restrict__ U, const Geom& g, 
     ld_soa<T, 18>(U + (t * 72 + mu * 18) * g.F, g.F, s3, r);
 }
 
+// One site's link product (shared by both schedules below).
 template <typename T, bool FUSED>
-__global__ void __launch_bounds__(128)
-    k_link_product(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s) {
-    const int64_t site = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (site >= g.F * g.nt) return;
-    const int t = static_cast<int>(site / g.F);
-    const int64_t s3 = site % g.F;
-    const int x = static_cast<int>(s3 % g.nx);
-    const int y = static_cast<int>((s3 / g.nx) % g.ny);
-    const int z = static_cast<int>(s3 / (int64_t(g.nx) * g.ny));
+__device__ __forceinline__ void link_site(const T* __restrict__ U, T* __restrict__ acc_out, const Geom& g, T s, int x,
+                                          int y, int z, int t) {
+    const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
+    const int64_t site = int64_t(t) * g.F + s3;
     T acc[18];
 #pragma unroll
     for (int k = 0; k < 18; ++k) acc[k] = T(0);
@@ -140,6 +136,44 @@ __global__ void __launch_bounds__(128)
     }
 #pragma unroll
     for (int k = 0; k < 18; ++k) acc_out[(int64_t(t) * 18 + k) * g.F + s3] = acc[k];
+}
+
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(128)
+    k_link_product(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s) {
+    const int64_t site = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (site >= g.F * g.nt) return;
+    const int t = static_cast<int>(site / g.F);
+    const int64_t s3 = site % g.F;
+    link_site<T, FUSED>(U, acc_out, g, s, static_cast<int>(s3 % g.nx), static_cast<int>((s3 / g.nx) % g.ny),
+                        static_cast<int>(s3 / (int64_t(g.nx) * g.ny)), t);
+}
+
+// Block-walk schedule: a CTA owns nx x BY x BZ sites of a slice and walks t; work items
+// (block, t-chunk) go chunk-major over a single wave, so the +t slice a CTA reads as
+// neighbours is what it reads as its own links one step later, and halo links come from
+// blocks other CTAs stream at the same time -- L2 hits instead of DRAM re-reads.
+struct LinkWalk {
+    int BY, BZ, nby;
+    int64_t nblocks;
+    int chunk;
+    int64_t nitems;
+};
+
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(128, 3)
+    k_link_walk(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, LinkWalk w, T s) {
+    const int tid = threadIdx.x;
+    const int lx = tid % g.nx, rr = tid / g.nx, ly = rr % w.BY, lz = rr / w.BY;
+    for (int64_t item = blockIdx.x; item < w.nitems; item += gridDim.x) {
+        const int64_t ch = item / w.nblocks;
+        const int64_t blk = item - ch * w.nblocks;
+        const int t0 = static_cast<int>(ch) * w.chunk;
+        const int t1 = min(t0 + w.chunk, g.nt);
+        const int y = static_cast<int>(blk % w.nby) * w.BY + ly;
+        const int z = static_cast<int>(blk / w.nby) * w.BZ + lz;
+        for (int t = t0; t < t1; ++t) link_site<T, FUSED>(U, acc_out, g, s, lx, y, z, t);
+    }
 }
 
 
@@ -331,6 +365,7 @@ static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk, 3 TMA walk
+static std::atomic<int> g_link_variant{0};  // 0 auto (block walk), 1 generic
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
@@ -406,6 +441,27 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     if (!U || !acc) return fail_invalid("link_product: null pointer");
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("link_product: mode must be SU3G_EXACT or SU3G_FMA");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
+    int BY = 0, BZ = 0;
+    if (g_link_variant.load() != 1 && walk_shape(nx, ny, nz, 128, BY, BZ)) {
+        LinkWalk w{BY, BZ, ny / BY, int64_t(ny / BY) * (nz / BZ), 0, 0};
+        const int nthr = nx * BY * BZ;
+        static int per_sm_cache[64][2][2] = {};
+        const DeviceInfo& di = device_info();
+        int& per_sm = per_sm_cache[di.device & 63][sizeof(T) == 8][mode == SU3G_FMA];
+        if (per_sm == 0) {
+            int b = 0;
+            if (mode == SU3G_FMA) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_link_walk<T, true>, nthr, 0);
+            else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_link_walk<T, false>, nthr, 0);
+            per_sm = b > 0 ? b : 1;
+        }
+        const int G = per_sm * di.num_sms;
+        w.chunk = pick_chunk(w.nblocks, nt, G);
+        w.nitems = w.nblocks * ((nt + w.chunk - 1) / w.chunk);
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(G, w.nitems));
+        if (mode == SU3G_FMA) k_link_walk<T, true><<<grid, nthr, 0, st>>>(U, acc, g, w, s);
+        else k_link_walk<T, false><<<grid, nthr, 0, st>>>(U, acc, g, w, s);
+        return check_launch("link_product(walk)");
+    }
     const int64_t n = g.F * nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
     if (mode == SU3G_FMA) k_link_product<T, true><<<grid, 128, 0, st>>>(U, acc, g, s);
@@ -425,6 +481,11 @@ int su3g_set_option(const char* name, int64_t value) {
         if (value < 0 || value > 3)
             return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk)");
         g_nn_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "link_variant") == 0) {
+        if (value < 0 || value > 1) return fail_invalid("set_option: link_variant must be 0 (auto) or 1 (generic)");
+        g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }
     return fail_invalid(std::string("set_option: unknown option ") + name);

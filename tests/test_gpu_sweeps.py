@@ -230,3 +230,22 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
         _lib.set_option("nn_variant", 0)
     with pytest.raises(ValueError):
         _lib.set_option("no_such_option", 1)
+
+
+@pytest.mark.parametrize("variant", [0, 1], ids=["block-walk", "generic"])
+@pytest.mark.parametrize("dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5)])
+def test_link_product_variants_bitwise(variant, dims, precision):
+    from paper_1309_0551_b200 import _lib
+
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(4000 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    want = coracle.link_product(U, dims, 1 / 6)
+    _lib.set_option("link_variant", variant)
+    try:
+        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+        tol = 1e-5 if dt == np.float32 else 1e-12
+        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
+    finally:
+        _lib.set_option("link_variant", 0)
