@@ -59,6 +59,9 @@ def parse_args(argv=None):
     p.add_argument("--workload", default="nn-weak")
     p.add_argument("--dtype", choices=["f32", "f64"], default=None)
     p.add_argument("--applications", type=int, default=10)
+    p.add_argument("--mode", choices=["exact", "fma"], default=None,
+                   help="SU(3) product arithmetic: exact = reference association, bit-identical (default "
+                        "for the NN sweep); fma = FMA chains within the north-star tolerance")
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sites", type=int, default=64**4, help="sites for routine:<name> workloads")
@@ -67,6 +70,8 @@ def parse_args(argv=None):
         p.error("--warmup must be >= 3")
     if args.dtype is None:
         args.dtype = "f64" if args.workload == "link" else "f32"
+    if args.mode is None:
+        args.mode = os.environ.get("SU3G_LINK_MODE", "exact") if args.workload == "link" else "exact"
     return args
 
 
@@ -227,7 +232,7 @@ def run_b200(args, rank, world, local):
 
     from paper_1309_0551_b200 import inputs, kernels, sweeps
     from paper_1309_0551_b200.lattice import Field, Lattice4D
-    from paper_1309_0551_b200.slab import SlabSweep
+    from paper_1309_0551_b200.slab import CudaSlabKernels, SlabSweep
 
     cfg = workload_config(args, world)
     dev = torch.device("cuda", local)
@@ -257,7 +262,7 @@ def run_b200(args, rank, world, local):
         v0 = Field.from_aos(lat, "vec", v_aos)
         va, vb = v0.empty_like(), v0.empty_like()
         va.data.copy_(v0.data)
-        slab = SlabSweep(U)
+        slab = SlabSweep(U, kernels=CudaSlabKernels(args.mode))
         ntl = lat.nt
         if world == 1:
             per_launch_sites = lat.volume
@@ -277,7 +282,7 @@ def run_b200(args, rank, world, local):
                 if world == 1:
                     if record:
                         e0.record(stream)
-                    sweeps.nn_sweep(U, va, out=vb)
+                    sweeps.nn_sweep(U, va, out=vb, mode=args.mode)
                     if record:
                         e1.record(stream)
                         dominant_events.append((e0, e1))
@@ -297,7 +302,7 @@ def run_b200(args, rank, world, local):
         del U_aos
         acc = Field(lat, "mat", tdt, dev)
         bytes_per_launch = lat.volume * LINK_BYTES[args.dtype]
-        mode = os.environ.get("SU3G_LINK_MODE", "fma")
+        mode = args.mode
 
         def step(record=False):
             if record:
@@ -415,6 +420,7 @@ def run_b200(args, rank, world, local):
         "scaling": "weak" if args.workload == "nn-weak" else ("strong" if args.workload == "nn-strong" else "weak"),
         "vs_baseline": None,
         "dtype": args.dtype,
+        "arithmetic": args.mode if cfg["kind"] in ("nn", "link") else "exact",
         "data": "synthetic (seeded SU(3) Gram-Schmidt links + complex-Gaussian vectors, generated on device)",
         "config": {
             "workload": cfg["name"],
@@ -480,7 +486,7 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
 
     from paper_1309_0551_b200 import inputs, sweeps
     from paper_1309_0551_b200.lattice import Field, Lattice4D
-    from paper_1309_0551_b200.slab import SlabSweep
+    from paper_1309_0551_b200.slab import CudaSlabKernels, SlabSweep
 
     steps = max(3, min(args.steps, 10))
     if cfg["kind"] == "nn":
@@ -494,7 +500,7 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
         v_d = torch.empty_like(v_h, device=dev)
         Uf = Field(lat, "mat4", tdt, dev)
         va, vb = Field(lat, "vec", tdt, dev), Field(lat, "vec", tdt, dev)
-        slab = SlabSweep(Uf)
+        slab = SlabSweep(Uf, kernels=CudaSlabKernels(args.mode))
 
         def step():
             U_d.copy_(U_h, non_blocking=True)
@@ -517,7 +523,7 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
         U_d = torch.empty_like(U_h, device=dev)
         o_d = torch.empty_like(out_h, device=dev)
         Uf = Field(lat, "mat4", tdt, dev)
-        mode = os.environ.get("SU3G_LINK_MODE", "fma")
+        mode = args.mode
 
         def step():
             U_d.copy_(U_h, non_blocking=True)

@@ -118,17 +118,23 @@ SU3G_API int su3g_soa_to_aos_f64(const double *soa, double *aos, int64_t sites_p
  *   w_lo (6*F reals)           = U_t(x)^dag v(x) on the slice before slice 0
  *        (computed by its owner with su3g_nn_halo_w), or NULL -> periodic.
  * Only slices t in [t_begin, t_end) of `out` are written (interior/boundary
- * split for overlapping a halo exchange).                                   */
+ * split for overlapping a halo exchange).
+ * mode SU3G_EXACT: reference association, bit-identical to the composed
+ * reference; SU3G_FMA: FMA chains in the products (north-star tolerance).
+ * Use the same mode for su3g_nn_halo_w so a sharded sweep stays bit-identical
+ * to the single-GPU one.                                                    */
 SU3G_API int su3g_nn_sweep_f32(const float *U, const float *v, float *out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
-                      int32_t t_begin, int32_t t_end, const float *v_hi, const float *w_lo, su3g_stream_t stream);
+                      int32_t t_begin, int32_t t_end, const float *v_hi, const float *w_lo, int32_t mode,
+                      su3g_stream_t stream);
 SU3G_API int su3g_nn_sweep_f64(const double *U, const double *v, double *out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
-                      int32_t t_begin, int32_t t_end, const double *v_hi, const double *w_lo, su3g_stream_t stream);
+                      int32_t t_begin, int32_t t_end, const double *v_hi, const double *w_lo, int32_t mode,
+                      su3g_stream_t stream);
 /* w_face = U_t(x)^dag v(x) on the LAST local t-slice (the halo a t-slab sends
  * to its +t neighbour; 6*F reals, SoA face) */
 SU3G_API int su3g_nn_halo_w_f32(const float *U, const float *v, float *w_face, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
-                       su3g_stream_t stream);
+                       int32_t mode, su3g_stream_t stream);
 SU3G_API int su3g_nn_halo_w_f64(const double *U, const double *v, double *w_face, int32_t nx, int32_t ny, int32_t nz,
-                       int32_t nt, su3g_stream_t stream);
+                       int32_t nt, int32_t mode, su3g_stream_t stream);
 
 /* ---- link-product sweep (BASELINE configs[3]) ------------------------------
  * acc(x) = sum over (mu,nu) in (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) of

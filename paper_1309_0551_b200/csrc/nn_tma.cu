@@ -135,7 +135,7 @@ struct Geo {
 
 // CNX/CBY/CBZ > 0: block geometry fixed at compile time (halos present in y and z),
 // so every shared-memory offset is an immediate; 0: runtime geometry.
-template <typename T, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
+template <typename T, bool FUSED, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
 __global__ void __launch_bounds__(NTHR, 1)
     k_nn_tma(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
              const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             T u[18], vp[6];
             ld_soa<T, 18>(U + (int64_t(tp) * 72 + 54) * F, F, s3, u);
             ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vp);
-            adj_mat_vec<T>(u, vp, wt);
+            amv<T, FUSED>(u, vp, wt);
         }
 
         for (int t = t0; t < t1; ++t, ++k) {
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                 for (int q = 0; q < 18; ++q) uh[q] = st[ub + q * hp + jj];
 #pragma unroll
                 for (int q = 0; q < 6; ++q) vh[q] = st[vb + q * hp + jj];
-                adj_mat_vec<T>(uh, vh, wh);
+                amv<T, FUSED>(uh, vh, wh);
                 const int xo = isy ? g.xhy() : g.xhz();
 #pragma unroll
                 for (int q = 0; q < 6; ++q) xb[xo + q * hp + jj] = wh[q];
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                 T w[6];
 #pragma unroll
                 for (int mu = 0; mu < 3; ++mu) {
-                    adj_mat_vec<T>(u + 18 * mu, vc, w);
+                    amv<T, FUSED>(u + 18 * mu, vc, w);
 #pragma unroll
                     for (int q = 0; q < 6; ++q) xb[g.xw() + (6 * mu + q) * NTHR + tid] = w[q];
                 }
@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(NTHR, 1)
                 for (int q = 0; q < 6; ++q) xb[g.xv() + q * NTHR + tid] = vc[q];
             }
             T wt_next[6], f3[6];
-            adj_mat_vec<T>(ut, vc, wt_next);
-            mat_vec<T>(ut, vnext, f3);  // forward +t term, summed last
+            amv<T, FUSED>(ut, vc, wt_next);
+            mv<T, FUSED>(ut, vnext, f3);  // forward +t term, summed last
             named_sync<NTHR>();
 
             // forward terms (add_su3_vector chain: ((f0 + f1) + f2) + f3)
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(NTHR, 1)
                 T nb[6], f[6];
 #pragma unroll
                 for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + ix_up];
-                mat_vec<T>(u, nb, acc);
+                mv<T, FUSED>(u, nb, acc);
                 if (iy_up >= 0) {
 #pragma unroll
                     for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + iy_up];
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
                     for (int q = 0; q < 6; ++q) nb[q] = st[g.hvyu() + q * g.HY + (-1 - iy_up)];
                 }
-                mat_vec<T>(u + 18, nb, f);
+                mv<T, FUSED>(u + 18, nb, f);
 #pragma unroll
                 for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
                 if (iz_up >= 0) {
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
                     for (int q = 0; q < 6; ++q) nb[q] = st[g.hvzu() + q * g.HZ + (-1 - iz_up)];
                 }
-                mat_vec<T>(u + 36, nb, f);
+                mv<T, FUSED>(u + 36, nb, f);
 #pragma unroll
                 for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
 #pragma unroll
@@ -432,7 +432,7 @@ bool tma_shape(int nx, int ny, int nz, int nthr, int& BY, int& BZ) {
 
 }  // namespace
 
-template <typename T, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
+template <typename T, bool FUSED, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
 static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                    const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st) {
     const int HY = (BY == ny) ? 0 : nx * BZ, HZ = (BZ == nz) ? 0 : nx * BY;
@@ -456,7 +456,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     const size_t smem = (STAGES * stage + xsize) * sizeof(T) + 2 * STAGES * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    cudaFuncSetAttribute(k_nn_tma<T, NTHR, STAGES, CNX, CBY, CBZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     TmaParams p{};
     p.nx = nx; p.ny = ny; p.nz = nz; p.nt = nt;
     p.F = int64_t(nx) * ny * nz;
@@ -469,13 +469,13 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
-    k_nn_tma<T, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
+    k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     return check_launch("nn_sweep(tma)");
 }
 
 template <typename T>
 int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
-                  const T* v_hi, const T* w_lo, cudaStream_t st) {
+                  const T* v_hi, const T* w_lo, int mode, cudaStream_t st) {
     constexpr int NTHR = sizeof(T) == 4 ? 256 : 128;
     if ((nx * int(sizeof(T))) % 16 != 0 || nx > 256) return 1;
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
@@ -483,14 +483,18 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (!tma_shape(nx, ny, nz, NTHR, BY, BZ)) return 1;
     if constexpr (sizeof(T) == 4) {  // the 64-wide production geometry, specialised
         if (nx == 64 && BY == 2 && BZ == 2 && ny > 2 && nz > 2)
-            return run_tma<T, NTHR, 2, 64, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+            return mode == SU3G_FMA
+                       ? run_tma<T, true, NTHR, 2, 64, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
+                       : run_tma<T, false, NTHR, 2, 64, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
     }
-    return run_tma<T, NTHR, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+    return mode == SU3G_FMA
+               ? run_tma<T, true, NTHR, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
+               : run_tma<T, false, NTHR, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
 }
 
 template int launch_nn_tma<float>(const float*, const float*, float*, int, int, int, int, int, int, const float*,
-                                  const float*, cudaStream_t);
+                                  const float*, int, cudaStream_t);
 template int launch_nn_tma<double>(const double*, const double*, double*, int, int, int, int, int, int,
-                                   const double*, const double*, cudaStream_t);
+                                   const double*, const double*, int, cudaStream_t);
 
 }  // namespace su3g

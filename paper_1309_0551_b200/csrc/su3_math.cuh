@@ -168,6 +168,34 @@ __device__ __forceinline__ void cdot_fma(PF p, QF q, T& re, T& im) {
 }
 
 template <typename T>
+__device__ __forceinline__ void mat_vec_fma(const T* a, const T* b, T* c) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        cdot_fma<T, PLAIN, 3>([&](int j, int r) { return a[(3 * i + j) * 2 + r]; },
+                              [&](int j, int r) { return b[2 * j + r]; }, c[2 * i], c[2 * i + 1]);
+}
+
+template <typename T>
+__device__ __forceinline__ void adj_mat_vec_fma(const T* a, const T* b, T* c) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        cdot_fma<T, CONJ_P, 3>([&](int j, int r) { return a[(3 * j + i) * 2 + r]; },
+                               [&](int j, int r) { return b[2 * j + r]; }, c[2 * i], c[2 * i + 1]);
+}
+
+// compile-time switch between the exact (reference association) and FMA forms
+template <typename T, bool FUSED>
+__device__ __forceinline__ void mv(const T* a, const T* b, T* c) {
+    if constexpr (FUSED) mat_vec_fma<T>(a, b, c);
+    else mat_vec<T>(a, b, c);
+}
+template <typename T, bool FUSED>
+__device__ __forceinline__ void amv(const T* a, const T* b, T* c) {
+    if constexpr (FUSED) adj_mat_vec_fma<T>(a, b, c);
+    else adj_mat_vec<T>(a, b, c);
+}
+
+template <typename T>
 __device__ __forceinline__ void mat_nn_fma(const T* a, const T* b, T* c) {
 #pragma unroll
     for (int i = 0; i < 3; ++i)

@@ -19,7 +19,7 @@ namespace su3g {
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256)
     k_nn_sweep(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin, int t_end,
                const T* __restrict__ v_hi, const T* __restrict__ w_lo) {
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(256)
         } else {
             ld_soa<T, 6>(v, F, s3, vn);
         }
-        mat_vec<T>(u, vn, f);
+        mv<T, FUSED>(u, vn, f);
 #pragma unroll
         for (int k = 0; k < 6; ++k) acc[k] = (mu == 0) ? f[k] : xadd(acc[k], f[k]);
     }
@@ -60,13 +60,13 @@ __global__ void __launch_bounds__(256)
             const int64_t d = step3(g, x, y, z, mu, -1);
             ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, d, u);
             ld_soa<T, 6>(v + int64_t(t) * 6 * F, F, d, vn);
-            adj_mat_vec<T>(u, vn, w);
+            amv<T, FUSED>(u, vn, w);
         } else if (t > 0 || w_lo == nullptr) {
             const int tp = (t > 0) ? t - 1 : g.nt - 1;
             T u[18], vn[6];
             ld_soa<T, 18>(U + (int64_t(tp) * 72 + 3 * 18) * F, F, s3, u);
             ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vn);
-            adj_mat_vec<T>(u, vn, w);
+            amv<T, FUSED>(u, vn, w);
         } else {
             ld_soa<T, 6>(w_lo, F, s3, w);
         }
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256)
     for (int k = 0; k < 6; ++k) out[(int64_t(t) * 6 + k) * F + s3] = acc[k];
 }
 
-template <typename T>
+template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256)
     k_nn_halo_w(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ w_face, Geom g) {
     const int64_t s3 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256)
     T u[18], vn[6], w[6];
     ld_soa<T, 18>(U + (int64_t(t) * 72 + 3 * 18) * g.F, g.F, s3, u);
     ld_soa<T, 6>(v + int64_t(t) * 6 * g.F, g.F, s3, vn);
-    adj_mat_vec<T>(u, vn, w);
+    amv<T, FUSED>(u, vn, w);
 #pragma unroll
     for (int k = 0; k < 6; ++k) w_face[k * g.F + s3] = w[k];
 }
@@ -212,7 +212,7 @@ struct WalkParams {
     int64_t nitems;  // nblocks * ceil((t_end - t_begin) / chunk), chunk-major
 };
 
-template <typename T, int MINB>
+template <typename T, bool FUSED, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw);
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
                 T u[18], vp[6];
                 ld_soa<T, 18>(p.U + (int64_t(tp) * 72 + 54) * F, F, s3, u);
                 ld_soa<T, 6>(p.v + int64_t(tp) * 6 * F, F, s3, vp);
-                adj_mat_vec<T>(u, vp, wt);
+                amv<T, FUSED>(u, vp, wt);
             }
         }
       for (int t = t0; t < t1; ++t) {
@@ -284,14 +284,14 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
                 u[k] = (mu == 1 || mu == 2) ? __ldg(Ut + (18 * mu + k) * F) : ld_stream(Ut + (18 * mu + k) * F, pol);
             if (mu < 3) {
                 T wm[6];
-                adj_mat_vec<T>(u, vc, wm);
+                amv<T, FUSED>(u, vc, wm);
 #pragma unroll
                 for (int k = 0; k < 6; ++k) sb[(6 * mu + k) * nthr + tid] = wm[k];
                 ld_soa<T, 6>(vt, F, s3_up[mu], nb);  // v(x+mu, t): L1 hit (this CTA read it as v(t+1) last step)
-                mat_vec<T>(u, nb, f);
+                mv<T, FUSED>(u, nb, f);
             } else {
-                adj_mat_vec<T>(u, vc, wt_next);
-                mat_vec<T>(u, vn, f);
+                amv<T, FUSED>(u, vc, wt_next);
+                mv<T, FUSED>(u, vn, f);
             }
 #pragma unroll
             for (int k = 0; k < 6; ++k) acc[k] = (mu == 0) ? f[k] : xadd(acc[k], f[k]);
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
             T uh[18], vh[6], wh[6];
             ld_soa<T, 18>(p.U + (int64_t(t) * 72 + 18) * F, F, s3_ydn, uh);
             ld_soa<T, 6>(vt, F, s3_ydn, vh);
-            adj_mat_vec<T>(uh, vh, wh);
+            amv<T, FUSED>(uh, vh, wh);
 #pragma unroll
             for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], wh[k]);
         }
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256, MINB) k_nn_walk(WalkParams<T> p) {
             T uh[18], vh[6], wh[6];
             ld_soa<T, 18>(p.U + (int64_t(t) * 72 + 36) * F, F, s3_zdn, uh);
             ld_soa<T, 6>(vt, F, s3_zdn, vh);
-            adj_mat_vec<T>(uh, vh, wh);
+            amv<T, FUSED>(uh, vh, wh);
 #pragma unroll
             for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], wh[k]);
         }
@@ -369,20 +369,22 @@ static std::atomic<int> g_link_variant{0};  // 0 auto (block walk), 1 generic
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
-                       const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st) {
+                       const T* v_hi, const T* w_lo, int BY, int BZ, int mode, cudaStream_t st) {
     constexpr int MINB = 2;
     WalkParams<T> p{U, v, out, v_hi, w_lo, nx, ny, nz, nt, int64_t(nx) * ny * nz, BY, BZ, ny / BY, t_begin, t_end,
                     0, 0, 0};
     p.nblocks = int64_t(ny / BY) * (nz / BZ);
     const int nthr = nx * BY * BZ;
     const size_t smem = size_t(2) * 18 * nthr * sizeof(T);
-    static int per_sm_cache[64][2] = {};
+    static int per_sm_cache[64][2][2] = {};
     const DeviceInfo& di = device_info();
-    int& per_sm = per_sm_cache[di.device & 63][sizeof(T) == 8];
+    const bool fused = mode == SU3G_FMA;
+    int& per_sm = per_sm_cache[di.device & 63][sizeof(T) == 8][fused];
     if (per_sm == 0) {
-        cudaFuncSetAttribute(k_nn_walk<T, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 18 * 256 * int(sizeof(T)));
+        auto kern = fused ? k_nn_walk<T, true, MINB> : k_nn_walk<T, false, MINB>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 18 * 256 * int(sizeof(T)));
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_nn_walk<T, MINB>, 256, 2 * 18 * 256 * sizeof(T));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 2 * 18 * 256 * sizeof(T));
         per_sm = b > 0 ? b : 1;
     }
     // blocks of fewer than 256 threads fit proportionally more CTAs per SM
@@ -390,7 +392,8 @@ static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, i
     p.chunk = pick_chunk(p.nblocks, t_end - t_begin, static_cast<int>(std::min<int64_t>(slots, 1 << 20)));
     p.nitems = p.nblocks * ((t_end - t_begin + p.chunk - 1) / p.chunk);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(p.nitems, slots));
-    k_nn_walk<T, MINB><<<static_cast<unsigned>(grid), nthr, smem, st>>>(p);
+    if (fused) k_nn_walk<T, true, MINB><<<static_cast<unsigned>(grid), nthr, smem, st>>>(p);
+    else k_nn_walk<T, false, MINB><<<static_cast<unsigned>(grid), nthr, smem, st>>>(p);
     return check_launch("nn_sweep(walk)");
 }
 
@@ -401,7 +404,8 @@ static int check_geom(const char* what, int nx, int ny, int nz, int nt) {
 
 template <typename T>
 static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
-                    const T* v_hi, const T* w_lo, cudaStream_t st) {
+                    const T* v_hi, const T* w_lo, int mode, cudaStream_t st) {
+    if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("nn_sweep: mode must be SU3G_EXACT or SU3G_FMA");
     if (int rc = check_geom("nn_sweep", nx, ny, nz, nt)) return rc;
     if (t_begin < 0 || t_end > nt || t_begin > t_end) return fail_invalid("nn_sweep: bad t range");
     if (!U || !v || !out) return fail_invalid("nn_sweep: null pointer");
@@ -413,25 +417,30 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 64;
     const bool auto_walk = variant == 0 && sizeof(T) == 4;
     if (auto_tma || variant == 3) {
-        const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+        const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
         if (rc != 1) return rc;
         if (variant == 3) return fail_invalid("nn_sweep: TMA kernel not applicable to this lattice");
     }
     if ((auto_walk || variant == 2) && walk_shape(nx, ny, nz, 256, BY, BZ))
-        return launch_walk<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+        return launch_walk<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, mode, st);
     if (variant == 2) return fail_invalid("nn_sweep: walk kernel not applicable to this lattice");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int64_t n = int64_t(t_end - t_begin) * g.F;
-    k_nn_sweep<T><<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo);
+    const unsigned gs = static_cast<unsigned>((n + 255) / 256);
+    if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo);
+    else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo);
     return check_launch("nn_sweep");
 }
 
 template <typename T>
-static int nn_halo_w(const T* U, const T* v, T* w, int nx, int ny, int nz, int nt, cudaStream_t st) {
+static int nn_halo_w(const T* U, const T* v, T* w, int nx, int ny, int nz, int nt, int mode, cudaStream_t st) {
+    if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("nn_halo_w: mode must be SU3G_EXACT or SU3G_FMA");
     if (int rc = check_geom("nn_halo_w", nx, ny, nz, nt)) return rc;
     if (!U || !v || !w) return fail_invalid("nn_halo_w: null pointer");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
-    k_nn_halo_w<T><<<static_cast<unsigned>((g.F + 255) / 256), 256, 0, st>>>(U, v, w, g);
+    const unsigned gs = static_cast<unsigned>((g.F + 255) / 256);
+    if (mode == SU3G_FMA) k_nn_halo_w<T, true><<<gs, 256, 0, st>>>(U, v, w, g);
+    else k_nn_halo_w<T, false><<<gs, 256, 0, st>>>(U, v, w, g);
     return check_launch("nn_halo_w");
 }
 
@@ -492,20 +501,24 @@ int su3g_set_option(const char* name, int64_t value) {
 }
 
 int su3g_nn_sweep_f32(const float* U, const float* v, float* out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
-                      int32_t t_begin, int32_t t_end, const float* v_hi, const float* w_lo, su3g_stream_t st) {
-    return nn_sweep<float>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, reinterpret_cast<cudaStream_t>(st));
+                      int32_t t_begin, int32_t t_end, const float* v_hi, const float* w_lo, int32_t mode,
+                      su3g_stream_t st) {
+    return nn_sweep<float>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode,
+                           reinterpret_cast<cudaStream_t>(st));
 }
 int su3g_nn_sweep_f64(const double* U, const double* v, double* out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
-                      int32_t t_begin, int32_t t_end, const double* v_hi, const double* w_lo, su3g_stream_t st) {
-    return nn_sweep<double>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, reinterpret_cast<cudaStream_t>(st));
+                      int32_t t_begin, int32_t t_end, const double* v_hi, const double* w_lo, int32_t mode,
+                      su3g_stream_t st) {
+    return nn_sweep<double>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode,
+                            reinterpret_cast<cudaStream_t>(st));
 }
 int su3g_nn_halo_w_f32(const float* U, const float* v, float* w, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
-                       su3g_stream_t st) {
-    return nn_halo_w<float>(U, v, w, nx, ny, nz, nt, reinterpret_cast<cudaStream_t>(st));
+                       int32_t mode, su3g_stream_t st) {
+    return nn_halo_w<float>(U, v, w, nx, ny, nz, nt, mode, reinterpret_cast<cudaStream_t>(st));
 }
 int su3g_nn_halo_w_f64(const double* U, const double* v, double* w, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
-                       su3g_stream_t st) {
-    return nn_halo_w<double>(U, v, w, nx, ny, nz, nt, reinterpret_cast<cudaStream_t>(st));
+                       int32_t mode, su3g_stream_t st) {
+    return nn_halo_w<double>(U, v, w, nx, ny, nz, nt, mode, reinterpret_cast<cudaStream_t>(st));
 }
 int su3g_link_product_f32(const float* U, float* acc, int32_t nx, int32_t ny, int32_t nz, int32_t nt, float s,
                           int32_t mode, su3g_stream_t st) {

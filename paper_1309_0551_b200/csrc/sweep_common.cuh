@@ -63,6 +63,6 @@ inline int pick_chunk(int64_t nblocks, int nt_range, int G) {
 // 1 when the lattice does not meet its constraints (caller falls back).
 template <typename T>
 int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
-                  const T* v_hi, const T* w_lo, cudaStream_t st);
+                  const T* v_hi, const T* w_lo, int mode, cudaStream_t st);
 
 }  // namespace su3g

@@ -37,6 +37,9 @@ TAG_W = 12
 class CudaSlabKernels:
     """Device compute for one slab: libsu3g kernels on t-sliced SoA fields."""
 
+    def __init__(self, mode: str = "exact"):
+        self.mode = mode
+
     def alloc_face(self, v: Field) -> torch.Tensor:
         return torch.empty((6, v.lattice.slice_sites), dtype=v.dtype, device=v.device)
 
@@ -44,10 +47,10 @@ class CudaSlabKernels:
         return v.face(0)
 
     def halo_w(self, U: Field, v: Field, w: torch.Tensor) -> None:
-        sweeps.nn_halo_w(U, v, w)
+        sweeps.nn_halo_w(U, v, w, mode=self.mode)
 
     def sweep(self, U: Field, v: Field, out: Field, t_range, v_hi, w_lo) -> None:
-        sweeps.nn_sweep(U, v, out=out, t_range=t_range, v_hi=v_hi, w_lo=w_lo)
+        sweeps.nn_sweep(U, v, out=out, t_range=t_range, v_hi=v_hi, w_lo=w_lo, mode=self.mode)
 
     def nt(self, v: Field) -> int:
         return v.lattice.nt

@@ -31,11 +31,20 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
-def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=None, w_lo=None) -> Field:
+def _mode(mode: str) -> int:
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {sorted(MODES)}")
+    return MODES[mode]
+
+
+def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=None, w_lo=None,
+             mode: str = "exact") -> Field:
     """One application of D on the slices t in t_range (default: all).
 
     v_hi / w_lo: (6, F) SoA halo faces for a t-slab (see include/su3g.h); None
-    closes t periodically on the local lattice.
+    closes t periodically on the local lattice.  mode "exact" (default) is
+    bit-identical to the composed reference; "fma" uses FMA chains in the SU(3)
+    products (north-star tolerance).
     """
     if U.kind != "mat4" or v.kind != "vec":
         raise ValueError("nn_sweep needs U of kind 'mat4' and v of kind 'vec'")
@@ -47,27 +56,27 @@ def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=No
     t0, t1 = (0, lat.nt) if t_range is None else t_range
     _lib.call(
         f"su3g_nn_sweep_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
-        lat.nx, lat.ny, lat.nz, lat.nt, t0, t1, _ptr(v_hi), _ptr(w_lo), _stream(U.device),
+        lat.nx, lat.ny, lat.nz, lat.nt, t0, t1, _ptr(v_hi), _ptr(w_lo), _mode(mode), _stream(U.device),
     )
     return out
 
 
-def nn_halo_w(U: Field, v: Field, w_face: torch.Tensor) -> torch.Tensor:
+def nn_halo_w(U: Field, v: Field, w_face: torch.Tensor, mode: str = "exact") -> torch.Tensor:
     """w = U_t^dag v on the last local t-slice -> (6, F) SoA face (sent to the +t neighbour)."""
     lat = U.lattice
     _lib.call(
         f"su3g_nn_halo_w_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), w_face.data_ptr(),
-        lat.nx, lat.ny, lat.nz, lat.nt, _stream(U.device),
+        lat.nx, lat.ny, lat.nz, lat.nt, _mode(mode), _stream(U.device),
     )
     return w_face
 
 
-def nn_apply(U: Field, v: Field, applications: int, scratch: Field | None = None) -> Field:
+def nn_apply(U: Field, v: Field, applications: int, scratch: Field | None = None, mode: str = "exact") -> Field:
     """v <- D v, `applications` times, ping-ponging between two buffers; returns the final field."""
     a = v
     b = scratch if scratch is not None else v.empty_like()
     for _ in range(applications):
-        nn_sweep(U, a, out=b)
+        nn_sweep(U, a, out=b, mode=mode)
         a, b = b, a
     return a
 
@@ -102,12 +111,12 @@ def _back(t: torch.Tensor, like):
     return t if like.is_cuda else t.cpu()
 
 
-def nn_sweep_aos(U, v, dims, applications: int = 1):
+def nn_sweep_aos(U, v, dims, applications: int = 1, mode: str = "exact"):
     """D^applications v for reference-layout U (V,4,3,3,2) and v (V,3,2); returns v's array family."""
     lat = Lattice4D.from_dims(dims)
     Uf = Field.from_aos(lat, "mat4", U)
     vf = Field.from_aos(lat, "vec", v)
-    res = nn_apply(Uf, vf, applications)
+    res = nn_apply(Uf, vf, applications, mode=mode)
     return _back(res.to_aos(), v)
 
 

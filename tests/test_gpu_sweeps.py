@@ -249,3 +249,36 @@ def test_link_product_variants_bitwise(variant, dims, precision):
         assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
     finally:
         _lib.set_option("link_variant", 0)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3], ids=["generic", "walk", "tma"])
+@pytest.mark.parametrize("dims", [(64, 4, 4, 6), (32, 8, 4, 5), (8, 8, 8, 8)])
+def test_nn_fma_mode_within_tolerance(variant, dims, precision):
+    """SU3G_FMA arithmetic: within the north-star tolerance of the reference, and every kernel variant
+    (and the sharded halo path) agrees bit for bit among themselves in that mode."""
+    from paper_1309_0551_b200 import _lib
+
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(8000 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    want = coracle.nn_sweep(U, v, dims)
+    tol = 1e-5 if dt == np.float32 else 1e-12
+    _lib.set_option("nn_variant", 1)
+    try:
+        ref_fma = sweeps.nn_sweep_aos(U, v, dims, mode="fma")
+    finally:
+        _lib.set_option("nn_variant", 0)
+    assert floored_rel_err(ref_fma, want) <= tol
+    _lib.set_option("nn_variant", variant)
+    try:
+        try:
+            got = sweeps.nn_sweep_aos(U, v, dims, mode="fma")
+        except ValueError as e:
+            if "not applicable" in str(e):
+                pytest.skip(f"variant {variant} not applicable to {dims}")
+            raise
+        assert np.array_equal(got, ref_fma)
+    finally:
+        _lib.set_option("nn_variant", 0)

@@ -45,7 +45,8 @@ def test_invalid_arguments_rejected_without_touching_the_device():
     # negative site count, null pointers -> SU3G_EINVAL before any CUDA call
     assert lib.su3g_mult_su3_mat_vec_f32(None, None, None, -1, None) == _lib.SU3G_EINVAL
     assert b"negative" in lib.su3g_last_error()
-    assert lib.su3g_nn_sweep_f32(None, None, None, 0, 4, 4, 4, 0, 4, None, None, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_nn_sweep_f32(None, None, None, 0, 4, 4, 4, 0, 4, None, None, 0, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_nn_sweep_f32(None, None, None, 4, 4, 4, 4, 0, 4, None, None, 9, None) == _lib.SU3G_EINVAL
     assert lib.su3g_link_product_f64(None, None, 4, 4, 4, 4, 0.5, 7, None) == _lib.SU3G_EINVAL
     with pytest.raises(ValueError):
         _lib.check(_lib.SU3G_EINVAL, "x")
