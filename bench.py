@@ -266,28 +266,16 @@ def run_b200(args, rank, world, local):
         ntl = lat.nt
         if world == 1:
             per_launch_sites = lat.volume
-            launches_per_app = 1
         else:
             per_launch_sites = max(ntl - 2, 0) * lat.slice_sites
-            launches_per_app = 2 + (1 if ntl > 2 else 0) + 1  # interior + 2 boundary + halo pack
+        launches_per_app = slab.launches_per_apply()
         bytes_per_launch = per_launch_sites * NN_BYTES[args.dtype]
         apps = cfg["apps"]
 
         def step(record=False):
             nonlocal va, vb
             for _ in range(apps):
-                if record:
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                if world == 1:
-                    if record:
-                        e0.record(stream)
-                    sweeps.nn_sweep(U, va, out=vb, mode=args.mode)
-                    if record:
-                        e1.record(stream)
-                        dominant_events.append((e0, e1))
-                else:
-                    _apply_sharded(slab, va, vb, record, dominant_events, stream)
+                slab.apply(va, vb, timer=(lambda: _EventTimer(stream, dominant_events)) if record else None)
                 va, vb = vb, va
 
         launches_per_step = apps * launches_per_app
@@ -454,30 +442,24 @@ def run_b200(args, rank, world, local):
     return line
 
 
-def _apply_sharded(slab, v, out, record, events, stream):
-    """slab.apply with CUDA events around the interior (dominant) kernel."""
-    import torch
+class _EventTimer:
+    """CUDA events around one kernel launch on `stream` (the dominant kernel's duration)."""
 
-    from paper_1309_0551_b200.slab import boundary_ranges
+    def __init__(self, stream, sink):
+        import torch
 
-    k = slab.k
-    w_send, v_hi, w_lo = slab._buffers(v)
-    k.halo_w(slab.U, v, w_send)
-    reqs = slab.exchange(v, w_send, v_hi, w_lo)
-    interior, edges = boundary_ranges(k.nt(v))
-    if interior is not None:
-        if record:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-        k.sweep(slab.U, v, out, interior, v_hi, w_lo)
-        if record:
-            e1.record(stream)
-            events.append((e0, e1))
-    for r in reqs:
-        r.wait()
-    for rng in edges:
-        k.sweep(slab.U, v, out, rng, v_hi, w_lo)
+        self.stream, self.sink = stream, sink
+        self.e0 = torch.cuda.Event(enable_timing=True)
+        self.e1 = torch.cuda.Event(enable_timing=True)
+
+    def __enter__(self):
+        self.e0.record(self.stream)
+        return self
+
+    def __exit__(self, *exc):
+        self.e1.record(self.stream)
+        self.sink.append((self.e0, self.e1))
+        return False
 
 
 def measure_e2e(args, cfg, rank, world, dev, tdt, stream):

@@ -481,7 +481,11 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
     int BY = 0, BZ = 0;
     if (!tma_shape(nx, ny, nz, NTHR, BY, BZ)) return 1;
-    if constexpr (sizeof(T) == 4) {  // the 64-wide production geometry, specialised
+    if constexpr (sizeof(T) == 4) {  // the production geometries, specialised
+        if (nx == 32 && BY == 2 && BZ == 4 && ny > 2 && nz > 4)
+            return mode == SU3G_FMA
+                       ? run_tma<T, true, NTHR, 2, 32, 2, 4>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
+                       : run_tma<T, false, NTHR, 2, 32, 2, 4>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
         if (nx == 64 && BY == 2 && BZ == 2 && ny > 2 && nz > 2)
             return mode == SU3G_FMA
                        ? run_tma<T, true, NTHR, 2, 64, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)

@@ -365,7 +365,7 @@ static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk, 3 TMA walk
-static std::atomic<int> g_link_variant{0};  // 0 auto (block walk), 1 generic
+static std::atomic<int> g_link_variant{0};  // 0 auto (= generic, measured faster), 1 generic, 2 block walk
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
@@ -414,7 +414,7 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const int variant = g_nn_variant.load();
     // auto policy (measured on B200, profiles/r01): f32 with full-width 64+ x rows -> TMA walk;
     // other f32 lattices -> register walk; f64 -> generic (fewest registers, best occupancy)
-    const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 64;
+    const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 32;
     const bool auto_walk = variant == 0 && sizeof(T) == 4;
     if (auto_tma || variant == 3) {
         const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
@@ -451,7 +451,7 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("link_product: mode must be SU3G_EXACT or SU3G_FMA");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     int BY = 0, BZ = 0;
-    if (g_link_variant.load() != 1 && walk_shape(nx, ny, nz, 128, BY, BZ)) {
+    if (g_link_variant.load() == 2 && walk_shape(nx, ny, nz, 128, BY, BZ)) {
         LinkWalk w{BY, BZ, ny / BY, int64_t(ny / BY) * (nz / BZ), 0, 0};
         const int nthr = nx * BY * BZ;
         static int per_sm_cache[64][2][2] = {};
@@ -493,7 +493,8 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 1) return fail_invalid("set_option: link_variant must be 0 (auto) or 1 (generic)");
+        if (value < 0 || value > 2)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (generic) or 2 (block walk)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -56,6 +56,18 @@ class CudaSlabKernels:
         return v.lattice.nt
 
 
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def _maybe(timer):
+    return timer() if timer is not None else _Null()
+
+
 def boundary_ranges(nt_local: int):
     """(interior range, boundary ranges) of local t-slices; halos only touch the boundary."""
     if nt_local <= 2:
@@ -103,22 +115,36 @@ class SlabSweep:
         ]
         return dist.batch_isend_irecv(ops)
 
-    def apply(self, v, out):
-        """out = D v on this slab (periodic in t across the ranks)."""
+    def apply(self, v, out, timer=None):
+        """out = D v on this slab (periodic in t across the ranks).
+
+        ``timer`` (optional) is a context-manager factory wrapped around the
+        dominant kernel launch -- the whole sweep on one rank, the interior
+        slices otherwise (bench.py records CUDA events with it).
+        """
         if self.world == 1:
-            self.k.sweep(self.U, v, out, (0, self.k.nt(v)), None, None)
+            with _maybe(timer):
+                self.k.sweep(self.U, v, out, (0, self.k.nt(v)), None, None)
             return out
         w_send, v_hi, w_lo = self._buffers(v)
         self.k.halo_w(self.U, v, w_send)
         reqs = self.exchange(v, w_send, v_hi, w_lo)
         interior, edges = boundary_ranges(self.k.nt(v))
         if interior is not None:
-            self.k.sweep(self.U, v, out, interior, v_hi, w_lo)
+            with _maybe(timer):
+                self.k.sweep(self.U, v, out, interior, v_hi, w_lo)
         for r in reqs:
             r.wait()
         for rng in edges:
             self.k.sweep(self.U, v, out, rng, v_hi, w_lo)
         return out
+
+    def launches_per_apply(self) -> int:
+        """Kernel launches of one application (halo pack + interior + boundary slices)."""
+        if self.world == 1:
+            return 1
+        interior, edges = boundary_ranges(self.k.nt(self.U))
+        return 1 + (interior is not None) + len(edges)
 
     def apply_n(self, v, scratch, applications: int):
         """v <- D v `applications` times (ping-pong); returns the buffer holding the result."""

@@ -189,3 +189,28 @@ def test_register_with_su3bench_plugin_registry():
             rb.BACKEND_NAMES = tuple(rb._BACKENDS)
     finally:
         sys.path.remove(ref)
+
+
+def test_bench_reference_arm_contract(capsys):
+    """bench.py --impl reference prints one JSON line with the contract keys (runs on CPU)."""
+    import json
+
+    import bench
+
+    bench.main(["--impl", "reference", "--steps", "1", "--warmup", "3"])
+    line = capsys.readouterr().out.strip().splitlines()[-1]
+    d = json.loads(line)
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "config", "impl", "cpu_baseline", "e2e"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["workload"].startswith("config5-weak")
+
+
+def test_bench_rejects_short_warmup():
+    import bench
+
+    with pytest.raises(SystemExit):
+        bench.parse_args(["--warmup", "2"])
