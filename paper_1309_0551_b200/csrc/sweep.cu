@@ -365,7 +365,7 @@ static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk, 3 TMA walk
-static std::atomic<int> g_link_variant{0};  // 0 auto (= generic, measured faster), 1 generic, 2 block walk
+static std::atomic<int> g_link_variant{0};  // 0 auto (ring), 1 generic, 2 block walk, 3 ring
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
@@ -451,7 +451,14 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("link_product: mode must be SU3G_EXACT or SU3G_FMA");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     int BY = 0, BZ = 0;
-    if (g_link_variant.load() == 2 && walk_shape(nx, ny, nz, 128, BY, BZ)) {
+    const int lv = g_link_variant.load();
+    if (lv == 0 || lv == 3) {
+        const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
+                                        : launch_link_ring<T, false>(U, acc, nx, ny, nz, nt, s, st);
+        if (rc != 1) return rc;
+        if (lv == 3) return fail_invalid("link_product: ring kernel not applicable to this lattice");
+    }
+    if (lv == 2 && walk_shape(nx, ny, nz, 128, BY, BZ)) {
         LinkWalk w{BY, BZ, ny / BY, int64_t(ny / BY) * (nz / BZ), 0, 0};
         const int nthr = nx * BY * BZ;
         static int per_sm_cache[64][2][2] = {};
@@ -493,8 +500,8 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 2)
-            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (generic) or 2 (block walk)");
+        if (value < 0 || value > 3)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

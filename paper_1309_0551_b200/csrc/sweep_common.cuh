@@ -65,4 +65,8 @@ template <typename T>
 int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                   const T* v_hi, const T* w_lo, int mode, cudaStream_t st);
 
+// cp.async-ring link product (link_ring.cu); 1 when the lattice does not fit its block shape.
+template <typename T, bool FUSED>
+int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
+
 }  // namespace su3g

@@ -232,8 +232,8 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
         _lib.set_option("no_such_option", 1)
 
 
-@pytest.mark.parametrize("variant", [0, 1], ids=["block-walk", "generic"])
-@pytest.mark.parametrize("dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5)])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "generic", "block-walk", "ring"])
+@pytest.mark.parametrize("dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4)])
 def test_link_product_variants_bitwise(variant, dims, precision):
     from paper_1309_0551_b200 import _lib
 
@@ -244,7 +244,13 @@ def test_link_product_variants_bitwise(variant, dims, precision):
     want = coracle.link_product(U, dims, 1 / 6)
     _lib.set_option("link_variant", variant)
     try:
-        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+        try:
+            got = sweeps.link_product_aos(U, dims, 1 / 6)
+        except ValueError as e:
+            if "not applicable" in str(e):
+                pytest.skip(f"link variant {variant} not applicable to {dims}")
+            raise
+        assert np.array_equal(got, want)
         tol = 1e-5 if dt == np.float32 else 1e-12
         assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
     finally:
