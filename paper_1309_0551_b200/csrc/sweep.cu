@@ -139,7 +139,7 @@ __device__ __forceinline__ void link_site(const T* __restrict__ U, T* __restrict
 }
 
 template <typename T, bool FUSED>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
     k_link_product(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s) {
     const int64_t site = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (site >= g.F * g.nt) return;
@@ -365,7 +365,7 @@ static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk, 3 TMA walk
-static std::atomic<int> g_link_variant{0};  // 0 auto (ring), 1 generic, 2 block walk, 3 ring
+static std::atomic<int> g_link_variant{0};  // 0 auto (= generic, measured fastest), 1 generic, 2 block walk, 3 ring
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
@@ -452,7 +452,7 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     int BY = 0, BZ = 0;
     const int lv = g_link_variant.load();
-    if (lv == 0 || lv == 3) {
+    if (lv == 3) {
         const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
                                         : launch_link_ring<T, false>(U, acc, nx, ny, nz, nt, s, st);
         if (rc != 1) return rc;
