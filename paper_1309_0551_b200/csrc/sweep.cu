@@ -139,7 +139,7 @@ __device__ __forceinline__ void link_site(const T* __restrict__ U, T* __restrict
 }
 
 template <typename T, bool FUSED>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(128)
     k_link_product(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s) {
     const int64_t site = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (site >= g.F * g.nt) return;
