@@ -363,11 +363,6 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f3[q]);
             }
-            mbar_arrive(&empty[s]);  // stage s fully read by this thread
-            if (tid == 0 && c2.valid) {  // refill it with step k + 2 once every thread is done
-                mbar_wait(&empty[s], static_cast<uint32_t>((k / STAGES) & 1));
-                issue(s, c2.blk, c2.t);
-            }
 
             // backward terms (sub_four_su3_vecs chain)
 #pragma unroll
@@ -402,7 +397,10 @@ __global__ void __launch_bounds__(NTHR, 1)
                 ut[q] = ut1[q];
                 ut1[q] = ut2[q];
             }
-            named_sync<NTHR>();  // exchange buffer free for the next step
+            named_sync<NTHR>();  // exchange buffer and stage s free for the next step
+            // refill stage s with step k + 2: every thread is past its last read of it, so
+            // no empty-barrier wait is needed (and warp 0 never stalls mid-step)
+            if (tid == 0 && c2.valid) issue(s, c2.blk, c2.t);
         }
     }
 }
