@@ -410,11 +410,6 @@ __global__ void __launch_bounds__(NTHR, 1)
                     vc[q] = vnext[q];
                     wt[q] = wt_next[q];
                 }
-    #pragma unroll
-                for (int q = 0; q < 18; ++q) {
-                    ut[q] = ut1[q];
-                    ut1[q] = ut2[q];
-                }
         }
         named_sync<NTHR>();  // exchange buffer and stage s free for the next step
         // refill stage s with step k + 2: every thread is past its last read of it, so no

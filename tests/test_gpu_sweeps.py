@@ -288,3 +288,29 @@ def test_nn_fma_mode_within_tolerance(variant, dims, precision):
         assert np.array_equal(got, ref_fma)
     finally:
         _lib.set_option("nn_variant", 0)
+
+
+@pytest.mark.parametrize("dims", [(32, 32, 64, 2), (64, 64, 16, 3), (32, 16, 16, 32), (64, 16, 16, 12)])
+def test_nn_tma_multi_item_schedules(dims, precision):
+    """Lattices with more work items than CTAs: every CTA walks several (block, t-chunk) items."""
+    from paper_1309_0551_b200 import _lib
+
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(9000 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    want = coracle.nn_sweep(U, v, dims)
+    for variant in (0, 2, 3):
+        _lib.set_option("nn_variant", variant)
+        try:
+            try:
+                got = sweeps.nn_sweep_aos(U, v, dims)
+            except ValueError as e:
+                if "not applicable" in str(e):
+                    continue
+                raise
+            bad = np.argwhere(np.any(got != want, axis=(1, 2)))
+            assert bad.size == 0, f"variant {variant}: {bad.size} wrong sites, first {bad[:5].ravel()}"
+        finally:
+            _lib.set_option("nn_variant", 0)
