@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libsu3g.so")
+LIB_PATH = os.environ.get("SU3G_LIB") or os.path.join(HERE, "lib", "libsu3g.so")  # SU3G_LIB: A/B builds
 HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "su3g.h")
 
 SU3G_OK = 0

@@ -140,9 +140,8 @@ __global__ void __launch_bounds__(NTHR, 1)
     k_nn_tma(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
              const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
              const __grid_constant__ CUtensorMap mapUzH, const __grid_constant__ CUtensorMap mapVyH,
-             const __grid_constant__ CUtensorMap mapVzH, const __grid_constant__ CUtensorMap mapWlo,
-             const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, const T* __restrict__ w_lo,
-             TmaParams p) {
+             const __grid_constant__ CUtensorMap mapVzH, const T* __restrict__ U, const T* __restrict__ v,
+             T* __restrict__ out, const T* __restrict__ w_lo, TmaParams p) {
     static_assert(STAGES == 2, "the refill of stage k%2 is step k+2 (two-step lookahead)");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     constexpr bool FIXED = CNX > 0;
@@ -224,18 +223,18 @@ __global__ void __launch_bounds__(NTHR, 1)
         return lx + int64_t(nx) * (y + int64_t(p.ny) * z);
     };
 
-    // Work sequence of this CTA: per item (block, t0..t1) one PROLOGUE step -- v(t0-1) (or
-    // the w_lo face) and v(t0) by TMA, U_t(t0-1) through the register pipeline -- then the
-    // real steps t0..t1-1.  Nothing is loaded synchronously: U_t of step k is requested two
-    // steps ahead (ut -> ut1 -> ut2), everything else arrives in the TMA stages.
+    // U_t of step k is loaded two steps ahead (registers ut -> ut1 -> ut2 pipeline); the
+    // cursor caches its site index so the per-step work has no 64-bit divisions
     struct Cursor {
         int64_t item, blk, s3;
-        int t, t0, t1;  // t == t0 - 1: prologue step
+        int t, t1;
         bool valid;
     };
     auto enter = [&](Cursor& c) {
-        item_range(p, c.item, c.blk, c.t0, c.t1);
-        c.t = c.t0 - 1;
+        int a0, a1;
+        item_range(p, c.item, c.blk, a0, a1);
+        c.t = a0;
+        c.t1 = a1;
         c.s3 = site_of(c.blk);
     };
     auto advance = [&](Cursor c) {
@@ -252,173 +251,156 @@ __global__ void __launch_bounds__(NTHR, 1)
         enter(c);
         return c;
     };
-    auto use_wlo = [&](const Cursor& c) { return c.t0 == 0 && w_lo != nullptr; };
-    auto prev_t = [&](const Cursor& c) { return c.t0 > 0 ? c.t0 - 1 : p.nt - 1; };
     auto load_ut = [&](const Cursor& c, T* r) {
-        if (!c.valid) return;
-        if (c.t < c.t0) {
-            if (!use_wlo(c)) ld_soa<T, 18>(U + (int64_t(prev_t(c)) * 72 + 54) * F, F, c.s3, r);
-        } else {
-            ld_soa<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, c.s3, r);
-        }
-    };
-    auto issue_step = [&](int s, const Cursor& c) {
-        if (c.t >= c.t0) {
-            issue(s, c.blk, c.t);
-            return;
-        }
-        const int y0 = static_cast<int>(c.blk % p.nby) * BY;
-        const int z0 = static_cast<int>(c.blk / p.nby) * BZ;
-        mbar_arrive_expect_tx(&full[s], uint32_t(12 * NTHR) * sizeof(T));
-        T* st = stage0 + s * SS;
-        if (use_wlo(c)) tma_load_4d(st + g.su(), &mapWlo, 0, y0, z0, 0, &full[s], pol_normal);
-        else tma_load_4d(st + g.su(), &mapV, 0, y0, z0, prev_t(c) * 6, &full[s], pol_normal);
-        tma_load_4d(st + g.sv(), &mapV, 0, y0, z0, c.t0 * 6, &full[s], pol_normal);
+        if (c.valid) ld_soa<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, c.s3, r);
     };
 
     T vc[6], wt[6], ut[18], ut1[18];
-    Cursor cur{static_cast<int64_t>(blockIdx.x), 0, 0, 0, 0, 0, static_cast<int64_t>(blockIdx.x) < p.nitems};
-    if (!cur.valid) return;
-    enter(cur);
-    Cursor ahead = cur;
-    if (tid == 0) issue_step(0, ahead);
-    load_ut(ahead, ut);
-    ahead = advance(ahead);
-    if (tid == 0 && ahead.valid) issue_step(1, ahead);
-    load_ut(ahead, ut1);
-    ahead = advance(ahead);  // -> step 2
-
-    for (int64_t k = 0; cur.valid; ++k, cur = advance(cur)) {
-        T ut2[18];
-        const Cursor c2 = ahead;  // step k + 2
-        load_ut(c2, ut2);
+    int64_t k = 0;
+    int64_t item = blockIdx.x;
+    int64_t blk = 0;
+    int t0 = 0, t1 = 0;
+    Cursor ahead{item, 0, 0, 0, 0, item < p.nitems};
+    if (ahead.valid) {
+        enter(ahead);
+        if (tid == 0) issue(0, ahead.blk, ahead.t);
+        load_ut(ahead, ut);
         ahead = advance(ahead);
-        const int s = static_cast<int>(k % STAGES);
-        mbar_wait(&full[s], static_cast<uint32_t>((k / STAGES) & 1));
-        const T* st = stage0 + s * SS;
+        if (tid == 0 && ahead.valid && STAGES > 1) issue(1, ahead.blk, ahead.t);
+        load_ut(ahead, ut1);
+        ahead = advance(ahead);  // -> step 2
+    }
+    for (; item < p.nitems; item += G) {
+        item_range(p, item, blk, t0, t1);
+        const int64_t s3 = site_of(blk);
+        ld_soa<T, 6>(v + int64_t(t0) * 6 * F, F, s3, vc);
+        if (t0 == 0 && w_lo != nullptr) {
+            ld_soa<T, 6>(w_lo, F, s3, wt);
+        } else {
+            const int tp = (t0 > 0) ? t0 - 1 : p.nt - 1;
+            T u[18], vp[6];
+            ld_soa<T, 18>(U + (int64_t(tp) * 72 + 54) * F, F, s3, u);
+            ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vp);
+            amv<T, FUSED>(u, vp, wt);
+        }
 
-        if (cur.t < cur.t0) {
-            // prologue: w_t(x, t0-1) (from the w_lo face, or U_t(t0-1)^dag v(t0-1)) and v(x, t0)
-            T x6[6];
+        for (int t = t0; t < t1; ++t, ++k) {
+            T ut2[18];
+            const Cursor c2 = ahead;  // step k + 2
+            load_ut(c2, ut2);
+            ahead = advance(ahead);
+            const int s = static_cast<int>(k % STAGES);
+            mbar_wait(&full[s], static_cast<uint32_t>((k / STAGES) & 1));
+            const T* st = stage0 + s * SS;
+
+            T u[54], vnext[6];
 #pragma unroll
-            for (int q = 0; q < 6; ++q) x6[q] = st[g.su() + q * NTHR + tid];
-            if (use_wlo(cur)) {
+            for (int q = 0; q < 54; ++q) u[q] = st[g.su() + q * NTHR + tid];
 #pragma unroll
-                for (int q = 0; q < 6; ++q) wt[q] = x6[q];
+            for (int q = 0; q < 6; ++q) vnext[q] = st[g.sv() + q * NTHR + tid];
+
+            // halo-row half-products: thread j computes halo site j
+            for (int j = tid; j < g.HY + g.HZ; j += NTHR) {
+                T uh[18], vh[6], wh[6];
+                const bool isy = j < g.HY;
+                const int jj = isy ? j : j - g.HY;
+                const int hp = isy ? g.HY : g.HZ;
+                const int ub = isy ? g.huy() : g.huz();
+                const int vb = isy ? g.hvyd() : g.hvzd();
+#pragma unroll
+                for (int q = 0; q < 18; ++q) uh[q] = st[ub + q * hp + jj];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) vh[q] = st[vb + q * hp + jj];
+                amv<T, FUSED>(uh, vh, wh);
+                const int xo = isy ? g.xhy() : g.xhz();
+#pragma unroll
+                for (int q = 0; q < 6; ++q) xb[xo + q * hp + jj] = wh[q];
+            }
+            // this site's half-products w_x, w_y, w_z and v(x,t) for the neighbours
+            {
+                T w[6];
+#pragma unroll
+                for (int mu = 0; mu < 3; ++mu) {
+                    amv<T, FUSED>(u + 18 * mu, vc, w);
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) xb[g.xw() + (6 * mu + q) * NTHR + tid] = w[q];
+                }
+#pragma unroll
+                for (int q = 0; q < 6; ++q) xb[g.xv() + q * NTHR + tid] = vc[q];
+            }
+            T wt_next[6], f3[6];
+            amv<T, FUSED>(ut, vc, wt_next);
+            mv<T, FUSED>(ut, vnext, f3);  // forward +t term, summed last
+            named_sync<NTHR>();
+
+            // forward terms (add_su3_vector chain: ((f0 + f1) + f2) + f3)
+            T acc[6];
+            {
+                T nb[6], f[6];
+#pragma unroll
+                for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + ix_up];
+                mv<T, FUSED>(u, nb, acc);
+                if (iy_up >= 0) {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + iy_up];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) nb[q] = st[g.hvyu() + q * g.HY + (-1 - iy_up)];
+                }
+                mv<T, FUSED>(u + 18, nb, f);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
+                if (iz_up >= 0) {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + iz_up];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 6; ++q) nb[q] = st[g.hvzu() + q * g.HZ + (-1 - iz_up)];
+                }
+                mv<T, FUSED>(u + 36, nb, f);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f3[q]);
+            }
+
+            // backward terms (sub_four_su3_vecs chain)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + q * NTHR + ix_dn]);
+            if (iy_dn >= 0) {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + (6 + q) * NTHR + iy_dn]);
             } else {
-                amv<T, FUSED>(ut, x6, wt);
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xhy() + q * g.HY + (-1 - iy_dn)]);
+            }
+            if (iz_dn >= 0) {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + (12 + q) * NTHR + iz_dn]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xhz() + q * g.HZ + (-1 - iz_dn)]);
             }
 #pragma unroll
-            for (int q = 0; q < 6; ++q) vc[q] = st[g.sv() + q * NTHR + tid];
-        } else {
-                T u[54], vnext[6];
-    #pragma unroll
-                for (int q = 0; q < 54; ++q) u[q] = st[g.su() + q * NTHR + tid];
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) vnext[q] = st[g.sv() + q * NTHR + tid];
+            for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], wt[q]);
 
-                // halo-row half-products: thread j computes halo site j
-                for (int j = tid; j < g.HY + g.HZ; j += NTHR) {
-                    T uh[18], vh[6], wh[6];
-                    const bool isy = j < g.HY;
-                    const int jj = isy ? j : j - g.HY;
-                    const int hp = isy ? g.HY : g.HZ;
-                    const int ub = isy ? g.huy() : g.huz();
-                    const int vb = isy ? g.hvyd() : g.hvzd();
-    #pragma unroll
-                    for (int q = 0; q < 18; ++q) uh[q] = st[ub + q * hp + jj];
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) vh[q] = st[vb + q * hp + jj];
-                    amv<T, FUSED>(uh, vh, wh);
-                    const int xo = isy ? g.xhy() : g.xhz();
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) xb[xo + q * hp + jj] = wh[q];
-                }
-                // this site's half-products w_x, w_y, w_z and v(x,t) for the neighbours
-                {
-                    T w[6];
-    #pragma unroll
-                    for (int mu = 0; mu < 3; ++mu) {
-                        amv<T, FUSED>(u + 18 * mu, vc, w);
-    #pragma unroll
-                        for (int q = 0; q < 6; ++q) xb[g.xw() + (6 * mu + q) * NTHR + tid] = w[q];
-                    }
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) xb[g.xv() + q * NTHR + tid] = vc[q];
-                }
-                T wt_next[6], f3[6];
-                amv<T, FUSED>(ut, vc, wt_next);
-                mv<T, FUSED>(ut, vnext, f3);  // forward +t term, summed last
-                named_sync<NTHR>();
-
-                // forward terms (add_su3_vector chain: ((f0 + f1) + f2) + f3)
-                T acc[6];
-                {
-                    T nb[6], f[6];
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + ix_up];
-                    mv<T, FUSED>(u, nb, acc);
-                    if (iy_up >= 0) {
-    #pragma unroll
-                        for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + iy_up];
-                    } else {
-    #pragma unroll
-                        for (int q = 0; q < 6; ++q) nb[q] = st[g.hvyu() + q * g.HY + (-1 - iy_up)];
-                    }
-                    mv<T, FUSED>(u + 18, nb, f);
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
-                    if (iz_up >= 0) {
-    #pragma unroll
-                        for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + iz_up];
-                    } else {
-    #pragma unroll
-                        for (int q = 0; q < 6; ++q) nb[q] = st[g.hvzu() + q * g.HZ + (-1 - iz_up)];
-                    }
-                    mv<T, FUSED>(u + 36, nb, f);
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f[q]);
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] = xadd(acc[q], f3[q]);
-                }
-
-                // backward terms (sub_four_su3_vecs chain)
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + q * NTHR + ix_dn]);
-                if (iy_dn >= 0) {
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + (6 + q) * NTHR + iy_dn]);
-                } else {
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xhy() + q * g.HY + (-1 - iy_dn)]);
-                }
-                if (iz_dn >= 0) {
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + (12 + q) * NTHR + iz_dn]);
-                } else {
-    #pragma unroll
-                    for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xhz() + q * g.HZ + (-1 - iz_dn)]);
-                }
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], wt[q]);
-
-                T* o = out + int64_t(cur.t) * 6 * F + cur.s3;
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) o[q * F] = acc[q];
-    #pragma unroll
-                for (int q = 0; q < 6; ++q) {
-                    vc[q] = vnext[q];
-                    wt[q] = wt_next[q];
-                }
-        }
-        named_sync<NTHR>();  // exchange buffer and stage s free for the next step
-        // refill stage s with step k + 2: every thread is past its last read of it, so no
-        // empty-barrier wait is needed (and warp 0 never stalls mid-step)
-        if (tid == 0 && c2.valid) issue_step(s, c2);
+            T* o = out + int64_t(t) * 6 * F + s3;
 #pragma unroll
-        for (int q = 0; q < 18; ++q) {
-            ut[q] = ut1[q];
-            ut1[q] = ut2[q];
+            for (int q = 0; q < 6; ++q) o[q * F] = acc[q];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                vc[q] = vnext[q];
+                wt[q] = wt_next[q];
+            }
+#pragma unroll
+            for (int q = 0; q < 18; ++q) {
+                ut[q] = ut1[q];
+                ut1[q] = ut2[q];
+            }
+            named_sync<NTHR>();  // exchange buffer and stage s free for the next step
+            // refill stage s with step k + 2: every thread is past its last read of it, so
+            // no empty-barrier wait is needed (and warp 0 never stalls mid-step)
+            if (tid == 0 && c2.valid) issue(s, c2.blk, c2.t);
         }
     }
 }
@@ -460,8 +442,6 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     } else {
         mVhi = mV;
     }
-    CUtensorMap mWlo = mV;
-    if (w_lo != nullptr && (!aligned16(w_lo) || !make_map<T>(&mWlo, w_lo, nx, ny, nz, 6, BY, BZ, 6))) return 1;
     mUy = mU; mVy = mV; mUz = mU; mVz = mV;
     if (HY && (!make_map<T>(&mUy, U, nx, ny, nz, int64_t(nt) * 72, 1, BZ, 18) ||
                !make_map<T>(&mVy, v, nx, ny, nz, int64_t(nt) * 6, 1, BZ, 6)))
@@ -487,7 +467,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
-    k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, mWlo, U, v, out, w_lo, p);
+    k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     return check_launch("nn_sweep(tma)");
 }
 
