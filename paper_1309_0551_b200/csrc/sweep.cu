@@ -117,21 +117,43 @@ __device__ __forceinline__ void link_site(const T* __restrict__ U, T* __restrict
     T acc[18];
 #pragma unroll
     for (int k = 0; k < 18; ++k) acc[k] = T(0);
-#pragma unroll 1
-    for (int mu = 0; mu < 3; ++mu) {
-        T a[18];
-        ld_link(U, g, site, mu, a);
-#pragma unroll 1
-        for (int nu = mu + 1; nu < 4; ++nu) {
-            T b[18], tm[18], p[18];
-            ld_link(U, g, site_step(g, x, y, z, t, mu), nu, b);
-            if (FUSED) mat_nn_fma<T>(a, b, tm);
-            else mat_nn<T>(a, b, tm);
-            ld_link(U, g, site_step(g, x, y, z, t, nu), mu, b);
-            if (FUSED) mat_na_fma<T>(tm, b, p);
-            else mat_na<T>(tm, b, p);
-#pragma unroll
-            for (int k = 0; k < 18; ++k) acc[k] = FUSED ? fma(s, p[k], acc[k]) : xadd(acc[k], xmul(s, p[k]));
+    // FMA mode: full unroll lets the next plane's link loads overlap this plane's math
+    // (measured 1.43 vs 1.79 ms at 48^4); exact mode keeps the rolled loop (unrolled it spills)
+    if constexpr (FUSED) {
+    #pragma unroll
+        for (int mu = 0; mu < 3; ++mu) {
+            T a[18];
+            ld_link(U, g, site, mu, a);
+    #pragma unroll
+            for (int nu = mu + 1; nu < 4; ++nu) {
+                T b[18], tm[18], p[18];
+                ld_link(U, g, site_step(g, x, y, z, t, mu), nu, b);
+                if (FUSED) mat_nn_fma<T>(a, b, tm);
+                else mat_nn<T>(a, b, tm);
+                ld_link(U, g, site_step(g, x, y, z, t, nu), mu, b);
+                if (FUSED) mat_na_fma<T>(tm, b, p);
+                else mat_na<T>(tm, b, p);
+    #pragma unroll
+                for (int k = 0; k < 18; ++k) acc[k] = FUSED ? fma(s, p[k], acc[k]) : xadd(acc[k], xmul(s, p[k]));
+            }
+        }
+    } else {
+    #pragma unroll 1
+        for (int mu = 0; mu < 3; ++mu) {
+            T a[18];
+            ld_link(U, g, site, mu, a);
+    #pragma unroll 1
+            for (int nu = mu + 1; nu < 4; ++nu) {
+                T b[18], tm[18], p[18];
+                ld_link(U, g, site_step(g, x, y, z, t, mu), nu, b);
+                if (FUSED) mat_nn_fma<T>(a, b, tm);
+                else mat_nn<T>(a, b, tm);
+                ld_link(U, g, site_step(g, x, y, z, t, nu), mu, b);
+                if (FUSED) mat_na_fma<T>(tm, b, p);
+                else mat_na<T>(tm, b, p);
+    #pragma unroll
+                for (int k = 0; k < 18; ++k) acc[k] = FUSED ? fma(s, p[k], acc[k]) : xadd(acc[k], xmul(s, p[k]));
+            }
         }
     }
 #pragma unroll
@@ -365,7 +387,7 @@ static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk, 3 TMA walk
-static std::atomic<int> g_link_variant{0};  // 0 auto (= generic, measured fastest), 1 generic, 2 block walk, 3 ring
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 generic, 2 block walk, 3 ring, 4 plane-split
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
@@ -452,6 +474,10 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     int BY = 0, BZ = 0;
     const int lv = g_link_variant.load();
+    if (lv == 4) {
+        return mode == SU3G_FMA ? launch_link_planes<T, true>(U, acc, nx, ny, nz, nt, s, st)
+                                : launch_link_planes<T, false>(U, acc, nx, ny, nz, nt, s, st);
+    }
     if (lv == 3) {
         const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
                                         : launch_link_ring<T, false>(U, acc, nx, ny, nz, nt, s, st);
@@ -500,8 +526,8 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 3)
-            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring)");
+        if (value < 0 || value > 4)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring), 4 (planes)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -69,4 +69,7 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
 template <typename T, bool FUSED>
 int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 
+template <typename T, bool FUSED>
+int launch_link_planes(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
+
 }  // namespace su3g

@@ -232,7 +232,7 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
         _lib.set_option("no_such_option", 1)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "generic", "block-walk", "ring"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4], ids=["auto", "generic", "block-walk", "ring", "planes"])
 @pytest.mark.parametrize("dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4)])
 def test_link_product_variants_bitwise(variant, dims, precision):
     from paper_1309_0551_b200 import _lib
