@@ -183,7 +183,7 @@ struct LinkWalk {
 };
 
 template <typename T, bool FUSED>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128)
     k_link_walk(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, LinkWalk w, T s) {
     const int tid = threadIdx.x;
     const int lx = tid % g.nx, rr = tid / g.nx, ly = rr % w.BY, lz = rr / w.BY;
