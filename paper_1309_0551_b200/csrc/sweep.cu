@@ -160,15 +160,24 @@ __device__ __forceinline__ void link_site(const T* __restrict__ U, T* __restrict
     for (int k = 0; k < 18; ++k) acc_out[(int64_t(t) * 18 + k) * g.F + s3] = acc[k];
 }
 
+// Sites are visited in (z-chunk, t, z, y, x) order with ZC z-planes per chunk: the
+// +t links a site gathers as neighbours are re-read as own links ZC*nx*ny sites
+// later (a few MB of traffic) instead of one whole slice later, so they stay in
+// L2 (natural t-major order measured 35% L2 hits, 1.7x the compulsory DRAM reads).
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(128)
-    k_link_product(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s) {
-    const int64_t site = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (site >= g.F * g.nt) return;
-    const int t = static_cast<int>(site / g.F);
-    const int64_t s3 = site % g.F;
-    link_site<T, FUSED>(U, acc_out, g, s, static_cast<int>(s3 % g.nx), static_cast<int>((s3 / g.nx) % g.ny),
-                        static_cast<int>(s3 / (int64_t(g.nx) * g.ny)), t);
+    k_link_product(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC) {
+    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (idx >= g.F * g.nt) return;
+    const int x = static_cast<int>(idx % g.nx);
+    int64_t r = idx / g.nx;
+    const int y = static_cast<int>(r % g.ny);
+    r /= g.ny;
+    const int zl = static_cast<int>(r % ZC);
+    r /= ZC;
+    const int t = static_cast<int>(r % g.nt);
+    const int z = static_cast<int>(r / g.nt) * ZC + zl;
+    link_site<T, FUSED>(U, acc_out, g, s, x, y, z, t);
 }
 
 // Block-walk schedule: a CTA owns nx x BY x BZ sites of a slice and walks t; work items
@@ -506,8 +515,15 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     }
     const int64_t n = g.F * nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
-    if (mode == SU3G_FMA) k_link_product<T, true><<<grid, 128, 0, st>>>(U, acc, g, s);
-    else k_link_product<T, false><<<grid, 128, 0, st>>>(U, acc, g, s);
+    int ZC = nz;  // largest divisor of nz that is <= 8 (1 -> plain t-major order when nz is prime > 8)
+    for (int c = std::min(nz, 8); c >= 1; --c)
+        if (nz % c == 0) {
+            ZC = c;
+            break;
+        }
+    if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
+    if (mode == SU3G_FMA) k_link_product<T, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
+    else k_link_product<T, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     return check_launch("link_product");
 }
 
@@ -526,8 +542,10 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 4)
-            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring), 4 (planes)");
+        if (value < 0 || value > 5)
+            return fail_invalid(
+                "set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring), 4 (planes), "
+                "5 (generic, natural order)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }
