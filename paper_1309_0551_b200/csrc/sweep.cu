@@ -22,15 +22,22 @@ namespace su3g {
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256)
     k_nn_sweep(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin, int t_end,
-               const T* __restrict__ v_hi, const T* __restrict__ w_lo) {
+               const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC) {
+    // visiting order (z-chunk of ZC planes, t, z, y, x): the t-1 slice a site reads (U_t, v)
+    // was streamed ZC*nx*ny sites earlier, not a whole slice earlier -> L2 hits
     const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     const int64_t F = g.F;
-    if (idx >= int64_t(t_end - t_begin) * F) return;
-    const int t = t_begin + static_cast<int>(idx / F);
-    const int64_t s3 = idx % F;
-    const int x = static_cast<int>(s3 % g.nx);
-    const int y = static_cast<int>((s3 / g.nx) % g.ny);
-    const int z = static_cast<int>(s3 / (int64_t(g.nx) * g.ny));
+    const int nts = t_end - t_begin;
+    if (idx >= int64_t(nts) * F) return;
+    const int x = static_cast<int>(idx % g.nx);
+    int64_t r = idx / g.nx;
+    const int y = static_cast<int>(r % g.ny);
+    r /= g.ny;
+    const int zl = static_cast<int>(r % ZC);
+    r /= ZC;
+    const int t = t_begin + static_cast<int>(r % nts);
+    const int z = static_cast<int>(r / nts) * ZC + zl;
+    const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
 
     T acc[6];
     // forward terms, mu = 0..3, summed left to right (add_su3_vector chain)
@@ -428,6 +435,13 @@ static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, i
     return check_launch("nn_sweep(walk)");
 }
 
+// largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
+static int chunk_planes(int nz, int cap) {
+    for (int c = std::min(nz, cap); c >= 1; --c)
+        if (nz % c == 0) return c;
+    return 1;
+}
+
 static int check_geom(const char* what, int nx, int ny, int nz, int nt) {
     if (nx < 1 || ny < 1 || nz < 1 || nt < 1) return fail_invalid(std::string(what) + ": lattice extents must be >= 1");
     return SU3G_OK;
@@ -458,8 +472,9 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int64_t n = int64_t(t_end - t_begin) * g.F;
     const unsigned gs = static_cast<unsigned>((n + 255) / 256);
-    if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo);
-    else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo);
+    const int ZC = (variant == 4) ? nz : chunk_planes(nz, 8);  // 4: natural t-major order (A/B knob)
+    if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+    else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
     return check_launch("nn_sweep");
 }
 
@@ -515,12 +530,7 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     }
     const int64_t n = g.F * nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
-    int ZC = nz;  // largest divisor of nz that is <= 8 (1 -> plain t-major order when nz is prime > 8)
-    for (int c = std::min(nz, 8); c >= 1; --c)
-        if (nz % c == 0) {
-            ZC = c;
-            break;
-        }
+    int ZC = chunk_planes(nz, 8);
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
     if (mode == SU3G_FMA) k_link_product<T, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     else k_link_product<T, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
@@ -536,8 +546,9 @@ extern "C" {
 int su3g_set_option(const char* name, int64_t value) {
     if (name == nullptr) return fail_invalid("set_option: null name");
     if (std::strcmp(name, "nn_variant") == 0) {
-        if (value < 0 || value > 3)
-            return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk)");
+        if (value < 0 || value > 4)
+            return fail_invalid(
+                "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major)");
         g_nn_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }
