@@ -1,5 +1,6 @@
 // libsu3g: error reporting and cached device properties.
 #include <cstdio>
+#include <atomic>
 #include <mutex>
 
 #include "su3g_common.cuh"
@@ -7,6 +8,10 @@
 namespace su3g {
 
 static thread_local std::string g_last_error;
+static std::atomic<int> g_sm_reserve{0};
+
+int sm_reserve() { return g_sm_reserve.load(); }
+void set_sm_reserve(int n) { g_sm_reserve.store(n); }
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 

@@ -461,7 +461,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.BY = BY; p.BZ = BZ; p.nby = ny / BY;
     p.nblocks = int64_t(ny / BY) * (nz / BZ);
     p.t_begin = t_begin; p.t_end = t_end;
-    const int G = di.num_sms;
+    const int G = sweep_sms();
     p.chunk = pick_chunk(p.nblocks, t_end - t_begin, G);
     p.nchunks = (t_end - t_begin + p.chunk - 1) / p.chunk;
     p.nitems = p.nblocks * p.nchunks;

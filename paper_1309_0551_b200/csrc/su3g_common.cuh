@@ -34,6 +34,15 @@ struct DeviceInfo {
 };
 const DeviceInfo& device_info();
 
+// SMs left free by the persistent sweep kernels so that concurrently launched
+// kernels (the NCCL halo exchange of a t-slab sweep) can be co-scheduled; set
+// through su3g_set_option("sm_reserve", n).
+int sm_reserve();
+inline int sweep_sms() {
+    const int n = device_info().num_sms - sm_reserve();
+    return n > 0 ? n : 1;
+}
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ----------------------------------------------------------------------------

@@ -16,6 +16,8 @@
 
 namespace su3g {
 
+void set_sm_reserve(int n);
+
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
 // ---------------------------------------------------------------------------
@@ -459,8 +461,11 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const int variant = g_nn_variant.load();
     // auto policy (measured on B200, profiles/r01): f32 with full-width 64+ x rows -> TMA walk;
     // other f32 lattices -> register walk; f64 -> generic (fewest registers, best occupancy)
-    const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 32;
-    const bool auto_walk = variant == 0 && sizeof(T) == 4;
+    // one or two boundary slices of a t-slab (the halo-dependent launches) go to the generic
+    // kernel: a walk kernel would pay a work-item prologue for every single-slice item
+    const bool boundary_only = (t_end - t_begin) <= 2 && nt > 2;
+    const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 32 && !boundary_only;
+    const bool auto_walk = variant == 0 && sizeof(T) == 4 && !boundary_only;
     if (auto_tma || variant == 3) {
         const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
         if (rc != 1) return rc;
@@ -554,6 +559,11 @@ int su3g_set_option(const char* name, int64_t value) {
             return fail_invalid(
                 "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major)");
         g_nn_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "sm_reserve") == 0) {
+        if (value < 0 || value > 64) return fail_invalid("set_option: sm_reserve must be in [0, 64]");
+        set_sm_reserve(static_cast<int>(value));
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {

@@ -32,6 +32,7 @@ from .lattice import Field
 
 TAG_V = 11
 TAG_W = 12
+SM_RESERVE = 4  # SMs kept free for the NCCL halo-exchange kernels while the interior runs
 
 
 class CudaSlabKernels:
@@ -54,6 +55,16 @@ class CudaSlabKernels:
 
     def nt(self, v: Field) -> int:
         return v.lattice.nt
+
+    def prepare(self, world: int) -> None:
+        """Leave SMs free for NCCL's kernels so the halo exchange overlaps the interior sweep.
+
+        The persistent sweep kernel fills every SM (all registers, ~210 KB smem), so a
+        concurrently launched NCCL kernel could not be co-scheduled until it finished.
+        """
+        from . import _lib
+
+        _lib.set_option("sm_reserve", SM_RESERVE if world > 1 else 0)
 
 
 class _Null:
@@ -88,6 +99,8 @@ class SlabSweep:
         else:
             self.rank, self.world = 0, 1
         self._faces = None
+        if hasattr(self.k, "prepare"):
+            self.k.prepare(self.world)
 
     @property
     def up(self) -> int:
