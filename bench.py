@@ -422,7 +422,7 @@ def run_b200(args, rank, world, local):
         "hbm_gbs": achieved,
         "roofline": {
             "bound": "hbm",
-            "kernel": {"nn": "k_nn_sweep", "link": "k_link_product"}.get(cfg["kind"], "k_stream"),
+            "kernel": {"nn": "k_nn_tma (f32) / k_nn_sweep (f64)", "link": "k_link_product"}.get(cfg["kind"], "k_stream"),
             "achieved": achieved,
             "peak": peak,
             "peak_source": peak_src,
