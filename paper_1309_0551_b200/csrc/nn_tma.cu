@@ -461,7 +461,9 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.BY = BY; p.BZ = BZ; p.nby = ny / BY;
     p.nblocks = int64_t(ny / BY) * (nz / BZ);
     p.t_begin = t_begin; p.t_end = t_end;
-    const int G = sweep_sms();
+    int per_sm = 1;  // resident CTAs per SM (2 for the 128-thread f32 geometry)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ>, NTHR, smem);
+    const int G = sweep_sms() * std::max(per_sm, 1);
     p.chunk = pick_chunk(p.nblocks, t_end - t_begin, G);
     p.nchunks = (t_end - t_begin + p.chunk - 1) / p.chunk;
     p.nitems = p.nblocks * p.nchunks;
@@ -471,9 +473,21 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     return check_launch("nn_sweep(tma)");
 }
 
+int g_tma_threads = 0;  // su3g_set_option("nn_tma_threads"): 0 auto, 128, 256
+
 template <typename T>
 int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                   const T* v_hi, const T* w_lo, int mode, cudaStream_t st) {
+    if constexpr (sizeof(T) == 4) {
+        // 32-wide lattices: 128-site blocks (32x2x2) fit two CTAs per SM, which hide each
+        // other's barrier and prologue stalls (BASELINE configs[2], 32^4)
+        const bool small = g_tma_threads == 128 || (g_tma_threads == 0 && nx == 32);
+        if (small && nx == 32 && ny % 2 == 0 && nz % 2 == 0 && ny > 2 && nz > 2 && aligned16(U) && aligned16(v) &&
+            (!v_hi || aligned16(v_hi)))
+            return mode == SU3G_FMA
+                       ? run_tma<T, true, 128, 2, 32, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, 2, 2, st)
+                       : run_tma<T, false, 128, 2, 32, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, 2, 2, st);
+    }
     constexpr int NTHR = sizeof(T) == 4 ? 256 : 128;
     if ((nx * int(sizeof(T))) % 16 != 0 || nx > 256) return 1;
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;

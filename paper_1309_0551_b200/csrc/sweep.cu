@@ -17,6 +17,7 @@
 namespace su3g {
 
 void set_sm_reserve(int n);
+extern int g_tma_threads;
 
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
@@ -559,6 +560,11 @@ int su3g_set_option(const char* name, int64_t value) {
             return fail_invalid(
                 "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major)");
         g_nn_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "nn_tma_threads") == 0) {
+        if (value != 0 && value != 128 && value != 256) return fail_invalid("set_option: nn_tma_threads must be 0, 128 or 256");
+        g_tma_threads = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "sm_reserve") == 0) {

@@ -314,3 +314,23 @@ def test_nn_tma_multi_item_schedules(dims, precision):
             assert bad.size == 0, f"variant {variant}: {bad.size} wrong sites, first {bad[:5].ravel()}"
         finally:
             _lib.set_option("nn_variant", 0)
+
+
+@pytest.mark.parametrize("threads", [128, 256])
+@pytest.mark.parametrize("dims", [(32, 8, 8, 12), (32, 32, 32, 4)])
+def test_nn_tma_block_sizes(threads, dims):
+    """The 128- and 256-site TMA geometries (32-wide lattices) agree with the oracle bit for bit."""
+    from paper_1309_0551_b200 import _lib
+
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(9500 + V)
+    U = inputs.random_links(rng, V, 4, dtype=np.float32)
+    v = inputs.random_vectors(rng, V, None, dtype=np.float32)
+    _lib.set_option("nn_tma_threads", threads)
+    _lib.set_option("nn_variant", 3)
+    try:
+        assert np.array_equal(sweeps.nn_sweep_aos(U, v, dims), coracle.nn_sweep(U, v, dims))
+        assert floored_rel_err(sweeps.nn_sweep_aos(U, v, dims, mode="fma"), coracle.nn_sweep(U, v, dims)) <= 1e-5
+    finally:
+        _lib.set_option("nn_tma_threads", 0)
+        _lib.set_option("nn_variant", 0)
