@@ -240,6 +240,10 @@ def run_b200(args, rank, world, local):
         from paper_1309_0551_b200 import _lib as _l
 
         _l.set_option("nn_variant", int(os.environ["SU3G_NN_VARIANT"]))
+    if os.environ.get("SU3G_CHUNK_PROLOGUE_X10"):
+        from paper_1309_0551_b200 import _lib as _l
+
+        _l.set_option("chunk_prologue_x10", int(os.environ["SU3G_CHUNK_PROLOGUE_X10"]))
     if os.environ.get("SU3G_NN_TMA_THREADS"):
         from paper_1309_0551_b200 import _lib as _l
 

@@ -562,6 +562,11 @@ int su3g_set_option(const char* name, int64_t value) {
         g_nn_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }
+    if (std::strcmp(name, "chunk_prologue_x10") == 0) {
+        if (value < 0 || value > 100) return fail_invalid("set_option: chunk_prologue_x10 must be in [0, 100]");
+        g_prologue_cost = double(value) / 10.0;
+        return SU3G_OK;
+    }
     if (std::strcmp(name, "nn_tma_threads") == 0) {
         if (value != 0 && value != 128 && value != 256) return fail_invalid("set_option: nn_tma_threads must be 0, 128 or 256");
         g_tma_threads = static_cast<int>(value);

@@ -41,6 +41,9 @@ __device__ __forceinline__ T ld_stream(const T* p, uint64_t pol) {
 }
 
 // chunk length that best balances the single wave of G CTAs (prologue = ~0.3 slice)
+// relative cost of a work item's prologue, in steps (su3g_set_option("chunk_prologue_x10"))
+inline double g_prologue_cost = 1.0;
+
 inline int pick_chunk(int64_t nblocks, int nt_range, int G) {
     int best_L = nt_range;
     double best_eff = -1;
@@ -49,7 +52,7 @@ inline int pick_chunk(int64_t nblocks, int nt_range, int G) {
         const int64_t items = nblocks * nchunks;
         const int64_t per = (items + G - 1) / G;
         const double work = double(nblocks) * nt_range;
-        const double eff = work / (double(per) * G * L) * (L / (L + 0.3));
+        const double eff = work / (double(per) * G * L) * (L / (L + g_prologue_cost));
         if (eff > best_eff + 1e-9) {
             best_eff = eff;
             best_L = L;
