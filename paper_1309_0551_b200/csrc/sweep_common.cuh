@@ -42,7 +42,7 @@ __device__ __forceinline__ T ld_stream(const T* p, uint64_t pol) {
 
 // chunk length that best balances the single wave of G CTAs (prologue = ~0.3 slice)
 // relative cost of a work item's prologue, in steps (su3g_set_option("chunk_prologue_x10"))
-inline double g_prologue_cost = 1.0;
+inline double g_prologue_cost = 2.0;
 
 inline int pick_chunk(int64_t nblocks, int nt_range, int G) {
     int best_L = nt_range;
