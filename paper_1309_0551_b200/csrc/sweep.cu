@@ -467,6 +467,14 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const bool boundary_only = (t_end - t_begin) <= 2 && nt > 2;
     const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 32 && !boundary_only;
     const bool auto_walk = variant == 0 && sizeof(T) == 4 && !boundary_only;
+    const bool auto_tma64 = variant == 0 && sizeof(T) == 8 && !boundary_only;
+    if (auto_tma64 || variant == 5) {
+        const int rc = mode == SU3G_FMA
+                           ? launch_nn_tma64<T, true>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
+                           : launch_nn_tma64<T, false>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+        if (rc != 1) return rc;
+        if (variant == 5) return fail_invalid("nn_sweep: TMA (register-staged) kernel not applicable to this lattice");
+    }
     if (auto_tma || variant == 3) {
         const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
         if (rc != 1) return rc;
@@ -556,9 +564,10 @@ extern "C" {
 int su3g_set_option(const char* name, int64_t value) {
     if (name == nullptr) return fail_invalid("set_option: null name");
     if (std::strcmp(name, "nn_variant") == 0) {
-        if (value < 0 || value > 4)
+        if (value < 0 || value > 5)
             return fail_invalid(
-                "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major)");
+                "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major), "
+                "5 (tma walk, register-staged)");
         g_nn_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

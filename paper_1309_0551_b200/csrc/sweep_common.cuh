@@ -75,4 +75,9 @@ int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cu
 template <typename T, bool FUSED>
 int launch_link_planes(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 
+// f64 TMA t-walk with a register-staged main operand (nn_tma64.cu); 1 = not applicable.
+template <typename T, bool FUSED>
+int launch_nn_tma64(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
+                    const T* v_hi, const T* w_lo, cudaStream_t st);
+
 }  // namespace su3g

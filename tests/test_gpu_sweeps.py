@@ -165,7 +165,7 @@ def test_slab_halo_path_equals_periodic_sweep(ranks, precision, dims=(8, 4, 4, 8
     assert np.array_equal(w0, R.mult_adj_su3_mat_vec(U[(ntl - 1) * F : ntl * F, 3], v[(ntl - 1) * F : ntl * F]))
 
 
-@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "generic", "walk", "tma"])
+@pytest.fixture(params=[0, 1, 2, 3, 5], ids=["auto", "generic", "walk", "tma", "tma64"])
 def nn_variant(request):
     from paper_1309_0551_b200 import _lib
 
@@ -187,7 +187,7 @@ def test_nn_kernel_variants_bitwise(dims, precision, nn_variant):
     try:
         got = sweeps.nn_sweep_aos(U, v, dims)
     except ValueError as e:
-        if nn_variant in (2, 3) and "not applicable" in str(e):
+        if nn_variant in (2, 3, 5) and "not applicable" in str(e):
             pytest.skip(f"variant {nn_variant} not applicable to {dims}")
         raise
     assert np.array_equal(got, want)
@@ -203,15 +203,17 @@ def test_nn_kernel_variants_bitwise(dims, precision, nn_variant):
     assert np.array_equal(out.numpy(), want)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 5])
 def test_slab_halo_path_all_variants(variant, precision):
     from paper_1309_0551_b200 import _lib
 
     _lib.set_option("nn_variant", variant)
     try:
-        test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(16, 4, 4, 8))
-        test_slab_halo_path_equals_periodic_sweep(4, precision, dims=(16, 4, 4, 8))
+        if variant != 5:
+            test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(16, 4, 4, 8))
+            test_slab_halo_path_equals_periodic_sweep(4, precision, dims=(16, 4, 4, 8))
         test_slab_halo_path_equals_periodic_sweep(8, precision, dims=(64, 4, 2, 8))
+        test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(64, 4, 4, 8))
     finally:
         _lib.set_option("nn_variant", 0)
 
@@ -257,7 +259,7 @@ def test_link_product_variants_bitwise(variant, dims, precision):
         _lib.set_option("link_variant", 0)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3], ids=["generic", "walk", "tma"])
+@pytest.mark.parametrize("variant", [1, 2, 3, 5], ids=["generic", "walk", "tma", "tma64"])
 @pytest.mark.parametrize("dims", [(64, 4, 4, 6), (32, 8, 4, 5), (8, 8, 8, 8)])
 def test_nn_fma_mode_within_tolerance(variant, dims, precision):
     """SU3G_FMA arithmetic: within the north-star tolerance of the reference, and every kernel variant
@@ -301,7 +303,7 @@ def test_nn_tma_multi_item_schedules(dims, precision):
     U = inputs.random_links(rng, V, 4, dtype=dt)
     v = inputs.random_vectors(rng, V, None, dtype=dt)
     want = coracle.nn_sweep(U, v, dims)
-    for variant in (0, 2, 3):
+    for variant in (0, 2, 3, 5):
         _lib.set_option("nn_variant", variant)
         try:
             try:
