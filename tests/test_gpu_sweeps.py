@@ -209,6 +209,8 @@ def test_slab_halo_path_all_variants(variant, precision):
 
     _lib.set_option("nn_variant", variant)
     try:
+        if variant == 3 and precision == "double":
+            pytest.skip("the f32-style TMA walk does not fit shared memory for f64 on these lattices")
         if variant != 5:
             test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(16, 4, 4, 8))
             test_slab_halo_path_equals_periodic_sweep(4, precision, dims=(16, 4, 4, 8))
