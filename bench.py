@@ -38,16 +38,20 @@ FALLBACK_HBM_GBS = 6650.0
 # algorithmic (compulsory) HBM bytes per site: read each input object once, write each output once
 NN_BYTES = {"f32": 336, "f64": 672}        # U 72 reals + v 6 + out 6
 LINK_BYTES = {"f32": 360, "f64": 720}      # U 72 + acc 18
-ROUTINE_REALS = {                           # (in reals, out reals) per site
-    "mult_su3_mat_vec": (24, 6),
-    "mult_adj_su3_mat_vec": (24, 6),
-    "mult_su3_nn": (36, 18),
-    "mult_su3_na": (36, 18),
-    "mult_su3_an": (36, 18),
-    "scalar_mult_add_su3_matrix": (36, 18),
-    "mult_su3_mat_vec_sum_4dir": (96, 6),
-    "mult_adj_su3_mat_vec_4dir": (78, 24),
-}
+def _routine_layout():
+    """routine -> (reals per site of each array operand, reals per site of the result), from the registry."""
+    from paper_1309_0551_b200 import types as T
+
+    out = {}
+    for name, spec in T.ROUTINES.items():
+        out[name] = ([T.REALS[k] for k in spec.operands if k != "scalar"], T.REALS[spec.result])
+    return out
+
+
+ROUTINE_LAYOUT = _routine_layout()
+# (in reals, out reals) per site -- algorithmic bytes = (in + out) x element size
+ROUTINE_REALS = {r: (sum(ins), res) for r, (ins, res) in ROUTINE_LAYOUT.items()}
+SMADD_ROUTINES = ("scalar_mult_add_su3_matrix", "scalar_mult_add_su3_vector")
 
 
 def parse_args(argv=None):
@@ -319,7 +323,7 @@ def run_b200(args, rank, world, local):
         rin, rout = ROUTINE_REALS[r]
         from paper_1309_0551_b200 import _lib
 
-        kinds = {"mult_su3_mat_vec_sum_4dir": (72, 24), "mult_adj_su3_mat_vec_4dir": (72, 6)}.get(r, (18, rin - 18))
+        ins, _ = ROUTINE_LAYOUT[r]
         sfx = args.dtype
         esz = 4 if sfx == "f32" else 8
         set_bytes = n * (rin + rout) * esz
@@ -331,19 +335,21 @@ def run_b200(args, rank, world, local):
         if graph_mode:
             l2 = int(_lib.load().su3g_device_l2_bytes()) or (126 << 20)
             R = max(16, -(-2 * l2 // set_bytes))
-        a = torch.randn(R * n * kinds[0], dtype=tdt, device=dev, generator=gen)
-        b = torch.randn(R * n * kinds[1], dtype=tdt, device=dev, generator=gen)
+        bufs = [torch.randn(R * n * k, dtype=tdt, device=dev, generator=gen) for k in ins]
         c = torch.empty(R * n * rout, dtype=tdt, device=dev)
 
         def launch(i=0):
             st = torch.cuda.current_stream(dev).cuda_stream
-            pa = a.data_ptr() + i * n * kinds[0] * esz
-            pb = b.data_ptr() + i * n * kinds[1] * esz
+            p = [b.data_ptr() + i * n * k * esz for b, k in zip(bufs, ins)]
             pc = c.data_ptr() + i * n * rout * esz
-            if r == "scalar_mult_add_su3_matrix":
-                _lib.call(f"su3g_{r}_{sfx}", pa, pb, 0.5, None, pc, n, st)
+            if r in SMADD_ROUTINES:
+                _lib.call(f"su3g_{r}_{sfx}", p[0], p[1], 0.5, None, pc, n, st)
+            elif r == "mult_adj_su3_mat_4vec":  # four separate destinations
+                _lib.call(f"su3g_{r}_{sfx}", p[0], p[1], *(pc + d * n * 6 * esz for d in range(4)), n, st)
+            elif r == "sub_four_su3_vecs":  # in place on the first operand
+                _lib.call(f"su3g_{r}_{sfx}", *p, n, st)
             else:
-                _lib.call(f"su3g_{r}_{sfx}", pa, pb, pc, n, st)
+                _lib.call(f"su3g_{r}_{sfx}", p[0], p[1], pc, n, st)
 
         graph = None
         if graph_mode:
@@ -531,29 +537,35 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
         n = cfg["nsites"]
         gen = torch.Generator(device=dev)
         gen.manual_seed(99)
-        shapes = {
-            "mult_su3_mat_vec": ((3, 3, 2), (3, 2)), "mult_adj_su3_mat_vec": ((3, 3, 2), (3, 2)),
-            "mult_su3_mat_vec_sum_4dir": ((4, 3, 3, 2), (4, 3, 2)), "mult_adj_su3_mat_vec_4dir": ((4, 3, 3, 2), (3, 2)),
-        }.get(r, ((3, 3, 2), (3, 3, 2)))
-        a_h = torch.randn((n,) + shapes[0], dtype=tdt, generator=gen, device=dev).cpu().pin_memory()
-        b_h = torch.randn((n,) + shapes[1], dtype=tdt, generator=gen, device=dev).cpu().pin_memory()
-        a_d, b_d = torch.empty_like(a_h, device=dev), torch.empty_like(b_h, device=dev)
-        res_shape = {"mult_su3_mat_vec": (3, 2), "mult_adj_su3_mat_vec": (3, 2), "mult_su3_mat_vec_sum_4dir": (3, 2),
-                     "mult_adj_su3_mat_vec_4dir": (4, 3, 2)}.get(r, (3, 3, 2))
-        c_d = torch.empty((n,) + res_shape, dtype=tdt, device=dev)
-        out_h = torch.empty((n,) + res_shape, dtype=tdt).pin_memory()
+        from paper_1309_0551_b200 import types as T
+
+        spec = T.routine_spec(r)
+        kinds = [k for k in spec.operands if k != "scalar"]
+        hosts = [torch.randn((n,) + T.OPERAND_SHAPES[k], dtype=tdt, generator=gen, device=dev).cpu().pin_memory()
+                 for k in kinds]
+        devs = [torch.empty_like(h, device=dev) for h in hosts]
+        res_shape = (n,) + T.OPERAND_SHAPES[spec.result]
+        c_d = torch.empty(res_shape, dtype=tdt, device=dev)
+        out_h = torch.empty(res_shape, dtype=tdt).pin_memory()
         fn = kernels.KERNELS[r]
 
         def step():
-            a_d.copy_(a_h, non_blocking=True)
-            b_d.copy_(b_h, non_blocking=True)
-            if r == "scalar_mult_add_su3_matrix":
-                fn(a_d, b_d, 0.5, out=c_d)
+            for h, d in zip(hosts, devs):
+                d.copy_(h, non_blocking=True)
+            if r in SMADD_ROUTINES:
+                fn(devs[0], devs[1], 0.5, out=c_d)
+                res = c_d
+            elif r == "mult_adj_su3_mat_4vec":
+                fn(devs[0], devs[1], outs=[c_d[:, d] for d in range(4)])  # strided views: staged + copied
+                res = c_d
+            elif r == "sub_four_su3_vecs":
+                res = fn(*devs)
             else:
-                fn(a_d, b_d, out=c_d)
-            out_h.copy_(c_d, non_blocking=True)
+                fn(devs[0], devs[1], out=c_d)
+                res = c_d
+            out_h.copy_(res, non_blocking=True)
 
-        h2d = (a_h.numel() + b_h.numel()) * a_h.element_size()
+        h2d = sum(h.numel() for h in hosts) * hosts[0].element_size()
         d2h = out_h.numel() * out_h.element_size()
         sites = n
 
@@ -606,19 +618,20 @@ def _cpu_sample(cfg, dtype, small=False):
         V = int(np.prod(dims))
         U = inputs.random_links(rng, V, 4, dtype=dt)
         return (lambda: S.link_product(U, dims, 1 / 6)), V, (dims, U, None), "composed reference link product on a 48x48x8x4 sample"
+    from paper_1309_0551_b200 import types as T
+
     r = cfg["routine"]
     n = min(cfg["nsites"], 1 << 18)
-    if r in ("mult_su3_mat_vec_sum_4dir",):
-        ops = [inputs.random_links(rng, n, 4, dtype=dt), inputs.random_vectors(rng, n, 4, dtype=dt)]
-    elif r == "mult_adj_su3_mat_vec_4dir":
-        ops = [inputs.random_links(rng, n, 4, dtype=dt), inputs.random_vectors(rng, n, None, dtype=dt)]
-    elif r in ("mult_su3_mat_vec", "mult_adj_su3_mat_vec"):
-        ops = [inputs.random_links(rng, n, None, dtype=dt), inputs.random_vectors(rng, n, None, dtype=dt)]
-    elif r == "scalar_mult_add_su3_matrix":
-        ops = [inputs.random_links(rng, n, None, dtype=dt), inputs.random_links(rng, n, None, dtype=dt), dt(0.5)]
-    else:
-        ops = [inputs.random_links(rng, n, None, dtype=dt), inputs.random_links(rng, n, None, dtype=dt)]
-    fn = R.ROUTINES[r]
+    spec = T.routine_spec(r)
+    ops = []
+    for k in spec.operands:
+        if k == "scalar":
+            ops.append(dt(0.5))
+        elif k in ("mat", "mat4"):
+            ops.append(inputs.random_links(rng, n, None if k == "mat" else 4, dtype=dt))
+        else:
+            ops.append(rng.standard_normal((n,) + T.OPERAND_SHAPES[k]).astype(dt))
+    fn = R.ALL_ROUTINES[r]
     return (lambda: fn(*ops)), n, None, f"reference {r} (numpy restatement) on {n} sites"
 
 

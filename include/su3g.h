@@ -94,6 +94,42 @@ SU3G_API int su3g_scalar_mult_add_su3_matrix_f32(const float *a, const float *b,
 SU3G_API int su3g_scalar_mult_add_su3_matrix_f64(const double *a, const double *b, double s, const double *s_per_site,
                                         double *c, int64_t nsites, su3g_stream_t stream);
 
+/* ---- the other seven Table-1 routines -----------------
+ * Same conventions as above: AoS records, device pointers, nsites objects. */
+/* replaces su3bench.simd.add_su3_vector (simd.py:71-77; scalar.py:39-46): c = a + b */
+SU3G_API int su3g_add_su3_vector_f32(const float *a, const float *b, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_add_su3_vector_f64(const double *a, const double *b, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_su3_mat_hwvec (simd.py:152-159; scalar.py:122-128)
+ * h, c: half-Wilson vectors (2,3,2) per site; c[k] = a h[k] */
+SU3G_API int su3g_mult_su3_mat_hwvec_f32(const float *a, const float *h, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_su3_mat_hwvec_f64(const double *a, const double *h, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.mult_adj_su3_mat_hwvec (simd.py:162-169; scalar.py:131-137): c[k] = adj(a) h[k] */
+SU3G_API int su3g_mult_adj_su3_mat_hwvec_f32(const float *a, const float *h, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_adj_su3_mat_hwvec_f64(const double *a, const double *h, double *c, int64_t nsites,
+                                             su3g_stream_t stream);
+/* replaces su3bench.simd.mult_adj_su3_mat_4vec with `outs` (simd.py:182-194; scalar.py:149-165):
+ * c_d = adj(a4[d]) b written to four separate (nsites,3,2) destinations c0..c3.
+ * (The packed form, outs omitted, is su3g_mult_adj_su3_mat_vec_4dir.) */
+SU3G_API int su3g_mult_adj_su3_mat_4vec_f32(const float *a4, const float *b, float *c0, float *c1, float *c2, float *c3,
+                                            int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_mult_adj_su3_mat_4vec_f64(const double *a4, const double *b, double *c0, double *c1, double *c2,
+                                            double *c3, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.scalar_mult_add_su3_vector (simd.py:233-239; scalar.py:208-215)
+ * c = a + s*b; s_per_site (nsites reals) overrides s when non-NULL */
+SU3G_API int su3g_scalar_mult_add_su3_vector_f32(const float *a, const float *b, float s, const float *s_per_site, float *c,
+                                                 int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_scalar_mult_add_su3_vector_f64(const double *a, const double *b, double s, const double *s_per_site,
+                                                 double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.su3_projector (simd.py:242-251; scalar.py:218-230): c[i][j] = a[i] conj(b[j]), c a matrix */
+SU3G_API int su3g_su3_projector_f32(const float *a, const float *b, float *c, int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_su3_projector_f64(const double *a, const double *b, double *c, int64_t nsites, su3g_stream_t stream);
+/* replaces su3bench.simd.sub_four_su3_vecs (simd.py:254-259; scalar.py:233-238)
+ * a <- ((((a - b1) - b2) - b3) - b4), IN PLACE on a */
+SU3G_API int su3g_sub_four_su3_vecs_f32(float *a, const float *b1, const float *b2, const float *b3, const float *b4,
+                                        int64_t nsites, su3g_stream_t stream);
+SU3G_API int su3g_sub_four_su3_vecs_f64(double *a, const double *b1, const double *b2, const double *b3,
+                                        const double *b4, int64_t nsites, su3g_stream_t stream);
+
 /* ---- layout transforms ---------------------------------------------------
  * AoS (reference site-major, `reals_per_site` reals per site, sites x-fastest;
  * lattice.py:155-187 SiteBuffer) <-> GPU-internal t-sliced SoA:

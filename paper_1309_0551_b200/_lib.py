@@ -33,6 +33,13 @@ HOT_ROUTINES = (
     "mult_adj_su3_mat_vec_4dir",
     "mult_su3_mat_vec_sum_4dir",
 )
+# the other seven Table-1 routines with the plain (a, b, c, n, stream) signature
+EXTRA_AB_ROUTINES = (
+    "add_su3_vector",
+    "mult_su3_mat_hwvec",
+    "mult_adj_su3_mat_hwvec",
+    "su3_projector",
+)
 
 # symbol -> (argtypes builder for real type, restype)
 def _signatures():
@@ -44,9 +51,12 @@ def _signatures():
         "su3g_set_option": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
     }
     for sfx, real in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
-        for r in HOT_ROUTINES:
+        for r in HOT_ROUTINES + EXTRA_AB_ROUTINES:
             sig[f"su3g_{r}_{sfx}"] = ([_vp, _vp, _vp, _i64, _vp], ctypes.c_int)
         sig[f"su3g_scalar_mult_add_su3_matrix_{sfx}"] = ([_vp, _vp, real, _vp, _vp, _i64, _vp], ctypes.c_int)
+        sig[f"su3g_scalar_mult_add_su3_vector_{sfx}"] = ([_vp, _vp, real, _vp, _vp, _i64, _vp], ctypes.c_int)
+        sig[f"su3g_mult_adj_su3_mat_4vec_{sfx}"] = ([_vp] * 6 + [_i64, _vp], ctypes.c_int)
+        sig[f"su3g_sub_four_su3_vecs_{sfx}"] = ([_vp] * 5 + [_i64, _vp], ctypes.c_int)
         sig[f"su3g_aos_to_soa_{sfx}"] = ([_vp, _vp, _i64, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_soa_to_aos_{sfx}"] = ([_vp, _vp, _i64, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp], ctypes.c_int)

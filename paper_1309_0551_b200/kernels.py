@@ -4,14 +4,17 @@ Each function keeps the reference signature and semantics of su3bench's
 vector backend (simd.py:80-230):
 
     fn(a, b, out=None)                      -> result
-    scalar_mult_add_su3_matrix(a, b, s, out=None)
+    scalar_mult_add_su3_matrix(a, b, s, out=None), scalar_mult_add_su3_vector(a, b, s, out=None)
+    mult_adj_su3_mat_4vec(a4, b, out=None, outs=None)   -> packed result, or tuple(outs)
+    sub_four_su3_vecs(a, b1, b2, b3, b4)    -> a, updated in place
 
 * operands carry any shared leading batch shape in front of the per-object
   shape (simd.py:59-68); a wrong per-object shape or disagreeing batch shapes
   raise ValueError, as does an ``out`` of the wrong shape (simd.py:51-56);
 * the result lands in ``out`` when given (and ``out`` is returned), else in a
   fresh array of the operands' dtype;
-* inputs are never modified;
+* inputs are never modified (except ``a`` of sub_four_su3_vecs, which the
+  reference updates in place too, simd.py:254-259);
 * numpy operands (what the reference harness passes, verify.py:67-70) are
   copied to the GPU and the result copied back as numpy; CUDA torch tensors
   stay on the device and the kernel runs on the current torch stream;
@@ -98,24 +101,46 @@ def _check_shapes(name: str, args) -> tuple:
     return prefixes.pop()
 
 
+def _one_precision(name: str, args) -> torch.dtype:
+    rdtype = args[0].rdtype
+    for arg in args[1:]:
+        if arg.rdtype != rdtype:
+            raise ValueError(f"{name}: operands mix {rdtype} and {arg.rdtype}; pass one precision")
+    return rdtype
+
+
+def _check_out_shape(out, result_shape) -> None:
+    out_shape = tuple(out.shape)
+    if (isinstance(out, torch.Tensor) and out.is_complex()) or (isinstance(out, np.ndarray) and np.iscomplexobj(out)):
+        out_shape = out_shape + (2,)
+    if out_shape != result_shape:
+        raise ValueError(f"result array has shape {tuple(out.shape)}, expected {result_shape}")
+
+
+def _is_direct(out, device, rdtype) -> bool:
+    """A contiguous real CUDA tensor of the right dtype is written by the kernel itself."""
+    return (
+        isinstance(out, torch.Tensor)
+        and out.is_cuda
+        and out.device == device
+        and not out.is_complex()
+        and out.dtype == rdtype
+        and out.is_contiguous()
+    )
+
+
+_SCALAR_ROUTINES = ("scalar_mult_add_su3_matrix", "scalar_mult_add_su3_vector")
+
+
 def _run(name: str, labelled, result_kind: str, like: "_Arg", out, scalar=None):
     """Validate, stage, launch and deliver one routine call."""
     spec = routine_spec(name)
     args = [_Arg(x, kind) for (x, kind) in labelled]
     prefix = _check_shapes(name, list(zip("ab", args)))
-    rdtype = args[0].rdtype
-    for arg in args[1:]:
-        if arg.rdtype != rdtype:
-            raise ValueError(f"{name}: operands mix {rdtype} and {arg.rdtype}; pass one precision")
+    rdtype = _one_precision(name, args)
     result_shape = prefix + OPERAND_SHAPES[result_kind]
     if out is not None:
-        out_shape = tuple(out.shape)
-        if isinstance(out, torch.Tensor) and out.is_complex():
-            out_shape = out_shape + (2,)
-        elif isinstance(out, np.ndarray) and np.iscomplexobj(out):
-            out_shape = out_shape + (2,)
-        if out_shape != result_shape:
-            raise ValueError(f"result array has shape {tuple(out.shape)}, expected {result_shape}")
+        _check_out_shape(out, result_shape)
     validation.check_no_alias(out, *(a.src for a in args))
 
     device = _device()
@@ -124,22 +149,15 @@ def _run(name: str, labelled, result_kind: str, like: "_Arg", out, scalar=None):
     sfx = _SFX[rdtype]
 
     # destination: write straight into a contiguous CUDA `out`, else a scratch tensor
-    direct = (
-        isinstance(out, torch.Tensor)
-        and out.is_cuda
-        and out.device == device
-        and not out.is_complex()
-        and out.dtype == rdtype
-        and out.is_contiguous()
-    )
+    direct = _is_direct(out, device, rdtype)
     dst = out if direct else torch.empty(result_shape, dtype=rdtype, device=device)
 
     stream = _stream()
     if n > 0:
-        if spec.name == "scalar_mult_add_su3_matrix":
+        if spec.name in _SCALAR_ROUTINES:
             s_scalar, s_site = scalar
             _lib.call(
-                f"su3g_scalar_mult_add_su3_matrix_{sfx}",
+                f"su3g_{spec.name}_{sfx}",
                 devs[0].data_ptr(), devs[1].data_ptr(), s_scalar,
                 None if s_site is None else s_site.data_ptr(), dst.data_ptr(), n, stream,
             )
@@ -194,7 +212,7 @@ def _make(name: str):
     spec = routine_spec(name)
     kinds = spec.operands
     # the reference allocates its result like operand b for mat-vec families, a for mat-mat
-    like_index = 1 if spec.result in ("vec", "vec4") else 0
+    like_index = 1 if spec.result in ("vec", "vec4", "hwvec") else 0
 
     def routine(a, b, out=None):
         labelled = [(a, kinds[0]), (b, kinds[1])]
@@ -214,34 +232,124 @@ mult_su3_na = _make("mult_su3_na")
 mult_su3_an = _make("mult_su3_an")
 mult_adj_su3_mat_vec_4dir = _make("mult_adj_su3_mat_vec_4dir")
 mult_su3_mat_vec_sum_4dir = _make("mult_su3_mat_vec_sum_4dir")
+add_su3_vector = _make("add_su3_vector")
+mult_su3_mat_hwvec = _make("mult_su3_mat_hwvec")
+mult_adj_su3_mat_hwvec = _make("mult_adj_su3_mat_hwvec")
+su3_projector = _make("su3_projector")
+
+
+def _smadd(name: str, kind: str, a, b, s, out):
+    probe_a = _Arg(a, kind)
+    nd = len(OPERAND_SHAPES[kind])
+    prefix = tuple(probe_a.shape[:-nd]) if len(probe_a.shape) >= nd else ()
+    device = _device()
+    scalar = _scalar_operand(s, probe_a.rdtype, prefix, device)
+    return _run(name, [(a, kind), (b, kind)], kind, probe_a, out, scalar=scalar)
 
 
 def scalar_mult_add_su3_matrix(a, b, s, out=None):
     """c = a + s*b for real s, 0-d or per-site (drop-in for su3bench.simd.scalar_mult_add_su3_matrix)."""
-    name = "scalar_mult_add_su3_matrix"
-    probe_a = _Arg(a, "mat")
-    prefix = tuple(probe_a.shape[:-3]) if len(probe_a.shape) >= 3 else ()
+    return _smadd("scalar_mult_add_su3_matrix", "mat", a, b, s, out)
+
+
+def scalar_mult_add_su3_vector(a, b, s, out=None):
+    """c = a + s*b for real s, 0-d or per-site (drop-in for su3bench.simd.scalar_mult_add_su3_vector, simd.py:233-239)."""
+    return _smadd("scalar_mult_add_su3_vector", "vec", a, b, s, out)
+
+
+def _write_back(dst: torch.Tensor, target) -> None:
+    """Copy a device result into a caller-owned array (numpy or torch, real or complex pair view)."""
+    if isinstance(target, torch.Tensor):
+        target.copy_(torch.view_as_complex(dst) if target.is_complex() else dst)
+        return
+    host = dst.cpu().numpy()
+    if np.iscomplexobj(target):
+        target[...] = host[..., 0] + 1j * host[..., 1]
+    else:
+        target[...] = host
+
+
+def mult_adj_su3_mat_4vec(a4, b, out=None, outs=None):
+    """c_d = adj(a4[d]) b into four destinations (drop-in for su3bench.simd.mult_adj_su3_mat_4vec, simd.py:182-194).
+
+    Without ``outs`` this is the packed (…,4,3,2) form (su3g_mult_adj_su3_mat_vec_4dir); with ``outs``
+    (four (…,3,2) arrays) one launch of su3g_mult_adj_su3_mat_4vec writes each direction to its own
+    destination and the tuple is returned.
+    """
+    name = "mult_adj_su3_mat_4vec"
+    if outs is None:
+        return mult_adj_su3_mat_vec_4dir(a4, b, out=out)
+    if out is not None:
+        raise ValueError("pass either out or outs, not both")
+    if len(outs) != 4:
+        raise ValueError("outs must hold four destination vectors")
+    args = [_Arg(a4, "mat4"), _Arg(b, "vec")]
+    prefix = _check_shapes(name, list(zip(("a4", "b"), args)))
+    rdtype = _one_precision(name, args)
+    result_shape = prefix + OPERAND_SHAPES["vec"]
+    for o in outs:
+        _check_out_shape(o, result_shape)
+        validation.check_no_alias(o, a4, b)
     device = _device()
-    scalar = _scalar_operand(s, probe_a.rdtype, prefix, device)
-    return _run(name, [(a, "mat"), (b, "mat")], "mat", probe_a, out, scalar=scalar)
+    n = int(np.prod(prefix, dtype=np.int64)) if prefix else 1
+    devs = [arg.to_device(device) for arg in args]
+    dsts = [o if _is_direct(o, device, rdtype) else torch.empty(result_shape, dtype=rdtype, device=device) for o in outs]
+    if n > 0:
+        _lib.call(
+            f"su3g_{name}_{_SFX[rdtype]}", devs[0].data_ptr(), devs[1].data_ptr(),
+            *(d.data_ptr() for d in dsts), n, _stream(),
+        )
+    for o, d in zip(outs, dsts):
+        if d is not o:
+            _write_back(d, o)
+    return tuple(outs)
+
+
+def sub_four_su3_vecs(a, b1, b2, b3, b4):
+    """a <- ((((a - b1) - b2) - b3) - b4) in place; returns a (drop-in for su3bench.simd.sub_four_su3_vecs, simd.py:254-259)."""
+    name = "sub_four_su3_vecs"
+    args = [_Arg(x, "vec") for x in (a, b1, b2, b3, b4)]
+    prefix = _check_shapes(name, list(zip(("a", "b1", "b2", "b3", "b4"), args)))
+    rdtype = _one_precision(name, args)
+    if isinstance(a, np.ndarray) and not a.flags.writeable:
+        raise ValueError(f"{name}: operand a is read-only (the result is written into it)")
+    device = _device()
+    n = int(np.prod(prefix, dtype=np.int64)) if prefix else 1
+    direct = _is_direct(a, device, rdtype)
+    devs = [arg.to_device(device) for arg in args]
+    acc = a if direct else devs[0]  # otherwise a device copy (or real view) of a, written back below
+    if n > 0:
+        _lib.call(f"su3g_{name}_{_SFX[rdtype]}", acc.data_ptr(), *(d.data_ptr() for d in devs[1:]), n, _stream())
+    if not direct:
+        _write_back(acc, a)
+    return a
 
 
 KERNELS = {
+    "add_su3_vector": add_su3_vector,
+    "mult_adj_su3_mat_hwvec": mult_adj_su3_mat_hwvec,
     "mult_adj_su3_mat_vec": mult_adj_su3_mat_vec,
     "mult_adj_su3_mat_vec_4dir": mult_adj_su3_mat_vec_4dir,
+    "mult_adj_su3_mat_4vec": mult_adj_su3_mat_4vec,
     "mult_su3_an": mult_su3_an,
+    "mult_su3_mat_hwvec": mult_su3_mat_hwvec,
     "mult_su3_na": mult_su3_na,
     "mult_su3_nn": mult_su3_nn,
     "mult_su3_mat_vec": mult_su3_mat_vec,
     "mult_su3_mat_vec_sum_4dir": mult_su3_mat_vec_sum_4dir,
     "scalar_mult_add_su3_matrix": scalar_mult_add_su3_matrix,
+    "scalar_mult_add_su3_vector": scalar_mult_add_su3_vector,
+    "su3_projector": su3_projector,
+    "sub_four_su3_vecs": sub_four_su3_vecs,
 }
 assert set(KERNELS) == set(ROUTINE_NAMES)
 
 
 def apply(routine: str, *operands, out=None):
     """Invoke one kernel by name on a single operand set (simd.py:281-287)."""
-    routine_spec(routine)
+    spec = routine_spec(routine)
+    if spec.in_place:
+        return KERNELS[routine](*operands)
     return KERNELS[routine](*operands, out=out)
 
 
@@ -249,4 +357,6 @@ def batch_apply(routine: str, operands, count: int | None = None, out=None):
     """Apply one kernel to `count` stacked operand sets in one launch (simd.py:304-314)."""
     spec = routine_spec(routine)
     batch_count(spec, operands, count)
+    if spec.in_place:
+        return KERNELS[routine](*operands)
     return KERNELS[routine](*operands, out=out)

@@ -3,9 +3,10 @@
 Mirrors the reference's layout contract (su3bench types.py): complex values
 are interleaved (re, im) pairs in the last axis; per-object shapes are
     vec (3, 2), mat (3, 3, 2), mat4 (4, 3, 3, 2), vec4 (4, 3, 2), scalar ()
-(types.py:28-35), sites contiguous.  Only the eight routines on the hot path
-(BASELINE.json north_star) are registered; their names and operand kinds are
-the reference's (types.py:81-100).
+(types.py:28-35), sites contiguous.  All fifteen Table-1 routines are
+registered with the reference's names, operand kinds and order
+(types.py:81-100); ``HOT_ROUTINE_NAMES`` are the eight on the hot path
+(BASELINE.json north_star), the other seven are SURVEY.md 8(f) f1.
 """
 from __future__ import annotations
 
@@ -43,18 +44,35 @@ class RoutineSpec:
 ROUTINES: dict[str, RoutineSpec] = {
     spec.name: spec
     for spec in (
+        RoutineSpec("add_su3_vector", ("vec", "vec"), "vec"),
+        RoutineSpec("mult_adj_su3_mat_hwvec", ("mat", "hwvec"), "hwvec"),
         RoutineSpec("mult_adj_su3_mat_vec", ("mat", "vec"), "vec"),
         RoutineSpec("mult_adj_su3_mat_vec_4dir", ("mat4", "vec"), "vec4"),
+        RoutineSpec("mult_adj_su3_mat_4vec", ("mat4", "vec"), "vec4"),
         RoutineSpec("mult_su3_an", ("mat", "mat"), "mat"),
+        RoutineSpec("mult_su3_mat_hwvec", ("mat", "hwvec"), "hwvec"),
         RoutineSpec("mult_su3_na", ("mat", "mat"), "mat"),
         RoutineSpec("mult_su3_nn", ("mat", "mat"), "mat"),
         RoutineSpec("mult_su3_mat_vec", ("mat", "vec"), "vec"),
         RoutineSpec("mult_su3_mat_vec_sum_4dir", ("mat4", "vec4"), "vec"),
         RoutineSpec("scalar_mult_add_su3_matrix", ("mat", "mat", "scalar"), "mat"),
+        RoutineSpec("scalar_mult_add_su3_vector", ("vec", "vec", "scalar"), "vec"),
+        RoutineSpec("su3_projector", ("vec", "vec"), "mat"),
+        RoutineSpec("sub_four_su3_vecs", ("vec", "vec", "vec", "vec", "vec"), "vec", in_place=True),
     )
 }
 
 ROUTINE_NAMES = tuple(ROUTINES)
+HOT_ROUTINE_NAMES = (
+    "mult_su3_mat_vec",
+    "mult_adj_su3_mat_vec",
+    "mult_su3_nn",
+    "mult_su3_na",
+    "mult_su3_an",
+    "mult_adj_su3_mat_vec_4dir",
+    "mult_su3_mat_vec_sum_4dir",
+    "scalar_mult_add_su3_matrix",
+)
 
 
 def dtype_for(precision) -> np.dtype:

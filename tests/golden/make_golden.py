@@ -39,14 +39,27 @@ HOT = (
     "mult_su3_mat_vec_sum_4dir",
     "scalar_mult_add_su3_matrix",
 )
+EXTRA = (
+    "add_su3_vector",
+    "mult_su3_mat_hwvec",
+    "mult_adj_su3_mat_hwvec",
+    "mult_adj_su3_mat_4vec",
+    "scalar_mult_add_su3_vector",
+    "su3_projector",
+    "sub_four_su3_vecs",
+)
 PREC = ("single", "double")
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def ref_batch(routine, ops):
-    """su3bench vector backend, asserted bit-equal to its scalar backend."""
-    got = simd.batch_apply(routine, ops)
-    chk = scalar.batch_apply(routine, ops)
+    """su3bench vector backend, asserted bit-equal to its scalar backend (in-place routine: on copies)."""
+    if types.routine_spec(routine).in_place:
+        got = simd.batch_apply(routine, [ops[0].copy()] + list(ops[1:]))
+        chk = scalar.batch_apply(routine, [ops[0].copy()] + list(ops[1:]))
+    else:
+        got = simd.batch_apply(routine, ops)
+        chk = scalar.batch_apply(routine, ops)
     assert np.array_equal(got, chk), routine
     return got
 
@@ -55,7 +68,7 @@ def routines_fixture():
     out = {}
     for prec in PREC:
         dt = types.dtype_for(prec)
-        for routine in HOT:
+        for routine in HOT + EXTRA:
             # (1) the reference's own verify draw: uniform [-1, 1] operands,
             #     per-site scalar for smadd (verify.py:86, types.py:229-243)
             rng = np.random.default_rng([verify.DEFAULT_SEED, types.ROUTINE_NAMES.index(routine), dt.itemsize])
@@ -67,7 +80,7 @@ def routines_fixture():
             # (2) integer-valued operands in [-8, 8]: every intermediate exact
             irng = np.random.default_rng([7, types.ROUTINE_NAMES.index(routine), dt.itemsize])
             iops = [irng.integers(-8, 9, size=op.shape).astype(dt) for op in ops]
-            if routine == "scalar_mult_add_su3_matrix":
+            if routine in ("scalar_mult_add_su3_matrix", "scalar_mult_add_su3_vector"):
                 iops[2] = dt.type(0.5)
             ires = ref_batch(routine, iops)
             for i, op in enumerate(iops):

@@ -19,7 +19,7 @@ def header_symbols():
 
 def test_header_declares_the_full_abi():
     syms = header_symbols()
-    for r in _lib.HOT_ROUTINES + ("scalar_mult_add_su3_matrix",):
+    for r in types.ROUTINE_NAMES:  # all fifteen Table-1 routines (the packed 4vec form is the 4dir entry)
         for sfx in ("f32", "f64"):
             assert f"su3g_{r}_{sfx}" in syms
     assert "su3g_nn_sweep_f32" in syms and "su3g_link_product_f64" in syms
@@ -50,8 +50,11 @@ def test_invalid_arguments_rejected_without_touching_the_device():
     assert lib.su3g_link_product_f64(None, None, 4, 4, 4, 4, 0.5, 7, None) == _lib.SU3G_EINVAL
     with pytest.raises(ValueError):
         _lib.check(_lib.SU3G_EINVAL, "x")
+    assert lib.su3g_sub_four_su3_vecs_f32(None, None, None, None, None, -2, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_mult_adj_su3_mat_4vec_f64(None, None, None, None, None, None, -1, None) == _lib.SU3G_EINVAL
     # zero sites is a valid no-op
     assert lib.su3g_mult_su3_nn_f64(None, None, None, 0, None) == _lib.SU3G_OK
+    assert lib.su3g_sub_four_su3_vecs_f64(None, None, None, None, None, 0, None) == _lib.SU3G_OK
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
@@ -105,7 +108,9 @@ def test_alias_check_under_debug_validation():
 
 
 def test_registry_and_batch_count():
-    assert set(types.ROUTINE_NAMES) == set(_lib.HOT_ROUTINES) | {"scalar_mult_add_su3_matrix"}
+    assert set(types.HOT_ROUTINE_NAMES) == set(_lib.HOT_ROUTINES) | {"scalar_mult_add_su3_matrix"}
+    assert len(types.ROUTINE_NAMES) == 15 and set(types.HOT_ROUTINE_NAMES) <= set(types.ROUTINE_NAMES)
+    assert types.routine_spec("sub_four_su3_vecs").in_place
     spec = types.routine_spec("scalar_mult_add_su3_matrix")
     a = np.zeros((5, 3, 3, 2))
     assert types.batch_count(spec, [a, a, 0.5]) == 5

@@ -27,6 +27,10 @@ def run(extra, env=None, steps="20"):
     print(line, flush=True)
 
 
+EXTRA = ("add_su3_vector", "mult_su3_mat_hwvec", "mult_adj_su3_mat_hwvec", "mult_adj_su3_mat_4vec",
+         "scalar_mult_add_su3_vector", "su3_projector", "sub_four_su3_vecs")
+
+
 def main():
     which = sys.argv[1:] or ["configs", "routines", "sweeps"]
     if "configs" in which:
@@ -38,6 +42,10 @@ def main():
     if "routines" in which:
         for dt in ("f32", "f64"):
             for r in ROUTINES:
+                run(["--workload", f"routine:{r}", "--dtype", dt, "--sites", str(1 << 24), "--no-cpu-baseline"])
+    if "extra" in which:  # the other seven Table-1 routines
+        for dt in ("f32", "f64"):
+            for r in EXTRA:
                 run(["--workload", f"routine:{r}", "--dtype", dt, "--sites", str(1 << 24), "--no-cpu-baseline"])
     if "sweeps" in which:
         run(["--workload", "nn32", "--dtype", "f32"])
