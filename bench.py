@@ -588,7 +588,8 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
         "h2d_bytes_per_step": int(h2d),
         "d2h_bytes_per_step": int(d2h),
         "steps": steps,
-        "path": "pinned host AoS -> H2D -> AoS->SoA -> kernels (+NCCL halos) -> SoA->AoS -> D2H",
+        "path": ("pinned host AoS -> H2D -> drop-in routine (AoS, C ABI) -> D2H" if cfg["kind"] == "routine" else
+                 "pinned host AoS -> H2D -> AoS->SoA -> kernels (+NCCL halos) -> SoA->AoS -> D2H"),
     }
 
 

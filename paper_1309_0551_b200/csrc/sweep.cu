@@ -23,9 +23,9 @@ extern int g_tma_threads;
 // NN sweep, one thread per site
 // ---------------------------------------------------------------------------
 template <typename T, bool FUSED>
-__global__ void __launch_bounds__(256)
-    k_nn_sweep(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin, int t_end,
-               const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC) {
+__device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
+                                              const Geom& g, int t_begin, int t_end, const T* __restrict__ v_hi,
+                                              const T* __restrict__ w_lo, int ZC) {
     // visiting order (z-chunk of ZC planes, t, z, y, x): the t-1 slice a site reads (U_t, v)
     // was streamed ZC*nx*ny sites earlier, not a whole slice earlier -> L2 hits
     const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -85,6 +85,22 @@ __global__ void __launch_bounds__(256)
     }
 #pragma unroll
     for (int k = 0; k < 6; ++k) out[(int64_t(t) * 6 + k) * F + s3] = acc[k];
+}
+
+// plain bounds: ptxas picks 64-98 registers; an explicit minBlocks of 1 would let it take 252
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(256)
+    k_nn_sweep(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin, int t_end,
+               const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC) {
+    nn_sweep_body<T, FUSED>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+}
+
+// occupancy A/B (nn_variant 6): registers capped for MINB CTAs per SM
+template <typename T, bool FUSED, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_nn_sweep_capped(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin,
+                      int t_end, const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC) {
+    nn_sweep_body<T, FUSED>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
 }
 
 template <typename T, bool FUSED>
@@ -406,7 +422,7 @@ static bool walk_shape(int nx, int ny, int nz, int max_threads, int& BY, int& BZ
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 2 walk, 3 TMA walk
-static std::atomic<int> g_link_variant{0};  // 0 auto, 1 generic, 2 block walk, 3 ring, 4 plane-split
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 generic, 2 block walk, 3 ring, 4 plane-split, 5, 6 rows
 
 template <typename T>
 static int launch_walk(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
@@ -491,6 +507,11 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     // (measured: 64^3 f64 0.64 -> 0.70 of HBM; 32^4 f64, whose slice is 22 MB, slightly prefers t-major)
     const bool big_slice = double(g.F) * 84 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
     const int ZC = (variant == 4 || !big_slice) ? nz : chunk_planes(nz, 8);  // 4: t-major order (A/B knob)
+    if (variant == 6) {  // occupancy A/B knob: register cap for 3 CTAs (24 warps) per SM
+        if (mode == SU3G_FMA) k_nn_sweep_capped<T, true, 3><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+        else k_nn_sweep_capped<T, false, 3><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+        return check_launch("nn_sweep");
+    }
     if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
     else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
     return check_launch("nn_sweep");
@@ -551,6 +572,10 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     const bool big_slice = double(g.F) * 72 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
     int ZC = big_slice ? chunk_planes(nz, 8) : nz;
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
+    if (lv == 6) {
+        return mode == SU3G_FMA ? launch_link_rows<T, true>(U, acc, g, s, ZC, st)
+                                : launch_link_rows<T, false>(U, acc, g, s, ZC, st);
+    }
     if (mode == SU3G_FMA) k_link_product<T, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     else k_link_product<T, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     return check_launch("link_product");
@@ -565,10 +590,10 @@ extern "C" {
 int su3g_set_option(const char* name, int64_t value) {
     if (name == nullptr) return fail_invalid("set_option: null name");
     if (std::strcmp(name, "nn_variant") == 0) {
-        if (value < 0 || value > 5)
+        if (value < 0 || value > 6)
             return fail_invalid(
                 "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major), "
-                "5 (tma walk, register-staged)");
+                "5 (tma walk, register-staged), 6 (generic, 3 CTAs/SM register cap)");
         g_nn_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }
@@ -588,10 +613,10 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 5)
+        if (value < 0 || value > 6)
             return fail_invalid(
                 "set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring), 4 (planes), "
-                "5 (generic, natural order)");
+                "5 (generic, natural order), 6 (low-register rows)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

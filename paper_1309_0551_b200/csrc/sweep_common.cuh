@@ -74,6 +74,8 @@ int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cu
 
 template <typename T, bool FUSED>
 int launch_link_planes(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
+template <typename T, bool FUSED>
+int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);
 
 // f64 TMA t-walk with a register-staged main operand (nn_tma64.cu); 1 = not applicable.
 template <typename T, bool FUSED>

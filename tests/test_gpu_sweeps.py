@@ -93,6 +93,13 @@ def test_link_product_config3_full_size():
     assert np.array_equal(got, want)
     del got
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
+    from paper_1309_0551_b200 import _lib
+
+    _lib.set_option("link_variant", 6)  # low-register rows kernel at full size (z-chunked order)
+    try:
+        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+    finally:
+        _lib.set_option("link_variant", 0)
 
 
 @pytest.mark.parametrize("C", [6, 18, 24, 72])
@@ -236,8 +243,10 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
         _lib.set_option("no_such_option", 1)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4], ids=["auto", "generic", "block-walk", "ring", "planes"])
-@pytest.mark.parametrize("dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4)])
+@pytest.mark.parametrize(
+    "variant", [0, 1, 2, 3, 4, 6], ids=["auto", "generic", "block-walk", "ring", "planes", "rows"]
+)
+@pytest.mark.parametrize("dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97)])
 def test_link_product_variants_bitwise(variant, dims, precision):
     from paper_1309_0551_b200 import _lib
 
