@@ -256,6 +256,9 @@ def run_b200(args, rank, world, local):
         from paper_1309_0551_b200 import _lib as _l
 
         _l.set_option("link_variant", int(os.environ["SU3G_LINK_VARIANT"]))
+    for env, opt in (("SU3G_LINK_MINB", "link_minb"), ("SU3G_LINK_EARLY_C", "link_early_c")):
+        if os.environ.get(env):
+            _l.set_option(opt, int(os.environ[env]))
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     gen = torch.Generator(device=dev)
     gen.manual_seed(inputs.SEED + 7919 * rank)

@@ -56,8 +56,12 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "nn_variant":   0 auto, 1 generic (z-chunked order), 2 register t-walk, 3 TMA t-walk,
  *                   4 generic in plain t-major order (A/B), 5 register-staged f64 TMA walk,
  *                   6 generic capped at 3 CTAs/SM worth of registers (A/B)
- *   "link_variant": 0 auto (= generic), 1 generic, 2 block walk, 3 cp.async ring, 4 plane-split,
- *                   5 generic in plain t-major order (A/B), 6 low-register rows (accumulator in smem)
+ *   "link_variant": 0 auto (= 6), 1 generic one-thread-per-site, 2 block walk, 3 cp.async ring,
+ *                   4 plane-split, 5 generic in plain t-major order (A/B), 6 low-register rows
+ *                   (accumulator in smem)
+ *   "link_minb":    CTAs/SM the rows kernel's register budget targets: 0 default (f64 4, f32 6),
+ *                   3, 4, 5, 6 or 8
+ *   "link_early_c": 1 = the rows kernel gathers U_mu(x+nu) together with U_nu(x+mu) (A/B)
  *   "sm_reserve":   SMs the persistent sweep kernels leave free for concurrent kernels
  *                   (NCCL halo exchange of a t-slab sweep); default 0 */
 SU3G_API int su3g_set_option(const char *name, int64_t value);

@@ -48,7 +48,7 @@ __device__ __forceinline__ void dot3(PF p, QF q, T& re, T& im) {
 
 }  // namespace
 
-template <typename T, bool FUSED, int MINB>
+template <typename T, bool FUSED, int MINB, bool EARLY_C>
 __global__ void __launch_bounds__(128, MINB)
     k_link_rows(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC) {
     __shared__ T sacc[18 * 128];
@@ -71,7 +71,9 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll 1
     for (int pl = 0; pl < 6; ++pl) {
         const int mu = c_plane_mu[pl], nu = c_plane_nu[pl];
-        T tm[18];
+        T tm[18], c[18];
+        // EARLY_C: gather C with B (both in flight together, +18 live reals); else after T is built
+        if constexpr (EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);
         {
             T b[18];
             ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b);  // B = U_nu(x + mu)
@@ -86,8 +88,7 @@ __global__ void __launch_bounds__(128, MINB)
                                           tm[(3 * i + k) * 2 + 1]);
             }
         }
-        T c[18];
-        ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);  // C = U_mu(x + nu)
+        if constexpr (!EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);  // C = U_mu(x + nu)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -109,12 +110,27 @@ __global__ void __launch_bounds__(128, MINB)
     for (int k = 0; k < 18; ++k) acc_out[(int64_t(t) * 18 + k) * g.F + s3] = acc[k * 128];
 }
 
+int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
+int g_link_early_c = 0;  // su3g_set_option("link_early_c"): gather C together with B
+
+template <typename T, bool FUSED, bool EARLY_C>
+static void launch_rows_minb(const T* U, T* acc, const Geom& g, T s, int ZC, unsigned grid, int minb, cudaStream_t st) {
+    switch (minb) {
+        case 3: k_link_rows<T, FUSED, 3, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 5: k_link_rows<T, FUSED, 5, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 6: k_link_rows<T, FUSED, 6, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 8: k_link_rows<T, FUSED, 8, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        default: k_link_rows<T, FUSED, 4, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+    }
+}
+
 template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st) {
-    constexpr int MINB = sizeof(T) == 8 ? 4 : 6;
     const int64_t n = g.F * g.nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
-    k_link_rows<T, FUSED, MINB><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
+    const int minb = g_link_minb ? g_link_minb : (sizeof(T) == 8 ? 4 : 6);
+    if (g_link_early_c) launch_rows_minb<T, FUSED, true>(U, acc, g, s, ZC, grid, minb, st);
+    else launch_rows_minb<T, FUSED, false>(U, acc, g, s, ZC, grid, minb, st);
     return check_launch("link_product(rows)");
 }
 
