@@ -240,23 +240,12 @@ def run_b200(args, rank, world, local):
 
     cfg = workload_config(args, world)
     dev = torch.device("cuda", local)
-    if os.environ.get("SU3G_NN_VARIANT"):
-        from paper_1309_0551_b200 import _lib as _l
+    # A/B tuning knobs (su3g_set_option), from the environment
+    from paper_1309_0551_b200 import _lib as _l
 
-        _l.set_option("nn_variant", int(os.environ["SU3G_NN_VARIANT"]))
-    if os.environ.get("SU3G_CHUNK_PROLOGUE_X10"):
-        from paper_1309_0551_b200 import _lib as _l
-
-        _l.set_option("chunk_prologue_x10", int(os.environ["SU3G_CHUNK_PROLOGUE_X10"]))
-    if os.environ.get("SU3G_NN_TMA_THREADS"):
-        from paper_1309_0551_b200 import _lib as _l
-
-        _l.set_option("nn_tma_threads", int(os.environ["SU3G_NN_TMA_THREADS"]))
-    if os.environ.get("SU3G_LINK_VARIANT"):
-        from paper_1309_0551_b200 import _lib as _l
-
-        _l.set_option("link_variant", int(os.environ["SU3G_LINK_VARIANT"]))
-    for env, opt in (("SU3G_LINK_MINB", "link_minb"), ("SU3G_LINK_EARLY_C", "link_early_c")):
+    for env, opt in (("SU3G_NN_VARIANT", "nn_variant"), ("SU3G_CHUNK_PROLOGUE_X10", "chunk_prologue_x10"),
+                     ("SU3G_NN_TMA_THREADS", "nn_tma_threads"), ("SU3G_LINK_VARIANT", "link_variant"),
+                     ("SU3G_LINK_MINB", "link_minb"), ("SU3G_LINK_EARLY_C", "link_early_c")):
         if os.environ.get(env):
             _l.set_option(opt, int(os.environ[env]))
     tdt = torch.float32 if args.dtype == "f32" else torch.float64

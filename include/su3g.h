@@ -135,6 +135,18 @@ SU3G_API int su3g_sub_four_su3_vecs_f32(float *a, const float *b1, const float *
 SU3G_API int su3g_sub_four_su3_vecs_f64(double *a, const double *b1, const double *b2, const double *b3,
                                         const double *b4, int64_t nsites, su3g_stream_t stream);
 
+/* ---- seeded fill ---------------------------------------
+ * replaces su3bench.lattice.SiteBuffer.randomize (lattice.py:192-197), i.e. numpy
+ * Generator.uniform(low, high) on the default PCG64 bit generator, written straight
+ * into device memory: out[i] = draw (skip + i) of the stream whose 128-bit state and
+ * increment are (state_hi:state_lo, inc_hi:inc_lo) as numpy's
+ * bit_generator.state reports them.  Bit-identical to numpy (f32: the float64 draw
+ * rounded to nearest, as numpy's assignment into a float32 array). */
+SU3G_API int su3g_uniform_fill_f32(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t skip,
+                                   double low, double high, float *out, int64_t n, su3g_stream_t stream);
+SU3G_API int su3g_uniform_fill_f64(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t skip,
+                                   double low, double high, double *out, int64_t n, su3g_stream_t stream);
+
 /* ---- layout transforms ---------------------------------------------------
  * AoS (reference site-major, `reals_per_site` reals per site, sites x-fastest;
  * lattice.py:155-187 SiteBuffer) <-> GPU-internal t-sliced SoA:

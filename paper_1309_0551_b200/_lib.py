@@ -23,6 +23,7 @@ SU3G_FMA = 1
 _vp = ctypes.c_void_p
 _i32 = ctypes.c_int32
 _i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
 
 HOT_ROUTINES = (
     "mult_su3_mat_vec",
@@ -57,6 +58,7 @@ def _signatures():
         sig[f"su3g_scalar_mult_add_su3_vector_{sfx}"] = ([_vp, _vp, real, _vp, _vp, _i64, _vp], ctypes.c_int)
         sig[f"su3g_mult_adj_su3_mat_4vec_{sfx}"] = ([_vp] * 6 + [_i64, _vp], ctypes.c_int)
         sig[f"su3g_sub_four_su3_vecs_{sfx}"] = ([_vp] * 5 + [_i64, _vp], ctypes.c_int)
+        sig[f"su3g_uniform_fill_{sfx}"] = ([_u64] * 4 + [_i64, ctypes.c_double, ctypes.c_double, _vp, _i64, _vp], ctypes.c_int)
         sig[f"su3g_aos_to_soa_{sfx}"] = ([_vp, _vp, _i64, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_soa_to_aos_{sfx}"] = ([_vp, _vp, _i64, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp], ctypes.c_int)

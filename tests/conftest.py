@@ -16,6 +16,11 @@ def pytest_configure(config):
 
 
 @pytest.fixture(scope="session")
+def golden_sitebuffer():
+    return dict(np.load(os.path.join(GOLDEN, "sitebuffer.npz")))
+
+
+@pytest.fixture(scope="session")
 def golden_routines():
     return dict(np.load(os.path.join(GOLDEN, "routines.npz")))
 

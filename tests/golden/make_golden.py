@@ -4,7 +4,8 @@ Run in the build container only (it needs /root/reference):
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
 
-Outputs ``tests/golden/routines.npz`` and ``tests/golden/sweeps.npz``.  Every
+Outputs ``tests/golden/routines.npz``, ``tests/golden/sweeps.npz`` and
+``tests/golden/sitebuffer.npz`` (fields randomized by su3bench's SiteBuffer).  Every
 output array below was computed by su3bench's own code path -- the vector
 backend ``simd.batch_apply`` (reference simd.py:304-314), cross-checked
 bit-for-bit against the scalar backend ``scalar.batch_apply``
@@ -183,10 +184,27 @@ def sweeps_fixture():
     return out
 
 
+SITEBUFFER_FIELDS = {"links": "mat4", "src": "vec", "b": "mat", "scale": "scalar", "h": "hwvec"}
+
+
+def sitebuffer_fixture():
+    """Fields randomized by the reference's own SiteBuffer (lattice.py:155-197)."""
+    out = {}
+    lat = lattice.Lattice4D.from_dims((2, 3, 2, 3))
+    for prec in PREC:
+        for seed in (12345, 20020614):
+            buf = lattice.SiteBuffer(lat, SITEBUFFER_FIELDS, precision=prec)
+            buf.randomize(seed)
+            for name in SITEBUFFER_FIELDS:
+                out[f"sitebuffer/{prec}/{seed}/{name}"] = np.array(buf[name])
+    return out
+
+
 def main():
+    np.savez_compressed(os.path.join(HERE, "sitebuffer.npz"), **sitebuffer_fixture())
     np.savez_compressed(os.path.join(HERE, "routines.npz"), **routines_fixture())
     np.savez_compressed(os.path.join(HERE, "sweeps.npz"), **sweeps_fixture())
-    for name in ("routines.npz", "sweeps.npz"):
+    for name in ("routines.npz", "sweeps.npz", "sitebuffer.npz"):
         p = os.path.join(HERE, name)
         print(name, os.path.getsize(p), "bytes")
 

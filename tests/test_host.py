@@ -219,3 +219,46 @@ def test_bench_rejects_short_warmup():
 
     with pytest.raises(SystemExit):
         bench.parse_args(["--warmup", "2"])
+
+
+def _pcg_model(state, inc, skip, n):
+    """Pure-Python PCG64 XSL-RR + uniform(-1, 1), with the jump-ahead fill.cu uses."""
+    M128, MULT = (1 << 128) - 1, 0x2360ED051FC65DA44385DF649FCCF645
+
+    def jump(delta):
+        am, ap, cm, cp = 1, 0, MULT, inc
+        while delta:
+            if delta & 1:
+                am, ap = (am * cm) & M128, (ap * cm + cp) & M128
+            cp, cm = ((cm + 1) * cp) & M128, (cm * cm) & M128
+            delta >>= 1
+        return am, ap
+
+    a, c = jump(skip + 1)
+    s = (a * state + c) & M128
+    out = []
+    for _ in range(n):
+        x = ((s >> 64) ^ s) & ((1 << 64) - 1)
+        r = s >> 122
+        x = ((x >> r) | (x << (64 - r))) & ((1 << 64) - 1) if r else x
+        out.append(-1.0 + 2.0 * ((x >> 11) * (1.0 / 9007199254740992.0)))
+        s = (s * MULT + inc) & M128
+    return np.array(out)
+
+
+@pytest.mark.parametrize("skip", [0, 1, 7, 1000, 123456789])
+def test_pcg64_jump_ahead_model_matches_numpy(skip):
+    """The jump-ahead + output function of csrc/fill.cu, modelled in Python, reproduces numpy's stream."""
+    from paper_1309_0551_b200.sitebuffer import pcg64_seed_state
+
+    state, inc = pcg64_seed_state(2024)
+    rng = np.random.default_rng(2024)
+    rng.bit_generator.advance(skip)
+    assert np.array_equal(_pcg_model(state, inc, skip, 5), rng.uniform(-1.0, 1.0, size=5))
+
+
+def test_device_sitebuffer_rejects_bad_alignment():
+    from paper_1309_0551_b200.sitebuffer import DeviceSiteBuffer
+
+    with pytest.raises(ValueError, match="power of two"):
+        DeviceSiteBuffer(lattice.Lattice4D(2, 2, 2, 2), {"a": "vec"}, alignment=12)
