@@ -38,6 +38,9 @@ FALLBACK_HBM_GBS = 6650.0
 # algorithmic (compulsory) HBM bytes per site: read each input object once, write each output once
 NN_BYTES = {"f32": 336, "f64": 672}        # U 72 reals + v 6 + out 6
 LINK_BYTES = {"f32": 360, "f64": 720}      # U 72 + acc 18
+# even/odd dslash, per lattice site per one-parity launch: all of U (forward links of the
+# output sites + backward links of their neighbours) + v on the other half + out on this half
+DSLASH_BYTES = {"f32": 288 + 24, "f64": 576 + 48}
 def _routine_layout():
     """routine -> (reals per site of each array operand, reals per site of the result), from the registry."""
     from paper_1309_0551_b200 import types as T
@@ -95,6 +98,9 @@ def workload_config(args, world):
         return dict(kind="nn", global_dims=(32, 32, 32, 32), apps=1, name="config2: periodic NN sweep 32^4, 1 application/step")
     if w == "link":
         return dict(kind="link", global_dims=(48, 48, 48, 48), apps=1, name="config3: link-product sweep 48^4, 1 sweep/step")
+    if w == "dslash":
+        return dict(kind="dslash", global_dims=(64, 64, 64, 16), apps=1,
+                    name="8(f) f3: even/odd dslash 64^3x16, D_eo + D_oe (both parities) per step")
     if w.startswith("routine:"):
         r = w.split(":", 1)[1]
         if r not in ROUTINE_REALS:
@@ -285,6 +291,30 @@ def run_b200(args, rank, world, local):
         launches_per_step = apps * launches_per_app
         sites_per_step = lat.volume * apps  # per rank
         del U_aos
+    elif cfg["kind"] == "dslash":
+        lat = Lattice4D(*cfg["global_dims"])  # replicas: every rank runs its own lattice
+        U_aos = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen)
+        U = Field.from_aos(lat, "mat4", U_aos)
+        del U_aos
+        v = Field.from_aos(lat, "vec", inputs.random_vectors_torch(lat.volume, None, tdt, dev, gen))
+        dout = v.empty_like()
+        bytes_per_launch = lat.volume * DSLASH_BYTES[args.dtype]
+        mode = args.mode
+
+        def step(record=False):
+            for parity in (0, 1):
+                if record:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                sweeps.dslash(U, v, parity, out=dout, mode=mode)
+                if record:
+                    e1.record(stream)
+                    dominant_events.append((e0, e1))
+
+        launches_per_step = 2
+        sites_per_step = lat.volume
+        cfg["name"] += f", {mode} arithmetic"
     elif cfg["kind"] == "link":
         lat = Lattice4D(*cfg["global_dims"])
         if world > 1:
@@ -414,7 +444,7 @@ def run_b200(args, rank, world, local):
         "scaling": "weak" if args.workload == "nn-weak" else ("strong" if args.workload == "nn-strong" else "weak"),
         "vs_baseline": None,
         "dtype": args.dtype,
-        "arithmetic": args.mode if cfg["kind"] in ("nn", "link") else "exact",
+        "arithmetic": args.mode if cfg["kind"] in ("nn", "link", "dslash") else "exact",
         "data": "synthetic (seeded SU(3) Gram-Schmidt links + complex-Gaussian vectors, generated on device)",
         "config": {
             "workload": cfg["name"],
@@ -428,7 +458,8 @@ def run_b200(args, rank, world, local):
         "hbm_gbs": achieved,
         "roofline": {
             "bound": "hbm",
-            "kernel": {"nn": "k_nn_tma (f32) / k_nn_sweep (f64)", "link": "k_link_product"}.get(cfg["kind"], "k_stream"),
+            "kernel": {"nn": "k_nn_tma (f32) / k_nn_sweep (f64)", "link": "k_link_rows",
+                       "dslash": "k_dslash"}.get(cfg["kind"], "k_stream"),
             "achieved": achieved,
             "peak": peak,
             "peak_source": peak_src,
@@ -502,6 +533,31 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
         h2d = U_h.numel() * U_h.element_size() + v_h.numel() * v_h.element_size()
         d2h = out_h.numel() * out_h.element_size()
         sites = lat.volume * cfg["apps"]
+    elif cfg["kind"] == "dslash":
+        lat = Lattice4D(*cfg["global_dims"])
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(98)
+        U_h = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen).cpu().pin_memory()
+        v_h = inputs.random_vectors_torch(lat.volume, None, tdt, dev, gen).cpu().pin_memory()
+        out_h = torch.empty_like(v_h).pin_memory()
+        U_d, v_d, o_d = torch.empty_like(U_h, device=dev), torch.empty_like(v_h, device=dev), torch.empty_like(v_h, device=dev)
+        Uf, vf = Field(lat, "mat4", tdt, dev), Field(lat, "vec", tdt, dev)
+        of = vf.empty_like()
+        mode = args.mode
+
+        def step():
+            U_d.copy_(U_h, non_blocking=True)
+            v_d.copy_(v_h, non_blocking=True)
+            Field.from_aos(lat, "mat4", U_d, out=Uf)
+            Field.from_aos(lat, "vec", v_d, out=vf)
+            for parity in (0, 1):
+                sweeps.dslash(Uf, vf, parity, out=of, mode=mode)
+            of.to_aos(out=o_d)
+            out_h.copy_(o_d, non_blocking=True)
+
+        h2d = U_h.numel() * U_h.element_size() + v_h.numel() * v_h.element_size()
+        d2h = out_h.numel() * out_h.element_size()
+        sites = lat.volume
     elif cfg["kind"] == "link":
         lat = Lattice4D(*cfg["global_dims"])
         gen = torch.Generator(device=dev)
@@ -597,7 +653,7 @@ def _cpu_sample(cfg, dtype, small=False):
 
     dt = np.float32 if dtype == "f32" else np.float64
     rng = inputs.config_rng(424242)
-    if cfg["kind"] == "nn":
+    if cfg["kind"] in ("nn", "dslash"):  # dslash: both parities = one NN application's site-ops
         nx, ny, nz = cfg["global_dims"][:3]
         if small:
             nx, ny, nz = min(nx, 32), min(ny, 32), min(nz, 32)
@@ -654,7 +710,7 @@ def _parallel_nn(state, threads):
 
 def cpu_baseline(args, cfg, threads=1, budget_s=10.0):
     fn, sites, state, desc = _cpu_sample(cfg, args.dtype)
-    if threads > 1 and cfg["kind"] == "nn":
+    if threads > 1 and cfg["kind"] in ("nn", "dslash"):
         def call():
             return _parallel_nn(state, threads)
     else:
@@ -684,7 +740,7 @@ def run_reference(args, rank, world):
         return None
     threads = os.cpu_count() or 1
     fn, sites, state, desc = _cpu_sample(cfg, args.dtype, small=True)
-    call = (lambda: _parallel_nn(state, threads)) if cfg["kind"] == "nn" else fn
+    call = (lambda: _parallel_nn(state, threads)) if cfg["kind"] in ("nn", "dslash") else fn
     if cfg["kind"] != "nn":
         threads = 1
     for _ in range(args.warmup):

@@ -59,9 +59,10 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "link_variant": 0 auto (= 6), 1 generic one-thread-per-site, 2 block walk, 3 cp.async ring,
  *                   4 plane-split, 5 generic in plain t-major order (A/B), 6 low-register rows
  *                   (accumulator in smem)
- *   "link_minb":    CTAs/SM the rows kernel's register budget targets: 0 default (f64 4, f32 6),
- *                   3, 4, 5, 6 or 8
- *   "link_early_c": 1 = the rows kernel gathers U_mu(x+nu) together with U_nu(x+mu) (A/B)
+ *   "link_minb":    CTAs/SM the rows kernel's register budget targets: 0 default (f64: 4 exact,
+ *                   3 FMA; f32: 6), 3, 4, 5, 6 or 8
+ *   "link_early_c": 1 = the rows kernel gathers U_mu(x+nu) together with U_nu(x+mu), 0 = after
+ *                   T = A B is built, -1 = default (1 for f32, 0 for f64)
  *   "sm_reserve":   SMs the persistent sweep kernels leave free for concurrent kernels
  *                   (NCCL halo exchange of a t-slab sweep); default 0 */
 SU3G_API int su3g_set_option(const char *name, int64_t value);
@@ -192,6 +193,19 @@ SU3G_API int su3g_nn_halo_w_f32(const float *U, const float *v, float *w_face, i
                        int32_t mode, su3g_stream_t stream);
 SU3G_API int su3g_nn_halo_w_f64(const double *U, const double *v, double *w_face, int32_t nx, int32_t ny, int32_t nz,
                        int32_t nt, int32_t mode, su3g_stream_t stream);
+
+/* ---- even/odd dslash -----------------------------------
+ * out(x) = sum_mu U_mu(x) v(x+mu) - sum_mu U_mu(x-mu)^dag v(x-mu) for the sites of one
+ * parity, (x+y+z+t) % 2 == parity, only; those read v on the other parity only.  Fused:
+ * forward mat_vec x4, backward adjoint products of the neighbours (adj_4dir), the
+ * add_su3_vector chain and sub_four_su3_vecs, in the NN sweep's association, so the
+ * values equal su3g_nn_sweep's on those sites bit for bit (EXACT).  Sites of the other
+ * parity in `out` are left untouched.  Every extent must be even; periodic lattice.
+ * U: t-sliced SoA, 72 reals/site; v, out: t-sliced SoA, 6 reals/site (full lattice). */
+SU3G_API int su3g_dslash_f32(const float *U, const float *v, float *out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                             int32_t parity, int32_t mode, su3g_stream_t stream);
+SU3G_API int su3g_dslash_f64(const double *U, const double *v, double *out, int32_t nx, int32_t ny, int32_t nz,
+                             int32_t nt, int32_t parity, int32_t mode, su3g_stream_t stream);
 
 /* ---- link-product sweep (BASELINE configs[3]) ------------------------------
  * acc(x) = sum over (mu,nu) in (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) of

@@ -96,3 +96,26 @@ def nn_sweep_slab(U_slab, v_slab, dims_local, v_hi, w_lo):
     bw.append(np.concatenate([w_lo, w_local], axis=0))
     F = R.add_su3_vector(R.add_su3_vector(R.add_su3_vector(fw[0], fw[1]), fw[2]), fw[3])
     return R.sub_four_su3_vecs(F, bw[0], bw[1], bw[2], bw[3])
+
+
+def parity_mask(dims):
+    """Boolean (V,) mask of even sites, (x+y+z+t) % 2 == 0, x fastest (lattice.py:3-6)."""
+    nx, ny, nz, nt = dims
+    t, z, y, x = np.meshgrid(np.arange(nt), np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    return ((x + y + z + t) % 2 == 0).reshape(-1)
+
+
+def dslash(U, v, dims, parity):
+    """Even/odd dslash: the NN sweep on the sites of one parity, 0 elsewhere.
+
+    On a lattice with even extents every neighbour of a parity-p site has parity
+    1-p, so the values are the composed NN sweep's (forward mat_vec chain, then
+    sub_four of the neighbours' adjoint products), restricted to those sites.
+    """
+    if any(d % 2 for d in dims):
+        raise ValueError("dslash needs even lattice extents")
+    full = nn_sweep(U, v, dims)
+    keep = parity_mask(dims) if parity == 0 else ~parity_mask(dims)
+    out = np.zeros_like(full)
+    out[keep] = full[keep]
+    return out

@@ -63,6 +63,7 @@ def _signatures():
         sig[f"su3g_soa_to_aos_{sfx}"] = ([_vp, _vp, _i64, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_halo_w_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
+        sig[f"su3g_dslash_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_link_product_{sfx}"] = ([_vp, _vp, _i32, _i32, _i32, _i32, real, _i32, _vp], ctypes.c_int)
     return sig
 

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(128, MINB)
 }
 
 int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
-int g_link_early_c = 0;  // su3g_set_option("link_early_c"): gather C together with B
+int g_link_early_c = -1;  // su3g_set_option("link_early_c"): gather C together with B (-1 = default)
 
 template <typename T, bool FUSED, bool EARLY_C>
 static void launch_rows_minb(const T* U, T* acc, const Geom& g, T s, int ZC, unsigned grid, int minb, cudaStream_t st) {
@@ -128,8 +128,11 @@ template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st) {
     const int64_t n = g.F * g.nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
-    const int minb = g_link_minb ? g_link_minb : (sizeof(T) == 8 ? 4 : 6);
-    if (g_link_early_c) launch_rows_minb<T, FUSED, true>(U, acc, g, s, ZC, grid, minb, st);
+    // defaults from the 48^4 sweep on B200 (fraction of HBM): f64 exact minb 4 (0.427; 3 with early C 0.429),
+    // f64 FMA minb 3 (0.474 vs 0.467 at 4), f32 minb 6 with early C (0.310 vs 0.299)
+    const int minb = g_link_minb ? g_link_minb : (sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6);
+    const bool early_c = g_link_early_c >= 0 ? g_link_early_c != 0 : sizeof(T) == 4;
+    if (early_c) launch_rows_minb<T, FUSED, true>(U, acc, g, s, ZC, grid, minb, st);
     else launch_rows_minb<T, FUSED, false>(U, acc, g, s, ZC, grid, minb, st);
     return check_launch("link_product(rows)");
 }

@@ -24,26 +24,14 @@ extern int g_link_early_c;
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
 // ---------------------------------------------------------------------------
+// One site of the NN sweep: out(x) = sum_mu U_mu(x) v(x+mu) - sum_mu U_mu(x-mu)^dag v(x-mu), association of
+// the composed reference (add_su3_vector chain, then sub_four_su3_vecs).  v_hi / w_lo: t-slab halos (or null).
 template <typename T, bool FUSED>
-__device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
-                                              const Geom& g, int t_begin, int t_end, const T* __restrict__ v_hi,
-                                              const T* __restrict__ w_lo, int ZC) {
-    // visiting order (z-chunk of ZC planes, t, z, y, x): the t-1 slice a site reads (U_t, v)
-    // was streamed ZC*nx*ny sites earlier, not a whole slice earlier -> L2 hits
-    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+__device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
+                                        const Geom& g, int x, int y, int z, int t, const T* __restrict__ v_hi,
+                                        const T* __restrict__ w_lo) {
     const int64_t F = g.F;
-    const int nts = t_end - t_begin;
-    if (idx >= int64_t(nts) * F) return;
-    const int x = static_cast<int>(idx % g.nx);
-    int64_t r = idx / g.nx;
-    const int y = static_cast<int>(r % g.ny);
-    r /= g.ny;
-    const int zl = static_cast<int>(r % ZC);
-    r /= ZC;
-    const int t = t_begin + static_cast<int>(r % nts);
-    const int z = static_cast<int>(r / nts) * ZC + zl;
     const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
-
     T acc[6];
     // forward terms, mu = 0..3, summed left to right (add_su3_vector chain)
 #pragma unroll
@@ -89,6 +77,26 @@ __device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* 
     for (int k = 0; k < 6; ++k) out[(int64_t(t) * 6 + k) * F + s3] = acc[k];
 }
 
+template <typename T, bool FUSED>
+__device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
+                                              const Geom& g, int t_begin, int t_end, const T* __restrict__ v_hi,
+                                              const T* __restrict__ w_lo, int ZC) {
+    // visiting order (z-chunk of ZC planes, t, z, y, x): the t-1 slice a site reads (U_t, v)
+    // was streamed ZC*nx*ny sites earlier, not a whole slice earlier -> L2 hits
+    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int nts = t_end - t_begin;
+    if (idx >= int64_t(nts) * g.F) return;
+    const int x = static_cast<int>(idx % g.nx);
+    int64_t r = idx / g.nx;
+    const int y = static_cast<int>(r % g.ny);
+    r /= g.ny;
+    const int zl = static_cast<int>(r % ZC);
+    r /= ZC;
+    const int t = t_begin + static_cast<int>(r % nts);
+    const int z = static_cast<int>(r / nts) * ZC + zl;
+    nn_site<T, FUSED>(U, v, out, g, x, y, z, t, v_hi, w_lo);
+}
+
 // plain bounds: ptxas picks 64-98 registers; an explicit minBlocks of 1 would let it take 252
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256)
@@ -103,6 +111,32 @@ __global__ void __launch_bounds__(256, MINB)
     k_nn_sweep_capped(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin,
                       int t_end, const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC) {
     nn_sweep_body<T, FUSED>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+}
+
+// ---------------------------------------------------------------------------
+// even/odd dslash: the NN operator evaluated only on the sites of one
+// parity, (x+y+z+t) % 2 == parity, which read v only on the other parity.  Fused in one
+// kernel: forward U_mu(x) v(x+mu), backward U_mu(x-mu)^dag v(x-mu) (the adj_4dir products of
+// the neighbours), the add chain and sub_four -- the NN sweep's association, so the result
+// equals the full sweep's on those sites bit for bit.  Sites of the other parity in `out`
+// are not touched.  One thread per output site, (z-chunk, t, z, y, x/2) order.
+// ---------------------------------------------------------------------------
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(256)
+    k_dslash(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int parity, int ZC) {
+    const int nxh = g.nx >> 1;
+    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (idx >= (g.F >> 1) * g.nt) return;
+    const int xh = static_cast<int>(idx % nxh);
+    int64_t r = idx / nxh;
+    const int y = static_cast<int>(r % g.ny);
+    r /= g.ny;
+    const int zl = static_cast<int>(r % ZC);
+    r /= ZC;
+    const int t = static_cast<int>(r % g.nt);
+    const int z = static_cast<int>(r / g.nt) * ZC + zl;
+    const int x = 2 * xh + ((y + z + t + parity) & 1);
+    nn_site<T, FUSED>(U, v, out, g, x, y, z, t, nullptr, nullptr);
 }
 
 template <typename T, bool FUSED>
@@ -532,6 +566,24 @@ static int nn_halo_w(const T* U, const T* v, T* w, int nx, int ny, int nz, int n
 }
 
 template <typename T>
+static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int parity, int mode,
+                  cudaStream_t st) {
+    if (int rc = check_geom("dslash", nx, ny, nz, nt)) return rc;
+    if ((nx | ny | nz | nt) & 1) return fail_invalid("dslash: every lattice extent must be even (checkerboard)");
+    if (parity != 0 && parity != 1) return fail_invalid("dslash: parity must be 0 (even) or 1 (odd)");
+    if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("dslash: mode must be SU3G_EXACT or SU3G_FMA");
+    if (!U || !v || !out) return fail_invalid("dslash: null pointer");
+    if (out == v) return fail_invalid("dslash: out must not alias v");
+    Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
+    const bool big_slice = double(g.F) * 72 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
+    const int ZC = big_slice ? chunk_planes(nz, 8) : nz;
+    const unsigned gs = static_cast<unsigned>(((g.F >> 1) * nt + 255) / 256);
+    if (mode == SU3G_FMA) k_dslash<T, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC);
+    else k_dslash<T, false><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC);
+    return check_launch("dslash");
+}
+
+template <typename T>
 static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, int mode, cudaStream_t st) {
     if (int rc = check_geom("link_product", nx, ny, nz, nt)) return rc;
     if (!U || !acc) return fail_invalid("link_product: null pointer");
@@ -623,7 +675,7 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_early_c") == 0) {
-        if (value != 0 && value != 1) return fail_invalid("set_option: link_early_c must be 0 or 1");
+        if (value < -1 || value > 1) return fail_invalid("set_option: link_early_c must be -1 (default), 0 or 1");
         g_link_early_c = static_cast<int>(value);
         return SU3G_OK;
     }
@@ -665,6 +717,14 @@ int su3g_link_product_f32(const float* U, float* acc, int32_t nx, int32_t ny, in
 int su3g_link_product_f64(const double* U, double* acc, int32_t nx, int32_t ny, int32_t nz, int32_t nt, double s,
                           int32_t mode, su3g_stream_t st) {
     return link_product<double>(U, acc, nx, ny, nz, nt, s, mode, reinterpret_cast<cudaStream_t>(st));
+}
+int su3g_dslash_f32(const float* U, const float* v, float* out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                    int32_t parity, int32_t mode, su3g_stream_t st) {
+    return dslash<float>(U, v, out, nx, ny, nz, nt, parity, mode, reinterpret_cast<cudaStream_t>(st));
+}
+int su3g_dslash_f64(const double* U, const double* v, double* out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                    int32_t parity, int32_t mode, su3g_stream_t st) {
+    return dslash<double>(U, v, out, nx, ny, nz, nt, parity, mode, reinterpret_cast<cudaStream_t>(st));
 }
 
 }  // extern "C"

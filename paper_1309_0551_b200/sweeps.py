@@ -6,6 +6,8 @@
                     the reference routines in the order of SURVEY.md 8(c).
 * ``nn_apply``      v <- D v repeated (configs[4]: 10 applications).
 * ``link_product``  acc = sum_planes s U_mu U_nu(x+mu) U_mu(x+nu)^dag (a14).
+* ``dslash``        the NN operator on one parity only (even/odd checkerboard,
+                    SURVEY.md 8(f) f3), fused in one kernel.
 
 The reference has no sweep routine; these are built from its
 per-site routines' arithmetic.  ``*_aos`` helpers take/return the reference
@@ -81,6 +83,29 @@ def nn_apply(U: Field, v: Field, applications: int, scratch: Field | None = None
     return a
 
 
+def dslash(U: Field, v: Field, parity: int, out: Field | None = None, mode: str = "exact") -> Field:
+    """out(x) = (D v)(x) on the sites with (x+y+z+t) % 2 == parity; reads v only on the other parity.
+
+    Sites of the other parity keep their value in a caller-supplied ``out`` (a
+    fresh ``out`` is zero there).  Every lattice extent must be even.  EXACT mode
+    equals ``nn_sweep`` on those sites bit for bit.
+    """
+    if U.kind != "mat4" or v.kind != "vec":
+        raise ValueError("dslash needs U of kind 'mat4' and v of kind 'vec'")
+    if U.lattice != v.lattice or U.dtype != v.dtype:
+        raise ValueError("U and v must share lattice and dtype")
+    if parity not in (0, 1):
+        raise ValueError("parity must be 0 (even) or 1 (odd)")
+    if out is None:
+        out = Field(v.lattice, "vec", v.dtype, v.device, data=torch.zeros_like(v.data))
+    lat = U.lattice
+    _lib.call(
+        f"su3g_dslash_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
+        lat.nx, lat.ny, lat.nz, lat.nt, int(parity), _mode(mode), _stream(U.device),
+    )
+    return out
+
+
 def link_product(U: Field, s: float = 1.0 / 6.0, mode: str = "exact", out: Field | None = None) -> Field:
     if U.kind != "mat4":
         raise ValueError("link_product needs U of kind 'mat4'")
@@ -124,3 +149,11 @@ def link_product_aos(U, dims, s: float = 1.0 / 6.0, mode: str = "exact"):
     lat = Lattice4D.from_dims(dims)
     Uf = Field.from_aos(lat, "mat4", U)
     return _back(link_product(Uf, s, mode).to_aos(), U)
+
+
+def dslash_aos(U, v, dims, parity: int, mode: str = "exact"):
+    """Reference-layout dslash: (V,3,2) result, D v on the parity sites and 0 elsewhere."""
+    lat = Lattice4D.from_dims(dims)
+    Uf = Field.from_aos(lat, "mat4", U)
+    vf = Field.from_aos(lat, "vec", v)
+    return _back(dslash(Uf, vf, parity, mode=mode).to_aos(), v)

@@ -132,6 +132,24 @@ def ref_nn_sweep(U, v, dims):
     return simd.batch_apply("sub_four_su3_vecs", [F.copy(), bw[0], bw[1], bw[2], bw[3]])
 
 
+def ref_dslash(U, v, dims, parity):
+    """Even/odd dslash composed from su3bench routines as SURVEY.md 8(f) f3 states it: forward
+    mat_vec x4, backward = adj_4dir evaluated on every site then gathered from x - mu, the
+    add_su3_vector chain, sub_four_su3_vecs; kept on the sites of one parity, 0 elsewhere."""
+    fw = [simd.batch_apply("mult_su3_mat_vec", [np.ascontiguousarray(U[:, mu]), _roll(v, dims, mu, 1)]) for mu in range(4)]
+    W = simd.batch_apply("mult_adj_su3_mat_vec_4dir", [U, v])
+    bw = [_roll(np.ascontiguousarray(W[:, mu]), dims, mu, -1) for mu in range(4)]
+    F = simd.batch_apply("add_su3_vector", [fw[0], fw[1]])
+    F = simd.batch_apply("add_su3_vector", [F, fw[2]])
+    F = simd.batch_apply("add_su3_vector", [F, fw[3]])
+    full = simd.batch_apply("sub_four_su3_vecs", [F.copy(), bw[0], bw[1], bw[2], bw[3]])
+    lat = lattice.Lattice4D.from_dims(dims)
+    par = np.array([sum(lat.site_coord(s)) % 2 for s in range(lat.volume)])  # lattice.py:129
+    out = np.zeros_like(full)
+    out[par == parity] = full[par == parity]
+    return out
+
+
 def ref_link_product(U, dims, s):
     dt = U.dtype
     acc = np.zeros((U.shape[0], 3, 3, 2), dtype=dt)
@@ -181,6 +199,19 @@ def sweeps_fixture():
             out[f"{tag}/{prec}/iv"] = iv
             out[f"{tag}/{prec}/inn"] = ref_nn_sweep(iU, iv, dims)
             out[f"{tag}/{prec}/ilink"] = ref_link_product(iU, dims, 0.5)
+    # even/odd dslash on even-extent lattices
+    for dims in ((4, 4, 4, 4), (2, 4, 6, 2), (6, 2, 4, 8)):
+        tag = "x".join(map(str, dims))
+        V = int(np.prod(dims))
+        for prec in PREC:
+            dt = types.dtype_for(prec)
+            rng = inputs.config_rng(500 + V + dt.itemsize)
+            U = inputs.random_links(rng, V, 4, dtype=dt)
+            v = inputs.random_vectors(rng, V, None, dtype=dt)
+            out[f"dslash/{tag}/{prec}/U"] = U
+            out[f"dslash/{tag}/{prec}/v"] = v
+            for parity in (0, 1):
+                out[f"dslash/{tag}/{prec}/p{parity}"] = ref_dslash(U, v, dims, parity)
     return out
 
 

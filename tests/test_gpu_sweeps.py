@@ -347,3 +347,79 @@ def test_nn_tma_block_sizes(threads, dims):
     finally:
         _lib.set_option("nn_tma_threads", 0)
         _lib.set_option("nn_variant", 0)
+
+
+# ---- even/odd dslash ----------------------------------------------
+
+DSLASH_DIMS = {"4x4x4x4": (4, 4, 4, 4), "2x4x6x2": (2, 4, 6, 2), "6x2x4x8": (6, 2, 4, 8)}
+
+
+@pytest.mark.parametrize("parity", [0, 1])
+@pytest.mark.parametrize("tag", sorted(DSLASH_DIMS))
+def test_dslash_golden_bitwise(golden_sweeps, tag, precision, parity):
+    g = golden_sweeps
+    U, v = g[f"dslash/{tag}/{precision}/U"], g[f"dslash/{tag}/{precision}/v"]
+    got = sweeps.dslash_aos(U, v, DSLASH_DIMS[tag], parity)
+    assert np.array_equal(got, g[f"dslash/{tag}/{precision}/p{parity}"])
+
+
+@pytest.mark.parametrize("dims", [(16, 16, 16, 16), (32, 8, 4, 6), (64, 64, 16, 2)])
+def test_dslash_vs_c_oracle(dims, precision):
+    from oracle import sweeps as OS
+
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(6000 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    full = coracle.nn_sweep(U, v, dims)
+    even = OS.parity_mask(dims)
+    for parity, keep in ((0, even), (1, ~even)):
+        got = sweeps.dslash_aos(U, v, dims, parity)
+        assert np.array_equal(got[keep], full[keep])
+        assert not np.any(got[~keep])
+        tol = 1e-5 if dt == np.float32 else 1e-12
+        assert floored_rel_err(sweeps.dslash_aos(U, v, dims, parity, mode="fma")[keep], full[keep]) <= tol
+
+
+def test_dslash_leaves_other_parity_untouched_and_composes(precision):
+    """out keeps its other-parity values; D_eo D_oe on an even source equals two full sweeps on even sites."""
+    from oracle import sweeps as OS
+
+    dt = _dt(precision)
+    dims = (8, 4, 6, 4)
+    lat = Lattice4D(*dims)
+    V = lat.volume
+    rng = inputs.config_rng(61)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    even = OS.parity_mask(dims)
+    Uf = Field.from_aos(lat, "mat4", U)
+    out = Field.from_aos(lat, "vec", np.full((V, 3, 2), 7.0, dtype=dt))
+    sweeps.dslash(Uf, Field.from_aos(lat, "vec", v), 0, out=out)
+    got = out.numpy()
+    assert np.all(got[~even] == 7.0)
+    assert np.array_equal(got[even], coracle.nn_sweep(U, v, dims)[even])
+    ve = np.where(even[:, None, None], v, 0).astype(dt)
+    w = sweeps.dslash(Uf, Field.from_aos(lat, "vec", ve), 1)
+    y = sweeps.dslash(Uf, w, 0).numpy()
+    want = coracle.nn_sweep(U, coracle.nn_sweep(U, ve, dims), dims)
+    assert np.array_equal(y[even], want[even])
+
+
+def test_dslash_argument_errors():
+    from paper_1309_0551_b200 import _lib
+
+    lat = Lattice4D(4, 4, 4, 3)
+    U = Field(lat, "mat4", torch.float32, torch.device("cuda"))
+    v = Field(lat, "vec", torch.float32, torch.device("cuda"))
+    with pytest.raises(ValueError, match="even"):
+        sweeps.dslash(U, v, 0)
+    lat = Lattice4D(4, 4, 4, 4)
+    U = Field(lat, "mat4", torch.float32, torch.device("cuda"))
+    v = Field(lat, "vec", torch.float32, torch.device("cuda"))
+    with pytest.raises(ValueError, match="parity"):
+        sweeps.dslash(U, v, 2)
+    with pytest.raises(ValueError, match="alias"):
+        sweeps.dslash(U, v, 0, out=v)
+    assert _lib.load().su3g_dslash_f32(None, None, None, 4, 4, 4, 4, 0, 0, None) == _lib.SU3G_EINVAL
