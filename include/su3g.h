@@ -16,8 +16,9 @@
  *     enqueue.  No allocation, no host synchronisation.
  *   - Arithmetic follows the reference association (separated sums, combine
  *     once, no FMA; scalar.py:8-14), so results are bit-identical to su3bench.
- *   - Return value: 0 = ok, <0 = invalid argument (SU3G_EINVAL), >0 = a
- *     cudaError_t.  su3g_last_error() returns the calling thread's message.
+ *   - Return value: 0 = ok, SU3G_EINVAL = invalid argument, SU3G_ENCCL = an
+ *     NCCL failure, >0 = a cudaError_t.  su3g_last_error() returns the calling
+ *     thread's message.
  *   - Result storage must not alias an input (the reference's contract,
  *     validation.py:25-34); it is the caller's responsibility, as there.
  */
@@ -40,6 +41,7 @@ typedef struct CUstream_st *su3g_stream_t; /* == cudaStream_t */
 
 #define SU3G_OK 0
 #define SU3G_EINVAL (-1)
+#define SU3G_ENCCL (-2) /* an NCCL call failed (message in su3g_last_error) */
 
 #define SU3G_ABI_VERSION 1
 
@@ -206,6 +208,29 @@ SU3G_API int su3g_dslash_f32(const float *U, const float *v, float *out, int32_t
                              int32_t parity, int32_t mode, su3g_stream_t stream);
 SU3G_API int su3g_dslash_f64(const double *U, const double *v, double *out, int32_t nx, int32_t ny, int32_t nz,
                              int32_t nt, int32_t parity, int32_t mode, su3g_stream_t stream);
+
+/* ---- t-slab multi-GPU NN sweep over NCCL (BASELINE configs[4]) ----
+ * One process (or thread) per GPU.  Rank r of G holds the t-slices
+ * [r*nt_local, (r+1)*nt_local) of the global lattice; U, v, out are its slab in the
+ * t-sliced SoA layout of su3g_nn_sweep.  su3g_slab_nn_sweep computes out = D v on the
+ * slab, exchanging the two one-site halos with ranks r-1 and r+1 (v on the first local
+ * slice, w = U_t^dag v on the last) over NCCL on the communicator's own stream while the
+ * interior slices run on `stream`; bit-identical to the unsharded periodic sweep.  A
+ * one-rank communicator exchanges with itself (periodic in t).
+ * NCCL is loaded at su3g_comm_init (dlopen "libnccl.so.2" or $SU3G_NCCL_LIB).
+ * The unique id (SU3G_COMM_ID_BYTES bytes, an ncclUniqueId) is created by one rank with
+ * su3g_comm_unique_id and distributed by the host program.  su3g_comm_init is collective
+ * and must be called with the rank's device current. */
+#define SU3G_COMM_ID_BYTES 128
+typedef struct su3g_comm *su3g_comm_t;
+SU3G_API int su3g_comm_unique_id(void *id_out);
+SU3G_API int su3g_comm_init(int32_t nranks, int32_t rank, const void *id, su3g_comm_t *comm);
+SU3G_API int su3g_comm_destroy(su3g_comm_t comm);
+SU3G_API int su3g_comm_rank(su3g_comm_t comm, int32_t *rank, int32_t *nranks);
+SU3G_API int su3g_slab_nn_sweep_f32(su3g_comm_t comm, const float *U, const float *v, float *out, int32_t nx,
+                                    int32_t ny, int32_t nz, int32_t nt_local, int32_t mode, su3g_stream_t stream);
+SU3G_API int su3g_slab_nn_sweep_f64(su3g_comm_t comm, const double *U, const double *v, double *out, int32_t nx,
+                                    int32_t ny, int32_t nz, int32_t nt_local, int32_t mode, su3g_stream_t stream);
 
 /* ---- link-product sweep (BASELINE configs[3]) ------------------------------
  * acc(x) = sum over (mu,nu) in (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) of

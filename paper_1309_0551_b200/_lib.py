@@ -17,6 +17,8 @@ HEADER_PATH = os.path.join(os.path.dirname(HERE), "include", "su3g.h")
 
 SU3G_OK = 0
 SU3G_EINVAL = -1
+SU3G_ENCCL = -2
+SU3G_COMM_ID_BYTES = 128
 SU3G_EXACT = 0
 SU3G_FMA = 1
 
@@ -50,6 +52,10 @@ def _signatures():
         "su3g_device_sm_count": ([], ctypes.c_int),
         "su3g_device_l2_bytes": ([], ctypes.c_int64),
         "su3g_set_option": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
+        "su3g_comm_unique_id": ([_vp], ctypes.c_int),
+        "su3g_comm_init": ([_i32, _i32, _vp, _vp], ctypes.c_int),
+        "su3g_comm_destroy": ([_vp], ctypes.c_int),
+        "su3g_comm_rank": ([_vp, _vp, _vp], ctypes.c_int),
     }
     for sfx, real in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
         for r in HOT_ROUTINES + EXTRA_AB_ROUTINES:
@@ -63,6 +69,7 @@ def _signatures():
         sig[f"su3g_soa_to_aos_{sfx}"] = ([_vp, _vp, _i64, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_halo_w_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
+        sig[f"su3g_slab_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_dslash_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_link_product_{sfx}"] = ([_vp, _vp, _i32, _i32, _i32, _i32, real, _i32, _vp], ctypes.c_int)
     return sig

@@ -262,3 +262,19 @@ def test_device_sitebuffer_rejects_bad_alignment():
 
     with pytest.raises(ValueError, match="power of two"):
         DeviceSiteBuffer(lattice.Lattice4D(2, 2, 2, 2), {"a": "vec"}, alignment=12)
+
+
+def test_comm_abi_without_a_gpu():
+    """Unique ids come from NCCL without a device; bad arguments are rejected before any CUDA call."""
+    from paper_1309_0551_b200.comm import NativeComm
+
+    lib = _lib.load()
+    uid = NativeComm.unique_id()
+    assert len(uid) == _lib.SU3G_COMM_ID_BYTES and any(uid)
+    h = ctypes.c_void_p()
+    assert lib.su3g_comm_init(2, 2, uid, ctypes.byref(h)) == _lib.SU3G_EINVAL
+    assert lib.su3g_comm_init(1, 0, None, ctypes.byref(h)) == _lib.SU3G_EINVAL
+    assert lib.su3g_comm_destroy(None) == _lib.SU3G_OK
+    assert lib.su3g_slab_nn_sweep_f32(None, None, None, None, 4, 4, 4, 4, 0, None) == _lib.SU3G_EINVAL
+    with pytest.raises(ValueError, match="128"):
+        NativeComm(1, 0, b"short")
