@@ -44,8 +44,8 @@ def test_one_rank_native_slab_equals_periodic_sweep(comm, dims, dtype):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_one_rank_native_slab_ten_applications(comm, dtype):
     U, v = _fields((32, 16, 8, 6), dtype, 71)
+    v2 = Field(v.lattice, "vec", v.dtype, v.device, data=v.data.clone())  # nn_apply ping-pongs through v
     want = sweeps.nn_apply(U, v, 10).numpy()
-    v2 = Field(v.lattice, "vec", v.dtype, v.device, data=v.data.clone())
     got = native_slab_apply(comm, U, v2, 10).numpy()
     assert np.array_equal(got, want)
 
