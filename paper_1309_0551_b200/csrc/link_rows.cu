@@ -48,10 +48,13 @@ __device__ __forceinline__ void dot3(PF p, QF q, T& re, T& im) {
 
 }  // namespace
 
-template <typename T, bool FUSED, int MINB, bool EARLY_C>
+template <typename T, bool FUSED, int MINB, bool EARLY_C, bool SMEM_A>
 __global__ void __launch_bounds__(128, MINB)
     k_link_rows(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC) {
     __shared__ T sacc[18 * 128];
+    // SMEM_A: A = U_mu(x) is gathered once per mu group (planes 0-2, 3-4, 5) into this thread's
+    // column of sA instead of once per plane from L2
+    __shared__ T sA[SMEM_A ? 18 * 128 : 1];
     const int tid = threadIdx.x;
     const int64_t idx = blockIdx.x * int64_t(blockDim.x) + tid;
     if (idx >= g.F * g.nt) return;  // no block-level sync below: early exit is safe
@@ -71,6 +74,14 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll 1
     for (int pl = 0; pl < 6; ++pl) {
         const int mu = c_plane_mu[pl], nu = c_plane_nu[pl];
+        if constexpr (SMEM_A) {
+            if (pl == 0 || pl == 3 || pl == 5) {
+                T a[18];
+                ld_link_part<T, 18>(U, g, site, mu, 0, a);
+#pragma unroll
+                for (int k = 0; k < 18; ++k) sA[k * 128 + tid] = a[k];
+            }
+        }
         T tm[18], c[18];
         // EARLY_C: gather C with B (both in flight together, +18 live reals); else after T is built
         if constexpr (EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);
@@ -80,7 +91,12 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 T a[6];
-                ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
+                if constexpr (SMEM_A) {
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) a[k] = sA[(6 * i + k) * 128 + tid];
+                } else {
+                    ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
+                }
 #pragma unroll
                 for (int k = 0; k < 3; ++k)  // t[i][k] = sum_j a[i][j] b[j][k]   (mat_nn)
                     dot3<T, FUSED, PLAIN>([&](int j, int q) { return a[2 * j + q]; },
@@ -112,15 +128,16 @@ __global__ void __launch_bounds__(128, MINB)
 
 int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
 int g_link_early_c = -1;  // su3g_set_option("link_early_c"): gather C together with B (-1 = default)
+int g_link_smem_a = 0;    // su3g_set_option("link_smem_a"): keep A = U_mu(x) in smem per mu group
 
-template <typename T, bool FUSED, bool EARLY_C>
+template <typename T, bool FUSED, bool EARLY_C, bool SMEM_A>
 static void launch_rows_minb(const T* U, T* acc, const Geom& g, T s, int ZC, unsigned grid, int minb, cudaStream_t st) {
     switch (minb) {
-        case 3: k_link_rows<T, FUSED, 3, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        case 5: k_link_rows<T, FUSED, 5, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        case 6: k_link_rows<T, FUSED, 6, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        case 8: k_link_rows<T, FUSED, 8, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        default: k_link_rows<T, FUSED, 4, EARLY_C><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 3: k_link_rows<T, FUSED, 3, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 5: k_link_rows<T, FUSED, 5, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 6: k_link_rows<T, FUSED, 6, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 8: k_link_rows<T, FUSED, 8, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        default: k_link_rows<T, FUSED, 4, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
     }
 }
 
@@ -132,8 +149,13 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     // f64 FMA minb 3 (0.474 vs 0.467 at 4), f32 minb 6 with early C (0.310 vs 0.299)
     const int minb = g_link_minb ? g_link_minb : (sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6);
     const bool early_c = g_link_early_c >= 0 ? g_link_early_c != 0 : sizeof(T) == 4;
-    if (early_c) launch_rows_minb<T, FUSED, true>(U, acc, g, s, ZC, grid, minb, st);
-    else launch_rows_minb<T, FUSED, false>(U, acc, g, s, ZC, grid, minb, st);
+    if (g_link_smem_a) {
+        if (early_c) launch_rows_minb<T, FUSED, true, true>(U, acc, g, s, ZC, grid, minb, st);
+        else launch_rows_minb<T, FUSED, false, true>(U, acc, g, s, ZC, grid, minb, st);
+    } else {
+        if (early_c) launch_rows_minb<T, FUSED, true, false>(U, acc, g, s, ZC, grid, minb, st);
+        else launch_rows_minb<T, FUSED, false, false>(U, acc, g, s, ZC, grid, minb, st);
+    }
     return check_launch("link_product(rows)");
 }
 

@@ -19,7 +19,9 @@ namespace su3g {
 void set_sm_reserve(int n);
 extern int g_tma_threads;
 extern int g_link_minb;
+int g_link_zc = 0;  // su3g_set_option("link_zc"): z-planes per visiting chunk of the link kernels (0 = auto)
 extern int g_link_early_c;
+extern int g_link_smem_a;
 
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
@@ -626,6 +628,7 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     const bool big_slice = double(g.F) * 72 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
     int ZC = big_slice ? chunk_planes(nz, 8) : nz;
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
+    if (g_link_zc > 0) ZC = chunk_planes(nz, g_link_zc);  // A/B knob: z-planes per chunk
     // default (auto) = the low-register rows kernel: 16 warps/SM instead of 8 for f64
     // (48^4 f64, same box: exact 0.323 -> 0.426 of HBM, FMA 0.406 -> 0.465)
     if (lv == 0 || lv == 6) {
@@ -672,6 +675,16 @@ int su3g_set_option(const char* name, int64_t value) {
         if (value != 0 && value != 3 && value != 4 && value != 5 && value != 6 && value != 8)
             return fail_invalid("set_option: link_minb must be 0 (default), 3, 4, 5, 6 or 8");
         g_link_minb = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "link_smem_a") == 0) {
+        if (value != 0 && value != 1) return fail_invalid("set_option: link_smem_a must be 0 or 1");
+        g_link_smem_a = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "link_zc") == 0) {
+        if (value < 0 || value > 4096) return fail_invalid("set_option: link_zc must be in [0, 4096]");
+        g_link_zc = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_early_c") == 0) {
