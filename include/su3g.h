@@ -65,7 +65,8 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *                   3 FMA; f32: 6), 3, 4, 5, 6 or 8
  *   "link_smem_a":  1 = the rows kernel keeps U_mu(x) in shared memory per mu group (A/B)
  *   "link_zc":      z-planes per visiting chunk of the link kernels (largest divisor of nz <= value;
- *                   0 = auto: 8 when a t-slice of links exceeds half of L2, else nz)
+ *                   0 = auto: 16 when a t-slice of links exceeds half of L2, else nz)
+ *   "sweep_zc":     the same for the one-thread-per-site NN sweep and dslash kernels (auto: 8)
  *   "link_early_c": 1 = the rows kernel gathers U_mu(x+nu) together with U_nu(x+mu), 0 = after
  *                   T = A B is built, -1 = default (1 for f32, 0 for f64)
  *   "sm_reserve":   SMs the persistent sweep kernels leave free for concurrent kernels

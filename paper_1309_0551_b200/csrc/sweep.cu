@@ -19,7 +19,8 @@ namespace su3g {
 void set_sm_reserve(int n);
 extern int g_tma_threads;
 extern int g_link_minb;
-int g_link_zc = 0;  // su3g_set_option("link_zc"): z-planes per visiting chunk of the link kernels (0 = auto)
+int g_link_zc = 0;   // su3g_set_option("link_zc"): z-planes per visiting chunk of the link kernels (0 = auto)
+int g_sweep_zc = 0;  // su3g_set_option("sweep_zc"): z-planes per chunk of the generic NN / dslash kernels
 extern int g_link_early_c;
 extern int g_link_smem_a;
 
@@ -544,7 +545,8 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     // z-chunked order only pays when one t-slice of operands does not fit comfortably in L2
     // (measured: 64^3 f64 0.64 -> 0.70 of HBM; 32^4 f64, whose slice is 22 MB, slightly prefers t-major)
     const bool big_slice = double(g.F) * 84 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
-    const int ZC = (variant == 4 || !big_slice) ? nz : chunk_planes(nz, 8);  // 4: t-major order (A/B knob)
+    int ZC = (variant == 4 || !big_slice) ? nz : chunk_planes(nz, 8);  // 4: t-major order (A/B knob)
+    if (g_sweep_zc > 0) ZC = chunk_planes(nz, g_sweep_zc);
     if (variant == 6) {  // occupancy A/B knob: register cap for 3 CTAs (24 warps) per SM
         if (mode == SU3G_FMA) k_nn_sweep_capped<T, true, 3><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
         else k_nn_sweep_capped<T, false, 3><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
@@ -578,7 +580,8 @@ static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (out == v) return fail_invalid("dslash: out must not alias v");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const bool big_slice = double(g.F) * 72 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
-    const int ZC = big_slice ? chunk_planes(nz, 8) : nz;
+    int ZC = big_slice ? chunk_planes(nz, 8) : nz;
+    if (g_sweep_zc > 0) ZC = chunk_planes(nz, g_sweep_zc);
     const unsigned gs = static_cast<unsigned>(((g.F >> 1) * nt + 255) / 256);
     if (mode == SU3G_FMA) k_dslash<T, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC);
     else k_dslash<T, false><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC);
@@ -626,7 +629,9 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     const int64_t n = g.F * nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
     const bool big_slice = double(g.F) * 72 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
-    int ZC = big_slice ? chunk_planes(nz, 8) : nz;
+    // z-planes per chunk: 16 measured best for the rows kernel at 48^4 f64 (exact 0.42 -> 0.455,
+    // FMA 0.475 -> 0.506 vs 8; 2, 4, 12, 48 also swept)
+    int ZC = big_slice ? chunk_planes(nz, 16) : nz;
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
     if (g_link_zc > 0) ZC = chunk_planes(nz, g_link_zc);  // A/B knob: z-planes per chunk
     // default (auto) = the low-register rows kernel: 16 warps/SM instead of 8 for f64
@@ -675,6 +680,11 @@ int su3g_set_option(const char* name, int64_t value) {
         if (value != 0 && value != 3 && value != 4 && value != 5 && value != 6 && value != 8)
             return fail_invalid("set_option: link_minb must be 0 (default), 3, 4, 5, 6 or 8");
         g_link_minb = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "sweep_zc") == 0) {
+        if (value < 0 || value > 4096) return fail_invalid("set_option: sweep_zc must be in [0, 4096]");
+        g_sweep_zc = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_smem_a") == 0) {
