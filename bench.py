@@ -72,6 +72,9 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sites", type=int, default=64**4, help="sites for routine:<name> workloads")
+    p.add_argument("--dims", default=None,
+                   help="experiments only: override the lattice nx,ny,nz,nt of nn-*/dslash/link workloads "
+                        "(for nn-weak, nt is per GPU)")
     args = p.parse_args(argv)
     if args.warmup < 3:
         p.error("--warmup must be >= 3")
@@ -87,6 +90,17 @@ def parse_args(argv=None):
 # ----------------------------------------------------------------------------
 
 def workload_config(args, world):
+    cfg = _workload_config(args, world)
+    if args.dims and cfg["kind"] in ("nn", "dslash", "link"):
+        d = tuple(int(x) for x in args.dims.split(","))
+        if len(d) != 4:
+            raise SystemExit("--dims needs nx,ny,nz,nt")
+        cfg["global_dims"] = d[:3] + (d[3] * (world if args.workload == "nn-weak" else 1),)
+        cfg["name"] += f" [dims override {d}]"
+    return cfg
+
+
+def _workload_config(args, world):
     w = args.workload
     if w == "nn-weak":
         return dict(kind="nn", global_dims=(64, 64, 64, 16 * world), apps=args.applications,

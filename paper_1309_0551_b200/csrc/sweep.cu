@@ -628,10 +628,11 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     }
     const int64_t n = g.F * nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
-    const bool big_slice = double(g.F) * 72 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
-    // z-planes per chunk: 16 measured best for the rows kernel at 48^4 f64 (exact 0.42 -> 0.455,
-    // FMA 0.475 -> 0.506 vs 8; 2, 4, 12, 48 also swept)
-    int ZC = big_slice ? chunk_planes(nz, 16) : nz;
+    // z-planes per chunk: 16 measured best for the rows kernel at 48^4 f64 (exact 0.427 -> 0.455,
+    // FMA 0.475 -> 0.506 against the unchunked order; 2, 4, 12 also swept).  Chunk once a t-slice of
+    // links is more than 1/8 of L2 (48^3 f64 = 64 MB, about half of L2, was left unchunked before).
+    const bool link_chunk = double(g.F) * 72 * sizeof(T) > 0.125 * double(device_info().l2_bytes);
+    int ZC = link_chunk ? chunk_planes(nz, 16) : nz;
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
     if (g_link_zc > 0) ZC = chunk_planes(nz, g_link_zc);  // A/B knob: z-planes per chunk
     // default (auto) = the low-register rows kernel: 16 warps/SM instead of 8 for f64
