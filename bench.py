@@ -267,7 +267,7 @@ def run_b200(args, rank, world, local):
                      ("SU3G_NN_TMA_THREADS", "nn_tma_threads"), ("SU3G_LINK_VARIANT", "link_variant"),
                      ("SU3G_LINK_MINB", "link_minb"), ("SU3G_LINK_EARLY_C", "link_early_c"),
                      ("SU3G_LINK_ZC", "link_zc"), ("SU3G_LINK_SMEM_A", "link_smem_a"),
-                     ("SU3G_SWEEP_ZC", "sweep_zc")):
+                     ("SU3G_SWEEP_ZC", "sweep_zc"), ("SU3G_SWEEP_PREFETCH", "sweep_prefetch")):
         if os.environ.get(env):
             _l.set_option(opt, int(os.environ[env]))
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
@@ -421,6 +421,9 @@ def run_b200(args, rank, world, local):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
+    dispatched = _l.last_kernel()  # the kernel the last launch of a step dispatched to
+    if cfg["kind"] == "nn" and world > 1:
+        dispatched = "interior: " + _interior_kernel(sweeps, U, va, vb, lat.nt, args.mode)
     clocks = ClockSampler(local)
     barrier(world, dev)
     torch.cuda.synchronize(dev)
@@ -474,8 +477,7 @@ def run_b200(args, rank, world, local):
         "hbm_gbs": achieved,
         "roofline": {
             "bound": "hbm",
-            "kernel": {"nn": "k_nn_tma (f32) / k_nn_sweep (f64)", "link": "k_link_rows",
-                       "dslash": "k_dslash"}.get(cfg["kind"], "k_stream"),
+            "kernel": dispatched,
             "achieved": achieved,
             "peak": peak,
             "peak_source": peak_src,
@@ -513,6 +515,19 @@ class _EventTimer:
         self.e1.record(self.stream)
         self.sink.append((self.e0, self.e1))
         return False
+
+
+def _interior_kernel(sweeps, U, va, vb, nt, mode) -> str:
+    """Name of the kernel the interior slices of a t-slab dispatch to (the dominant launch at N > 1)."""
+    import torch
+
+    from paper_1309_0551_b200 import _lib
+
+    if nt <= 2:
+        return "none (every slice is a boundary slice)"
+    sweeps.nn_sweep(U, va, out=vb, t_range=(1, nt - 1), mode=mode)
+    torch.cuda.synchronize()
+    return _lib.last_kernel()
 
 
 def measure_e2e(args, cfg, rank, world, dev, tdt, stream):

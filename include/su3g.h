@@ -51,6 +51,9 @@ typedef struct CUstream_st *su3g_stream_t; /* == cudaStream_t */
 
 SU3G_API int su3g_abi_version(void);
 SU3G_API const char *su3g_last_error(void);
+/* name (and geometry) of the kernel the calling thread's last launch dispatched to, e.g.
+ * "k_nn_tma<f32,64x2x2,256thr>" -- the sweeps choose among several kernels at run time */
+SU3G_API const char *su3g_last_kernel(void);
 /* number of SMs / L2 bytes of the current device (0 on failure) */
 SU3G_API int su3g_device_sm_count(void);
 SU3G_API int64_t su3g_device_l2_bytes(void);
@@ -67,6 +70,9 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "link_zc":      z-planes per visiting chunk of the link kernels (largest divisor of nz <= value;
  *                   0 = auto: 16 when a t-slice of links exceeds half of L2, else nz)
  *   "sweep_zc":     the same for the one-thread-per-site NN sweep and dslash kernels (auto: 8)
+ *   "sweep_prefetch": L2 prefetch distance of the one-thread-per-site kernels (generic NN, dslash,
+ *                   link rows) in quarter waves of CTAs: thread 0 issues cp.async.bulk.prefetch.L2
+ *                   for the sites of the CTA that far ahead (0 = off, max 16)
  *   "link_early_c": 1 = the rows kernel gathers U_mu(x+nu) together with U_nu(x+mu), 0 = after
  *                   T = A B is built, -1 = default (1 for f32, 0 for f64)
  *   "sm_reserve":   SMs the persistent sweep kernels leave free for concurrent kernels

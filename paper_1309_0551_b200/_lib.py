@@ -49,6 +49,7 @@ def _signatures():
     sig = {
         "su3g_abi_version": ([], ctypes.c_int),
         "su3g_last_error": ([], ctypes.c_char_p),
+        "su3g_last_kernel": ([], ctypes.c_char_p),
         "su3g_device_sm_count": ([], ctypes.c_int),
         "su3g_device_l2_bytes": ([], ctypes.c_int64),
         "su3g_set_option": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
@@ -115,6 +116,11 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def last_kernel() -> str:
+    """Kernel (with geometry) the calling thread's last libsu3g launch dispatched to."""
+    return load().su3g_last_kernel().decode(errors="replace")
 
 
 def set_option(name: str, value: int) -> None:

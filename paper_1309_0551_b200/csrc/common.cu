@@ -8,6 +8,9 @@
 namespace su3g {
 
 static thread_local std::string g_last_error;
+static thread_local std::string g_last_kernel;
+
+void note_kernel(const std::string& name) { g_last_kernel = name; }
 static std::atomic<int> g_sm_reserve{0};
 
 int sm_reserve() { return g_sm_reserve.load(); }
@@ -57,6 +60,8 @@ extern "C" {
 int su3g_abi_version(void) { return SU3G_ABI_VERSION; }
 
 const char* su3g_last_error(void) { return su3g::g_last_error.c_str(); }
+
+const char* su3g_last_kernel(void) { return su3g::g_last_kernel.c_str(); }
 
 int su3g_device_sm_count(void) { return su3g::device_info().num_sms; }
 

@@ -14,6 +14,8 @@
 // fit 16 warps/SM for f64.  Arithmetic per element is exactly link_site's --
 // mat_nn, then mat_na, then acc + s*P in plane order -- row by row, so EXACT
 // mode is bit-identical to the reference composition.
+#include <algorithm>
+
 #include "sweep_common.cuh"
 #include "su3_math.cuh"
 
@@ -50,7 +52,9 @@ __device__ __forceinline__ void dot3(PF p, QF q, T& re, T& im) {
 
 template <typename T, bool FUSED, int MINB, bool EARLY_C, bool SMEM_A>
 __global__ void __launch_bounds__(128, MINB)
-    k_link_rows(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC) {
+    k_link_rows(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC, int ahead) {
+    if (ahead > 0 && threadIdx.x == 0)  // L2 prefetch of the CTA one wave ahead (sweep_prefetch)
+        prefetch_cta_l2<T>(U, 72, g, blockIdx.x + int64_t(ahead), blockDim.x, 0, g.nt, ZC);
     __shared__ T sacc[18 * 128];
     // SMEM_A: A = U_mu(x) is gathered once per mu group (planes 0-2, 3-4, 5) into this thread's
     // column of sA instead of once per plane from L2
@@ -128,16 +132,18 @@ __global__ void __launch_bounds__(128, MINB)
 
 int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
 int g_link_early_c = -1;  // su3g_set_option("link_early_c"): gather C together with B (-1 = default)
-int g_link_smem_a = 0;    // su3g_set_option("link_smem_a"): keep A = U_mu(x) in smem per mu group
+int g_link_smem_a = 0;
+extern int g_sweep_prefetch;    // su3g_set_option("link_smem_a"): keep A = U_mu(x) in smem per mu group
 
 template <typename T, bool FUSED, bool EARLY_C, bool SMEM_A>
-static void launch_rows_minb(const T* U, T* acc, const Geom& g, T s, int ZC, unsigned grid, int minb, cudaStream_t st) {
+static void launch_rows_minb(const T* U, T* acc, const Geom& g, T s, int ZC, unsigned grid, int minb, int ahead,
+                             cudaStream_t st) {
     switch (minb) {
-        case 3: k_link_rows<T, FUSED, 3, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        case 5: k_link_rows<T, FUSED, 5, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        case 6: k_link_rows<T, FUSED, 6, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        case 8: k_link_rows<T, FUSED, 8, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-        default: k_link_rows<T, FUSED, 4, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 3: k_link_rows<T, FUSED, 3, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        case 5: k_link_rows<T, FUSED, 5, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        case 6: k_link_rows<T, FUSED, 6, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        case 8: k_link_rows<T, FUSED, 8, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        default: k_link_rows<T, FUSED, 4, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
     }
 }
 
@@ -149,12 +155,16 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     // f64 FMA minb 3 (0.474 vs 0.467 at 4), f32 minb 6 with early C (0.310 vs 0.299)
     const int minb = g_link_minb ? g_link_minb : (sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6);
     const bool early_c = g_link_early_c >= 0 ? g_link_early_c != 0 : sizeof(T) == 4;
+    // L2 prefetch one wave ahead (sweep_prefetch): resident CTAs per SM from the register target
+    const int ahead = (g_sweep_prefetch > 0 && (int64_t(g.nx) * g.ny) % 128 == 0 && aligned16(U))
+                          ? std::max(1, minb * device_info().num_sms * g_sweep_prefetch / 4)
+                          : 0;
     if (g_link_smem_a) {
-        if (early_c) launch_rows_minb<T, FUSED, true, true>(U, acc, g, s, ZC, grid, minb, st);
-        else launch_rows_minb<T, FUSED, false, true>(U, acc, g, s, ZC, grid, minb, st);
+        if (early_c) launch_rows_minb<T, FUSED, true, true>(U, acc, g, s, ZC, grid, minb, ahead, st);
+        else launch_rows_minb<T, FUSED, false, true>(U, acc, g, s, ZC, grid, minb, ahead, st);
     } else {
-        if (early_c) launch_rows_minb<T, FUSED, true, false>(U, acc, g, s, ZC, grid, minb, st);
-        else launch_rows_minb<T, FUSED, false, false>(U, acc, g, s, ZC, grid, minb, st);
+        if (early_c) launch_rows_minb<T, FUSED, true, false>(U, acc, g, s, ZC, grid, minb, ahead, st);
+        else launch_rows_minb<T, FUSED, false, false>(U, acc, g, s, ZC, grid, minb, ahead, st);
     }
     return check_launch("link_product(rows)");
 }

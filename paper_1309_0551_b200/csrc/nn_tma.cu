@@ -470,6 +470,9 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.has_vhi = v_hi != nullptr;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
     k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
+    note_kernel(std::string("k_nn_tma<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(nx) + "x" +
+                std::to_string(BY) + "x" + std::to_string(BZ) + (CNX ? "" : " runtime-geometry") + "," +
+                std::to_string(NTHR) + "thr>");
     return check_launch("nn_sweep(tma)");
 }
 

@@ -460,6 +460,7 @@ int launch_parts(const typename Op::T* a, const typename Op::T* b, Dest<typename
     int64_t grid = std::min<int64_t>(ntiles, int64_t(per_sm) * di.num_sms);
     if (grid < 1) grid = 1;
     k_stream_parts<Op><<<static_cast<unsigned>(grid), G::THREADS, G::SMEM, stream>>>(a, b, c, n);
+    note_kernel(std::string("k_stream_parts<") + Op::name + ">");
     return check_launch(Op::name);
 }
 
@@ -482,6 +483,7 @@ int launch(const typename Op::T* a, const typename Op::T* b, const typename Op::
     if (!aligned) {
         const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(di.num_sms) * 8);
         k_direct<Op><<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, b, s_site, s, c, n);
+        note_kernel(std::string("k_direct<") + Op::name + ">");
         return check_launch(Op::name);
     }
     if constexpr (HasParts<Op>::value) return launch_parts<Op>(a, b, Dest<typename Op::T>{{c, c, c, c}}, n, stream);
@@ -497,6 +499,7 @@ int launch(const typename Op::T* a, const typename Op::T* b, const typename Op::
     int64_t grid = std::min<int64_t>(ntiles, int64_t(per_sm) * di.num_sms);
     if (grid < 1) grid = 1;
     k_stream<Op><<<static_cast<unsigned>(grid), G::TS, G::SMEM, stream>>>(a, b, s_site, s, c, n);
+    note_kernel(std::string("k_stream<") + Op::name + ">");
     return check_launch(Op::name);
 }
 
@@ -516,6 +519,7 @@ int launch_split(const typename Op::T* a, const typename Op::T* b, Dest<typename
     if (!aligned) {
         const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(di.num_sms) * 8);
         k_direct_split<Op><<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, b, c, n);
+        note_kernel(std::string("k_direct_split<") + Op::name + ">");
         return check_launch(Op::name);
     }
     return launch_parts<Op>(a, b, c, n, stream);
@@ -568,6 +572,7 @@ int launch_sub_four(T* a, const T* b1, const T* b2, const T* b3, const T* b4, in
     const int64_t work = vec ? m / L : m;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, int64_t(di.num_sms) * 8));
     k_sub_four<T, V><<<static_cast<unsigned>(grid), 256, 0, stream>>>(a, b1, b2, b3, b4, m, vec);
+    note_kernel(vec ? "k_sub_four<vectorised>" : "k_sub_four<scalar>");
     return check_launch("sub_four_su3_vecs");
 }
 

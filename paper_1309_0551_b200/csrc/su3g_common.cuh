@@ -22,6 +22,7 @@ namespace su3g {
 void set_error(const std::string& msg);
 int fail_invalid(const std::string& msg);      // returns SU3G_EINVAL
 int check_launch(const char* what);            // cudaGetLastError -> status
+void note_kernel(const std::string& name);     // su3g_last_kernel(): which kernel the last dispatch chose
 
 // ----------------------------------------------------------------------------
 // device properties (cached per device)
@@ -106,6 +107,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
             smem_addr(dst_smem)),
         "l"(src_gmem), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
+}
+
+// global -> L2 only (no smem, no completion): warms L2 for a later reader (bytes % 16 == 0, 16-B aligned)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
 }
 
 // shared -> global, bulk-group completion

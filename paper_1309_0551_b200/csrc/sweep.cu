@@ -21,6 +21,7 @@ extern int g_tma_threads;
 extern int g_link_minb;
 int g_link_zc = 0;   // su3g_set_option("link_zc"): z-planes per visiting chunk of the link kernels (0 = auto)
 int g_sweep_zc = 0;  // su3g_set_option("sweep_zc"): z-planes per chunk of the generic NN / dslash kernels
+int g_sweep_prefetch = 0;  // su3g_set_option("sweep_prefetch"): L2 prefetch distance in quarter waves (0 = off)
 extern int g_link_early_c;
 extern int g_link_smem_a;
 
@@ -83,7 +84,11 @@ __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __rest
 template <typename T, bool FUSED>
 __device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
                                               const Geom& g, int t_begin, int t_end, const T* __restrict__ v_hi,
-                                              const T* __restrict__ w_lo, int ZC) {
+                                              const T* __restrict__ w_lo, int ZC, int ahead = 0) {
+    if (ahead > 0 && threadIdx.x == 0) {
+        prefetch_cta_l2<T>(U, 72, g, blockIdx.x + int64_t(ahead), blockDim.x, t_begin, t_end - t_begin, ZC);
+        prefetch_cta_l2<T>(v, 6, g, blockIdx.x + int64_t(ahead), blockDim.x, t_begin, t_end - t_begin, ZC);
+    }
     // visiting order (z-chunk of ZC planes, t, z, y, x): the t-1 slice a site reads (U_t, v)
     // was streamed ZC*nx*ny sites earlier, not a whole slice earlier -> L2 hits
     const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -104,8 +109,8 @@ __device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* 
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256)
     k_nn_sweep(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin, int t_end,
-               const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC) {
-    nn_sweep_body<T, FUSED>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+               const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC, int ahead) {
+    nn_sweep_body<T, FUSED>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
 }
 
 // occupancy A/B (nn_variant 6): registers capped for MINB CTAs per SM
@@ -126,7 +131,12 @@ __global__ void __launch_bounds__(256, MINB)
 // ---------------------------------------------------------------------------
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256)
-    k_dslash(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int parity, int ZC) {
+    k_dslash(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int parity, int ZC,
+             int ahead) {
+    if (ahead > 0 && threadIdx.x == 0) {
+        prefetch_cta_l2<T>(U, 72, g, blockIdx.x + int64_t(ahead), blockDim.x, 0, g.nt, ZC, 2);
+        prefetch_cta_l2<T>(v, 6, g, blockIdx.x + int64_t(ahead), blockDim.x, 0, g.nt, ZC, 2);
+    }
     const int nxh = g.nx >> 1;
     const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (idx >= (g.F >> 1) * g.nt) return;
@@ -528,7 +538,10 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
         const int rc = mode == SU3G_FMA
                            ? launch_nn_tma64<T, true>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
                            : launch_nn_tma64<T, false>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
-        if (rc != 1) return rc;
+        if (rc != 1) {
+            note_kernel("k_nn_tma64");
+            return rc;
+        }
         if (variant == 5) return fail_invalid("nn_sweep: TMA (register-staged) kernel not applicable to this lattice");
     }
     if (auto_tma || variant == 3) {
@@ -537,7 +550,11 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
         if (variant == 3) return fail_invalid("nn_sweep: TMA kernel not applicable to this lattice");
     }
     if ((auto_walk || variant == 2) && walk_shape(nx, ny, nz, 256, BY, BZ))
+    {
+        note_kernel(std::string("k_nn_walk<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(nx) + "x" +
+                    std::to_string(BY) + "x" + std::to_string(BZ) + ">");
         return launch_walk<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, mode, st);
+    }
     if (variant == 2) return fail_invalid("nn_sweep: walk kernel not applicable to this lattice");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int64_t n = int64_t(t_end - t_begin) * g.F;
@@ -550,10 +567,20 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     if (variant == 6) {  // occupancy A/B knob: register cap for 3 CTAs (24 warps) per SM
         if (mode == SU3G_FMA) k_nn_sweep_capped<T, true, 3><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
         else k_nn_sweep_capped<T, false, 3><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+        note_kernel("k_nn_sweep_capped<3 CTAs/SM>");
         return check_launch("nn_sweep");
     }
-    if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
-    else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC);
+    // L2 prefetch one wave ahead (sweep_prefetch): needs each CTA's sites to be one s3 run
+    int ahead = 0;
+    if (g_sweep_prefetch > 0 && (int64_t(nx) * ny) % 256 == 0 && (aligned16(U) && aligned16(v))) {
+        int per_sm = 0;
+        if (mode == SU3G_FMA) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_sweep<T, true>, 256, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_sweep<T, false>, 256, 0);
+        ahead = std::max(1, std::max(per_sm, 1) * device_info().num_sms * g_sweep_prefetch / 4);
+    }
+    if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    note_kernel(std::string("k_nn_sweep<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
     return check_launch("nn_sweep");
 }
 
@@ -583,8 +610,16 @@ static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     int ZC = big_slice ? chunk_planes(nz, 8) : nz;
     if (g_sweep_zc > 0) ZC = chunk_planes(nz, g_sweep_zc);
     const unsigned gs = static_cast<unsigned>(((g.F >> 1) * nt + 255) / 256);
-    if (mode == SU3G_FMA) k_dslash<T, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC);
-    else k_dslash<T, false><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC);
+    int ahead = 0;
+    if (g_sweep_prefetch > 0 && (int64_t(nx / 2) * ny) % 256 == 0 && aligned16(U) && aligned16(v)) {
+        int per_sm = 0;
+        if (mode == SU3G_FMA) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dslash<T, true>, 256, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dslash<T, false>, 256, 0);
+        ahead = std::max(1, std::max(per_sm, 1) * device_info().num_sms * g_sweep_prefetch / 4);
+    }
+    if (mode == SU3G_FMA) k_dslash<T, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
+    else k_dslash<T, false><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
+    note_kernel(std::string("k_dslash<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
     return check_launch("dslash");
 }
 
@@ -624,6 +659,7 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
         const unsigned grid = static_cast<unsigned>(std::min<int64_t>(G, w.nitems));
         if (mode == SU3G_FMA) k_link_walk<T, true><<<grid, nthr, 0, st>>>(U, acc, g, w, s);
         else k_link_walk<T, false><<<grid, nthr, 0, st>>>(U, acc, g, w, s);
+        note_kernel("k_link_walk");
         return check_launch("link_product(walk)");
     }
     const int64_t n = g.F * nt;
@@ -638,11 +674,13 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     // default (auto) = the low-register rows kernel: 16 warps/SM instead of 8 for f64
     // (48^4 f64, same box: exact 0.323 -> 0.426 of HBM, FMA 0.406 -> 0.465)
     if (lv == 0 || lv == 6) {
+        note_kernel(std::string("k_link_rows<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
         return mode == SU3G_FMA ? launch_link_rows<T, true>(U, acc, g, s, ZC, st)
                                 : launch_link_rows<T, false>(U, acc, g, s, ZC, st);
     }
     if (mode == SU3G_FMA) k_link_product<T, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     else k_link_product<T, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
+    note_kernel(std::string("k_link_product<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
     return check_launch("link_product");
 }
 
@@ -681,6 +719,11 @@ int su3g_set_option(const char* name, int64_t value) {
         if (value != 0 && value != 3 && value != 4 && value != 5 && value != 6 && value != 8)
             return fail_invalid("set_option: link_minb must be 0 (default), 3, 4, 5, 6 or 8");
         g_link_minb = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "sweep_prefetch") == 0) {
+        if (value < 0 || value > 16) return fail_invalid("set_option: sweep_prefetch must be in [0, 16]");
+        g_sweep_prefetch = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "sweep_zc") == 0) {
