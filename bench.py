@@ -72,6 +72,9 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sites", type=int, default=64**4, help="sites for routine:<name> workloads")
+    p.add_argument("--halo", choices=["nccl", "p2p"], default="nccl",
+                   help="t-slab halo transport of the nn-* workloads: NCCL send/recv overlapped with the interior "
+                        "(default), or the fused boundary kernel pushing halos over NVLink (csrc/p2p.cu)")
     p.add_argument("--dims", default=None,
                    help="experiments only: override the lattice nx,ny,nz,nt of nn-*/dslash/link workloads "
                         "(for nn-weak, nt is per GPU)")
@@ -288,21 +291,38 @@ def run_b200(args, rank, world, local):
         v0 = Field.from_aos(lat, "vec", v_aos)
         va, vb = v0.empty_like(), v0.empty_like()
         va.data.copy_(v0.data)
-        slab = SlabSweep(U, kernels=CudaSlabKernels(args.mode))
         ntl = lat.nt
-        if world == 1:
-            per_launch_sites = lat.volume
-        else:
-            per_launch_sites = max(ntl - 2, 0) * lat.slice_sites
-        launches_per_app = slab.launches_per_apply()
-        bytes_per_launch = per_launch_sites * NN_BYTES[args.dtype]
         apps = cfg["apps"]
+        if args.halo == "p2p":
+            from paper_1309_0551_b200.p2p import P2PSlabSweep
 
-        def step(record=False):
-            nonlocal va, vb
-            for _ in range(apps):
-                slab.apply(va, vb, timer=(lambda: _EventTimer(stream, dominant_events)) if record else None)
-                va, vb = vb, va
+            p2p = P2PSlabSweep(U, mode=args.mode)
+            per_launch_sites = lat.volume  # timed unit: one application (boundary + interior launches)
+            launches_per_app = 2 if ntl > 2 else 1
+
+            def step(record=False):
+                nonlocal va, vb
+                for _ in range(apps):
+                    if record:
+                        with _EventTimer(stream, dominant_events):
+                            p2p.apply(va, vb)
+                    else:
+                        p2p.apply(va, vb)
+                    va, vb = vb, va
+        else:
+            slab = SlabSweep(U, kernels=CudaSlabKernels(args.mode))
+            if world == 1:
+                per_launch_sites = lat.volume
+            else:
+                per_launch_sites = max(ntl - 2, 0) * lat.slice_sites
+            launches_per_app = slab.launches_per_apply()
+
+            def step(record=False):
+                nonlocal va, vb
+                for _ in range(apps):
+                    slab.apply(va, vb, timer=(lambda: _EventTimer(stream, dominant_events)) if record else None)
+                    va, vb = vb, va
+        bytes_per_launch = per_launch_sites * NN_BYTES[args.dtype]
 
         launches_per_step = apps * launches_per_app
         sites_per_step = lat.volume * apps  # per rank
@@ -422,7 +442,9 @@ def run_b200(args, rank, world, local):
         step()
     torch.cuda.synchronize(dev)
     dispatched = _l.last_kernel()  # the kernel the last launch of a step dispatched to
-    if cfg["kind"] == "nn" and world > 1:
+    if cfg["kind"] == "nn" and args.halo == "p2p":
+        dispatched = "k_p2p_boundary + interior " + dispatched + " (timed together, per application)"
+    elif cfg["kind"] == "nn" and world > 1:
         dispatched = "interior: " + _interior_kernel(sweeps, U, va, vb, lat.nt, args.mode)
     clocks = ClockSampler(local)
     barrier(world, dev)
@@ -470,7 +492,8 @@ def run_b200(args, rank, world, local):
             "lattice": list(cfg.get("global_dims", [])) or None,
             "sites_per_gpu": sites_per_step // max(cfg["apps"], 1),
             "applications_per_step": cfg["apps"],
-            "parallelism": f"t-slab x{world}" if cfg["kind"] == "nn" else f"replicas x{world}",
+            "parallelism": (f"t-slab x{world}, halos via " + ("fused NVLink push (p2p)" if args.halo == "p2p" else "NCCL")
+                            if cfg["kind"] == "nn" else f"replicas x{world}"),
             "l2": "inputs larger than L2 (U alone > 1 GB/GPU); no flush needed",
         },
         "impl": "b200",
@@ -550,14 +573,25 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
         v_d = torch.empty_like(v_h, device=dev)
         Uf = Field(lat, "mat4", tdt, dev)
         va, vb = Field(lat, "vec", tdt, dev), Field(lat, "vec", tdt, dev)
-        slab = SlabSweep(Uf, kernels=CudaSlabKernels(args.mode))
+        if args.halo == "p2p":
+            from paper_1309_0551_b200.p2p import P2PSlabSweep
+
+            slab = P2PSlabSweep(Uf, mode=args.mode)
+
+            def run_apps(a, b, n):
+                return slab.apply_n(a, n, scratch=b)
+        else:
+            slab = SlabSweep(Uf, kernels=CudaSlabKernels(args.mode))
+
+            def run_apps(a, b, n):
+                return slab.apply_n(a, b, n)
 
         def step():
             U_d.copy_(U_h, non_blocking=True)
             v_d.copy_(v_h, non_blocking=True)
             Field.from_aos(lat, "mat4", U_d, out=Uf)
             Field.from_aos(lat, "vec", v_d, out=va)
-            res = slab.apply_n(va, vb, cfg["apps"])
+            res = run_apps(va, vb, cfg["apps"])
             res.to_aos(out=v_d)
             out_h.copy_(v_d, non_blocking=True)
 

@@ -242,6 +242,38 @@ SU3G_API int su3g_slab_nn_sweep_f32(su3g_comm_t comm, const float *U, const floa
 SU3G_API int su3g_slab_nn_sweep_f64(su3g_comm_t comm, const double *U, const double *v, double *out, int32_t nx,
                                     int32_t ny, int32_t nz, int32_t nt_local, int32_t mode, su3g_stream_t stream);
 
+/* ---- fused compute + halo push over NVLink (t-slab NN sweep) ------------
+ * The boundary kernel of application e computes the slab's slices t = 0 and t = nt-1 and
+ * stores the NEXT application's halos straight into the neighbours' windows (rank r-1 gets
+ * out(t=0) as its v_hi, rank r+1 gets U_t^dag out(nt-1) as its w_lo), then releases a
+ * system-scope flag; the interior slices follow on the same stream while the peers' pushes
+ * land.  No NCCL kernel, no host round trip, bit-identical to the periodic sweep.
+ * Window: one device buffer per rank of su3g_p2p_window_bytes() bytes, zero-initialised
+ * (halo faces x 2 parities + flags); every rank maps its neighbours' windows with CUDA IPC
+ * (su3g_ipc_get_handle / su3g_ipc_open_handle; with one rank, pass the own window as both
+ * peers).  win_lo = window of rank r-1, win_hi = window of rank r+1.
+ * Epochs: su3g_p2p_prime(e) pushes the halos of a fresh source v for application e (call it
+ * after all ranks' previous launches completed, with e greater than every epoch used so far);
+ * su3g_p2p_nn_sweep(e) then computes out = D v for application e and primes e+1 from out, so
+ * ping-pong applications e, e+1, e+2, ... need no further priming.  Waits are bounded
+ * (~20 s): a timed-out wait sets the error word at su3g_p2p_ctrl_offset() + 20. */
+SU3G_API int64_t su3g_p2p_window_bytes(int32_t nx, int32_t ny, int32_t nz, int32_t elem_size);
+SU3G_API int64_t su3g_p2p_ctrl_offset(int32_t nx, int32_t ny, int32_t nz, int32_t elem_size);
+#define SU3G_IPC_HANDLE_BYTES 64
+SU3G_API int su3g_ipc_get_handle(const void *dev_ptr, void *handle_out);
+SU3G_API int su3g_ipc_open_handle(const void *handle, void **dev_ptr_out);
+SU3G_API int su3g_ipc_close(void *dev_ptr);
+SU3G_API int su3g_p2p_prime_f32(const float *U, const float *v, int32_t nx, int32_t ny, int32_t nz, int32_t nt_local,
+                                void *win, void *win_lo, void *win_hi, int64_t epoch, int32_t mode, su3g_stream_t stream);
+SU3G_API int su3g_p2p_prime_f64(const double *U, const double *v, int32_t nx, int32_t ny, int32_t nz, int32_t nt_local,
+                                void *win, void *win_lo, void *win_hi, int64_t epoch, int32_t mode, su3g_stream_t stream);
+SU3G_API int su3g_p2p_nn_sweep_f32(const float *U, const float *v, float *out, int32_t nx, int32_t ny, int32_t nz,
+                                   int32_t nt_local, void *win, void *win_lo, void *win_hi, int64_t epoch, int32_t mode,
+                                   su3g_stream_t stream);
+SU3G_API int su3g_p2p_nn_sweep_f64(const double *U, const double *v, double *out, int32_t nx, int32_t ny, int32_t nz,
+                                   int32_t nt_local, void *win, void *win_lo, void *win_hi, int64_t epoch, int32_t mode,
+                                   su3g_stream_t stream);
+
 /* ---- link-product sweep (BASELINE configs[3]) ------------------------------
  * acc(x) = sum over (mu,nu) in (0,1),(0,2),(0,3),(1,2),(1,3),(2,3) of
  *          s * U_mu(x) U_nu(x+mu) U_mu(x+nu)^dag, accumulated in that order

@@ -19,6 +19,7 @@ SU3G_OK = 0
 SU3G_EINVAL = -1
 SU3G_ENCCL = -2
 SU3G_COMM_ID_BYTES = 128
+SU3G_IPC_HANDLE_BYTES = 64
 SU3G_EXACT = 0
 SU3G_FMA = 1
 
@@ -57,6 +58,11 @@ def _signatures():
         "su3g_comm_init": ([_i32, _i32, _vp, _vp], ctypes.c_int),
         "su3g_comm_destroy": ([_vp], ctypes.c_int),
         "su3g_comm_rank": ([_vp, _vp, _vp], ctypes.c_int),
+        "su3g_p2p_window_bytes": ([_i32, _i32, _i32, _i32], ctypes.c_int64),
+        "su3g_p2p_ctrl_offset": ([_i32, _i32, _i32, _i32], ctypes.c_int64),
+        "su3g_ipc_get_handle": ([_vp, _vp], ctypes.c_int),
+        "su3g_ipc_open_handle": ([_vp, _vp], ctypes.c_int),
+        "su3g_ipc_close": ([_vp], ctypes.c_int),
     }
     for sfx, real in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
         for r in HOT_ROUTINES + EXTRA_AB_ROUTINES:
@@ -70,6 +76,8 @@ def _signatures():
         sig[f"su3g_soa_to_aos_{sfx}"] = ([_vp, _vp, _i64, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp], ctypes.c_int)
         sig[f"su3g_nn_halo_w_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
+        sig[f"su3g_p2p_prime_{sfx}"] = ([_vp, _vp] + [_i32] * 4 + [_vp, _vp, _vp, _i64, _i32, _vp], ctypes.c_int)
+        sig[f"su3g_p2p_nn_sweep_{sfx}"] = ([_vp, _vp, _vp] + [_i32] * 4 + [_vp, _vp, _vp, _i64, _i32, _vp], ctypes.c_int)
         sig[f"su3g_slab_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_dslash_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_link_product_{sfx}"] = ([_vp, _vp, _i32, _i32, _i32, _i32, real, _i32, _vp], ctypes.c_int)

@@ -1,0 +1,64 @@
+// The per-site NN operator shared by the sweep kernels (sweep.cu) and the fused
+// peer-push boundary kernel (p2p.cu): one site's out(x), in the association of the
+// composed reference oracle.
+#pragma once
+
+#include "sweep_common.cuh"
+#include "su3_math.cuh"
+
+namespace su3g {
+
+// One site of the NN sweep: out(x) = sum_mu U_mu(x) v(x+mu) - sum_mu U_mu(x-mu)^dag v(x-mu), association of
+// the composed reference (add_su3_vector chain, then sub_four_su3_vecs).  v_hi / w_lo: t-slab halos (or null).
+template <typename T, bool FUSED>
+__device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
+                                        const Geom& g, int x, int y, int z, int t, const T* __restrict__ v_hi,
+                                        const T* __restrict__ w_lo) {
+    const int64_t F = g.F;
+    const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
+    T acc[6];
+    // forward terms, mu = 0..3, summed left to right (add_su3_vector chain)
+#pragma unroll
+    for (int mu = 0; mu < 4; ++mu) {
+        T u[18], vn[6], f[6];
+        ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, s3, u);
+        if (mu < 3) {
+            ld_soa<T, 6>(v + int64_t(t) * 6 * F, F, step3(g, x, y, z, mu, +1), vn);
+        } else if (t + 1 < g.nt) {
+            ld_soa<T, 6>(v + int64_t(t + 1) * 6 * F, F, s3, vn);
+        } else if (v_hi != nullptr) {
+            ld_soa<T, 6>(v_hi, F, s3, vn);
+        } else {
+            ld_soa<T, 6>(v, F, s3, vn);
+        }
+        mv<T, FUSED>(u, vn, f);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) acc[k] = (mu == 0) ? f[k] : xadd(acc[k], f[k]);
+    }
+    // backward terms, subtracted left to right (sub_four_su3_vecs)
+#pragma unroll
+    for (int mu = 0; mu < 4; ++mu) {
+        T w[6];
+        if (mu < 3) {
+            T u[18], vn[6];
+            const int64_t d = step3(g, x, y, z, mu, -1);
+            ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, d, u);
+            ld_soa<T, 6>(v + int64_t(t) * 6 * F, F, d, vn);
+            amv<T, FUSED>(u, vn, w);
+        } else if (t > 0 || w_lo == nullptr) {
+            const int tp = (t > 0) ? t - 1 : g.nt - 1;
+            T u[18], vn[6];
+            ld_soa<T, 18>(U + (int64_t(tp) * 72 + 3 * 18) * F, F, s3, u);
+            ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vn);
+            amv<T, FUSED>(u, vn, w);
+        } else {
+            ld_soa<T, 6>(w_lo, F, s3, w);
+        }
+#pragma unroll
+        for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], w[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 6; ++k) out[(int64_t(t) * 6 + k) * F + s3] = acc[k];
+}
+
+}  // namespace su3g

@@ -278,3 +278,14 @@ def test_comm_abi_without_a_gpu():
     assert lib.su3g_slab_nn_sweep_f32(None, None, None, None, 4, 4, 4, 4, 0, None) == _lib.SU3G_EINVAL
     with pytest.raises(ValueError, match="128"):
         NativeComm(1, 0, b"short")
+
+
+def test_p2p_abi_argument_checks():
+    lib = _lib.load()
+    nb = lib.su3g_p2p_window_bytes(64, 64, 64, 4)
+    assert nb == 4 * 6 * 64**3 * 4 + 128 and lib.su3g_p2p_ctrl_offset(64, 64, 64, 4) == nb - 128
+    assert lib.su3g_p2p_window_bytes(0, 4, 4, 4) == -1 and lib.su3g_p2p_window_bytes(4, 4, 4, 2) == -1
+    assert lib.su3g_p2p_nn_sweep_f32(None, None, None, 4, 4, 4, 4, None, None, None, 0, 0, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_p2p_prime_f64(None, None, 4, 4, 4, 4, None, None, None, 0, 0, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_ipc_get_handle(None, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_ipc_close(None) == _lib.SU3G_OK
