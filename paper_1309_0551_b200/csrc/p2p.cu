@@ -119,8 +119,7 @@ __global__ void __launch_bounds__(256)
     k_p2p_prime(const T* __restrict__ U, const T* __restrict__ v, Geom g, Window<T> me, Window<T> lo, Window<T> hi,
                 long long epoch) {
     const int par = static_cast<int>(epoch & 1);
-    const int64_t s3 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (s3 < g.F) {
+    for (int64_t s3 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s3 < g.F; s3 += int64_t(gridDim.x) * blockDim.x) {
 #pragma unroll
         for (int c = 0; c < 6; ++c) lo.vhi[par][c * g.F + s3] = v[c * g.F + s3];  // v(t=0) -> rank r-1
         push_w<T, FUSED>(U, v, g, s3, hi.wlo[par]);                                // w(nt-1) -> rank r+1
@@ -136,8 +135,9 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     const int par = static_cast<int>(epoch & 1), nxt = par ^ 1;
     const int nsl = g.nt == 1 ? 1 : 2;
-    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-    if (idx < nsl * g.F) {
+    // grid-stride over the boundary sites: few, persistent CTAs, so few system-scope fences in signal_peers
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < nsl * g.F;
+         idx += int64_t(gridDim.x) * blockDim.x) {
         const int t = idx < g.F ? 0 : g.nt - 1;
         const int64_t s3 = idx < g.F ? idx : idx - g.F;
         const int x = static_cast<int>(s3 % g.nx);
@@ -170,7 +170,8 @@ int p2p_prime(const T* U, const T* v, int nx, int ny, int nz, int nt, void* me, 
     if (!U || !v) return fail_invalid("p2p_prime: null pointer");
     if (epoch < 0) return fail_invalid("p2p_prime: epoch must be >= 0");
     const Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
-    const unsigned grid = static_cast<unsigned>((g.F + 255) / 256);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>((g.F + 255) / 256, 4LL * device_info().num_sms)));
     const Window<T> wm = window_at<T>(me, g.F), wl = window_at<T>(lo, g.F), wh = window_at<T>(hi, g.F);
     if (mode == SU3G_FMA) k_p2p_prime<T, true><<<grid, 256, 0, st>>>(U, v, g, wm, wl, wh, epoch);
     else k_p2p_prime<T, false><<<grid, 256, 0, st>>>(U, v, g, wm, wl, wh, epoch);
@@ -187,7 +188,8 @@ int p2p_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, vo
     if (epoch < 0) return fail_invalid("p2p_nn_sweep: epoch must be >= 0");
     const Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int nsl = nt == 1 ? 1 : 2;
-    const unsigned grid = static_cast<unsigned>((nsl * g.F + 255) / 256);
+    const unsigned grid = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>((nsl * g.F + 255) / 256, 4LL * device_info().num_sms)));
     const Window<T> wm = window_at<T>(me, g.F), wl = window_at<T>(lo, g.F), wh = window_at<T>(hi, g.F);
     // boundary first: its pushes for application e+1 then overlap this rank's interior
     if (mode == SU3G_FMA) k_p2p_boundary<T, true><<<grid, 256, 0, st>>>(U, v, out, g, wm, wl, wh, epoch);
