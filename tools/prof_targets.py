@@ -1,7 +1,8 @@
-"""Launch each profiling target a few times in one process (for a single ncu capture).
+"""Launch each profiling target ONCE in one process, for a single ncu capture:
 
-    ncu --set full -k regex:'k_link_rows|k_dslash' ... python tools/prof_targets.py
-Targets: link product 48^4 f64 exact (k_link_rows), even/odd dslash 64^3x16 f32 exact (k_dslash).
+    ncu --set full -k regex:'k_link_rows|k_dslash|k_nn_tma' -c 3 ... python tools/prof_targets.py
+Targets: link product 48^4 f64 exact (k_link_rows), even/odd dslash 64^3x16 f32 exact (k_dslash),
+NN sweep 64^3x16 f32 exact (k_nn_tma, the headline kernel).
 """
 import os
 import sys
@@ -20,16 +21,14 @@ def main():
     gen.manual_seed(5)
     lat = Lattice4D(48, 48, 48, 48)
     U = Field.from_aos(lat, "mat4", inputs.random_links_torch(lat.volume, 4, torch.float64, dev, gen))
-    for _ in range(3):
-        acc = sweeps.link_product(U, 1.0 / 6.0)
-    del U, acc
+    sweeps.link_product(U, 1.0 / 6.0)
+    del U
     lat = Lattice4D(64, 64, 64, 16)
     U = Field.from_aos(lat, "mat4", inputs.random_links_torch(lat.volume, 4, torch.float32, dev, gen))
     v = Field.from_aos(lat, "vec", inputs.random_vectors_torch(lat.volume, None, torch.float32, dev, gen))
     out = v.empty_like()
-    for _ in range(3):
-        for parity in (0, 1):
-            sweeps.dslash(U, v, parity, out=out)
+    sweeps.dslash(U, v, 0, out=out)
+    sweeps.nn_sweep(U, v, out=out)
     torch.cuda.synchronize()
     print("ok")
 

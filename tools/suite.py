@@ -55,7 +55,10 @@ def main():
         run(["--workload", "nn-strong", "--dtype", "f32"], steps="5")
         run(["--workload", "nn-strong", "--dtype", "f64"], steps="5")
         run(["--workload", "link", "--dtype", "f64"], steps="5")
-        run(["--workload", "link", "--dtype", "f64"], env={"SU3G_LINK_MODE": "exact"}, steps="5")
+        run(["--workload", "link", "--dtype", "f64"], env={"SU3G_LINK_MODE": "fma"}, steps="5")
+        run(["--workload", "link", "--dtype", "f32"], steps="5")
+        run(["--workload", "dslash", "--dtype", "f32"])
+        run(["--workload", "dslash", "--dtype", "f64"])
 
 
 if __name__ == "__main__":
