@@ -66,7 +66,7 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *                   (accumulator in smem)
  *   "link_minb":    CTAs/SM the rows kernel's register budget targets: 0 default (f64: 4 exact,
  *                   3 FMA; f32: 6), 3, 4, 5, 6 or 8
- *   "link_smem_a":  1 = the rows kernel keeps U_mu(x) in shared memory per mu group (A/B)
+ *   "link_prefetch_b": 1 = the rows kernel gathers the next plane's U_nu(x+mu) during this plane (A/B)
  *   "link_zc":      z-planes per visiting chunk of the link kernels (largest divisor of nz <= value;
  *                   0 = auto: 16 when a t-slice of links exceeds half of L2, else nz)
  *   "sweep_zc":     the same for the one-thread-per-site NN sweep and dslash kernels (auto: 8)

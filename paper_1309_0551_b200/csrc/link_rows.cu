@@ -50,15 +50,12 @@ __device__ __forceinline__ void dot3(PF p, QF q, T& re, T& im) {
 
 }  // namespace
 
-template <typename T, bool FUSED, int MINB, bool EARLY_C, bool SMEM_A>
+template <typename T, bool FUSED, int MINB, bool EARLY_C, bool PREF_B>
 __global__ void __launch_bounds__(128, MINB)
     k_link_rows(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC, int ahead) {
     if (ahead > 0 && threadIdx.x == 0)  // L2 prefetch of the CTA one wave ahead (sweep_prefetch)
         prefetch_cta_l2<T>(U, 72, g, blockIdx.x + int64_t(ahead), blockDim.x, 0, g.nt, ZC);
     __shared__ T sacc[18 * 128];
-    // SMEM_A: A = U_mu(x) is gathered once per mu group (planes 0-2, 3-4, 5) into this thread's
-    // column of sA instead of once per plane from L2
-    __shared__ T sA[SMEM_A ? 18 * 128 : 1];
     const int tid = threadIdx.x;
     const int64_t idx = blockIdx.x * int64_t(blockDim.x) + tid;
     if (idx >= g.F * g.nt) return;  // no block-level sync below: early exit is safe
@@ -74,39 +71,38 @@ __global__ void __launch_bounds__(128, MINB)
     const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
     const int64_t site = int64_t(t) * g.F + s3;
     T* acc = sacc + tid;  // element k at acc[k * 128]
+    // PREF_B: B of plane p+1 is gathered during plane p's C phase (one more matrix in flight)
+    T bn[PREF_B ? 18 : 1];
+    if constexpr (PREF_B) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, c_plane_mu[0]), c_plane_nu[0], 0, bn);
 
 #pragma unroll 1
     for (int pl = 0; pl < 6; ++pl) {
         const int mu = c_plane_mu[pl], nu = c_plane_nu[pl];
-        if constexpr (SMEM_A) {
-            if (pl == 0 || pl == 3 || pl == 5) {
-                T a[18];
-                ld_link_part<T, 18>(U, g, site, mu, 0, a);
-#pragma unroll
-                for (int k = 0; k < 18; ++k) sA[k * 128 + tid] = a[k];
-            }
-        }
         T tm[18], c[18];
         // EARLY_C: gather C with B (both in flight together, +18 live reals); else after T is built
         if constexpr (EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);
         {
             T b[18];
-            ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b);  // B = U_nu(x + mu)
+            if constexpr (PREF_B) {
+#pragma unroll
+                for (int k = 0; k < 18; ++k) b[k] = bn[k];
+            } else {
+                ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b);  // B = U_nu(x + mu)
+            }
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 T a[6];
-                if constexpr (SMEM_A) {
-#pragma unroll
-                    for (int k = 0; k < 6; ++k) a[k] = sA[(6 * i + k) * 128 + tid];
-                } else {
-                    ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
-                }
+                ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
 #pragma unroll
                 for (int k = 0; k < 3; ++k)  // t[i][k] = sum_j a[i][j] b[j][k]   (mat_nn)
                     dot3<T, FUSED, PLAIN>([&](int j, int q) { return a[2 * j + q]; },
                                           [&](int j, int q) { return b[(3 * j + k) * 2 + q]; }, tm[(3 * i + k) * 2],
                                           tm[(3 * i + k) * 2 + 1]);
             }
+        }
+        if constexpr (PREF_B) {
+            if (pl < 5)
+                ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, c_plane_mu[pl + 1]), c_plane_nu[pl + 1], 0, bn);
         }
         if constexpr (!EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);  // C = U_mu(x + nu)
 #pragma unroll
@@ -132,18 +128,18 @@ __global__ void __launch_bounds__(128, MINB)
 
 int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
 int g_link_early_c = -1;  // su3g_set_option("link_early_c"): gather C together with B (-1 = default)
-int g_link_smem_a = 0;
-extern int g_sweep_prefetch;    // su3g_set_option("link_smem_a"): keep A = U_mu(x) in smem per mu group
+int g_link_pref_b = 0;    // su3g_set_option("link_prefetch_b"): gather the next plane's B during this plane
+extern int g_sweep_prefetch;
 
-template <typename T, bool FUSED, bool EARLY_C, bool SMEM_A>
+template <typename T, bool FUSED, bool EARLY_C, bool PREF_B>
 static void launch_rows_minb(const T* U, T* acc, const Geom& g, T s, int ZC, unsigned grid, int minb, int ahead,
                              cudaStream_t st) {
     switch (minb) {
-        case 3: k_link_rows<T, FUSED, 3, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
-        case 5: k_link_rows<T, FUSED, 5, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
-        case 6: k_link_rows<T, FUSED, 6, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
-        case 8: k_link_rows<T, FUSED, 8, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
-        default: k_link_rows<T, FUSED, 4, EARLY_C, SMEM_A><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        case 3: k_link_rows<T, FUSED, 3, EARLY_C, PREF_B><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        case 5: k_link_rows<T, FUSED, 5, EARLY_C, PREF_B><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        case 6: k_link_rows<T, FUSED, 6, EARLY_C, PREF_B><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        case 8: k_link_rows<T, FUSED, 8, EARLY_C, PREF_B><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
+        default: k_link_rows<T, FUSED, 4, EARLY_C, PREF_B><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead); break;
     }
 }
 
@@ -159,7 +155,7 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     const int ahead = (g_sweep_prefetch > 0 && (int64_t(g.nx) * g.ny) % 128 == 0 && aligned16(U))
                           ? std::max(1, minb * device_info().num_sms * g_sweep_prefetch / 4)
                           : 0;
-    if (g_link_smem_a) {
+    if (g_link_pref_b) {
         if (early_c) launch_rows_minb<T, FUSED, true, true>(U, acc, g, s, ZC, grid, minb, ahead, st);
         else launch_rows_minb<T, FUSED, false, true>(U, acc, g, s, ZC, grid, minb, ahead, st);
     } else {

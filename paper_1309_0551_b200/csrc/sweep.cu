@@ -24,7 +24,7 @@ int g_link_zc = 0;   // su3g_set_option("link_zc"): z-planes per visiting chunk 
 int g_sweep_zc = 0;  // su3g_set_option("sweep_zc"): z-planes per chunk of the generic NN / dslash kernels
 int g_sweep_prefetch = 0;  // su3g_set_option("sweep_prefetch"): L2 prefetch distance in quarter waves (0 = off)
 extern int g_link_early_c;
-extern int g_link_smem_a;
+extern int g_link_pref_b;
 
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
@@ -679,9 +679,9 @@ int su3g_set_option(const char* name, int64_t value) {
         g_sweep_zc = static_cast<int>(value);
         return SU3G_OK;
     }
-    if (std::strcmp(name, "link_smem_a") == 0) {
-        if (value != 0 && value != 1) return fail_invalid("set_option: link_smem_a must be 0 or 1");
-        g_link_smem_a = static_cast<int>(value);
+    if (std::strcmp(name, "link_prefetch_b") == 0) {
+        if (value != 0 && value != 1) return fail_invalid("set_option: link_prefetch_b must be 0 or 1");
+        g_link_pref_b = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_zc") == 0) {
