@@ -10,11 +10,37 @@ namespace su3g {
 
 // One site of the NN sweep: out(x) = sum_mu U_mu(x) v(x+mu) - sum_mu U_mu(x-mu)^dag v(x-mu), association of
 // the composed reference (add_su3_vector chain, then sub_four_su3_vecs).  v_hi / w_lo: t-slab halos (or null).
-template <typename T, bool FUSED>
+// L2 eviction hints (HINTS): in the one-thread-per-site visiting orders every link is read
+// twice -- first as a site's own forward link, last as the next site's backward link --
+// so the backward gathers are marked evict-first (their line has no further use) and the
+// output is stored streaming, leaving L2 to the lines that will be read again.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
+    float r;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
+    double r;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+template <typename T, int N>
+__device__ __forceinline__ void ld_soa_last(const T* __restrict__ p, int64_t F, int64_t s3, T* r, uint64_t pol) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) r[k] = ld_hint(p + k * F + s3, pol);
+}
+
+template <typename T, bool FUSED, bool HINTS = false>
 __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
                                         const Geom& g, int x, int y, int z, int t, const T* __restrict__ v_hi,
                                         const T* __restrict__ w_lo) {
     const int64_t F = g.F;
+    const uint64_t pol = HINTS ? l2_evict_first_policy() : 0;
     const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
     T acc[6];
     // forward terms, mu = 0..3, summed left to right (add_su3_vector chain)
@@ -42,13 +68,15 @@ __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __rest
         if (mu < 3) {
             T u[18], vn[6];
             const int64_t d = step3(g, x, y, z, mu, -1);
-            ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, d, u);
+            if constexpr (HINTS) ld_soa_last<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, d, u, pol);
+            else ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, d, u);
             ld_soa<T, 6>(v + int64_t(t) * 6 * F, F, d, vn);
             amv<T, FUSED>(u, vn, w);
         } else if (t > 0 || w_lo == nullptr) {
             const int tp = (t > 0) ? t - 1 : g.nt - 1;
             T u[18], vn[6];
-            ld_soa<T, 18>(U + (int64_t(tp) * 72 + 3 * 18) * F, F, s3, u);
+            if constexpr (HINTS) ld_soa_last<T, 18>(U + (int64_t(tp) * 72 + 3 * 18) * F, F, s3, u, pol);
+            else ld_soa<T, 18>(U + (int64_t(tp) * 72 + 3 * 18) * F, F, s3, u);
             ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vn);
             amv<T, FUSED>(u, vn, w);
         } else {
@@ -58,7 +86,10 @@ __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __rest
         for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], w[k]);
     }
 #pragma unroll
-    for (int k = 0; k < 6; ++k) out[(int64_t(t) * 6 + k) * F + s3] = acc[k];
+    for (int k = 0; k < 6; ++k) {
+        if constexpr (HINTS) __stcs(out + (int64_t(t) * 6 + k) * F + s3, acc[k]);
+        else out[(int64_t(t) * 6 + k) * F + s3] = acc[k];
+    }
 }
 
 }  // namespace su3g

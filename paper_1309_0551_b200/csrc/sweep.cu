@@ -22,6 +22,7 @@ extern int g_tma_threads;
 extern int g_link_minb;
 int g_link_zc = 0;   // su3g_set_option("link_zc"): z-planes per visiting chunk of the link kernels (0 = auto)
 int g_sweep_zc = 0;  // su3g_set_option("sweep_zc"): z-planes per chunk of the generic NN / dslash kernels
+int g_sweep_hints = 0;     // su3g_set_option("sweep_l2_hints"): evict-first backward gathers, streaming stores
 int g_sweep_prefetch = 0;  // su3g_set_option("sweep_prefetch"): L2 prefetch distance in quarter waves (0 = off)
 extern int g_link_early_c;
 extern int g_link_pref_b;
@@ -29,7 +30,7 @@ extern int g_link_pref_b;
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
 // ---------------------------------------------------------------------------
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool HINTS = false>
 __device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
                                               const Geom& g, int t_begin, int t_end, const T* __restrict__ v_hi,
                                               const T* __restrict__ w_lo, int ZC, int ahead = 0) {
@@ -50,15 +51,15 @@ __device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* 
     r /= ZC;
     const int t = t_begin + static_cast<int>(r % nts);
     const int z = static_cast<int>(r / nts) * ZC + zl;
-    nn_site<T, FUSED>(U, v, out, g, x, y, z, t, v_hi, w_lo);
+    nn_site<T, FUSED, HINTS>(U, v, out, g, x, y, z, t, v_hi, w_lo);
 }
 
 // plain bounds: ptxas picks 64-98 registers; an explicit minBlocks of 1 would let it take 252
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool HINTS = false>
 __global__ void __launch_bounds__(256)
     k_nn_sweep(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin, int t_end,
                const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC, int ahead) {
-    nn_sweep_body<T, FUSED>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    nn_sweep_body<T, FUSED, HINTS>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
 }
 
 // occupancy A/B (nn_variant 6): registers capped for MINB CTAs per SM
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(256, MINB)
 // equals the full sweep's on those sites bit for bit.  Sites of the other parity in `out`
 // are not touched.  One thread per output site, (z-chunk, t, z, y, x/2) order.
 // ---------------------------------------------------------------------------
-template <typename T, bool FUSED>
+template <typename T, bool FUSED, bool HINTS = false>
 __global__ void __launch_bounds__(256)
     k_dslash(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int parity, int ZC,
              int ahead) {
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(256)
     const int t = static_cast<int>(r % g.nt);
     const int z = static_cast<int>(r / g.nt) * ZC + zl;
     const int x = 2 * xh + ((y + z + t + parity) & 1);
-    nn_site<T, FUSED>(U, v, out, g, x, y, z, t, nullptr, nullptr);
+    nn_site<T, FUSED, HINTS>(U, v, out, g, x, y, z, t, nullptr, nullptr);
 }
 
 template <typename T, bool FUSED>
@@ -526,8 +527,13 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_sweep<T, false>, 256, 0);
         ahead = std::max(1, std::max(per_sm, 1) * device_info().num_sms * g_sweep_prefetch / 4);
     }
-    if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
-    else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    if (g_sweep_hints) {
+        if (mode == SU3G_FMA) k_nn_sweep<T, true, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+        else k_nn_sweep<T, false, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    } else {
+        if (mode == SU3G_FMA) k_nn_sweep<T, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+        else k_nn_sweep<T, false><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    }
     note_kernel(std::string("k_nn_sweep<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
     return check_launch("nn_sweep");
 }
@@ -565,8 +571,13 @@ static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dslash<T, false>, 256, 0);
         ahead = std::max(1, std::max(per_sm, 1) * device_info().num_sms * g_sweep_prefetch / 4);
     }
-    if (mode == SU3G_FMA) k_dslash<T, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
-    else k_dslash<T, false><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
+    if (g_sweep_hints) {
+        if (mode == SU3G_FMA) k_dslash<T, true, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
+        else k_dslash<T, false, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
+    } else {
+        if (mode == SU3G_FMA) k_dslash<T, true><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
+        else k_dslash<T, false><<<gs, 256, 0, st>>>(U, v, out, g, parity, ZC, ahead);
+    }
     note_kernel(std::string("k_dslash<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
     return check_launch("dslash");
 }
@@ -667,6 +678,11 @@ int su3g_set_option(const char* name, int64_t value) {
         if (value != 0 && value != 3 && value != 4 && value != 5 && value != 6 && value != 8)
             return fail_invalid("set_option: link_minb must be 0 (default), 3, 4, 5, 6 or 8");
         g_link_minb = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "sweep_l2_hints") == 0) {
+        if (value != 0 && value != 1) return fail_invalid("set_option: sweep_l2_hints must be 0 or 1");
+        g_sweep_hints = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "sweep_prefetch") == 0) {

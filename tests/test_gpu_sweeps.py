@@ -423,3 +423,28 @@ def test_dslash_argument_errors():
     with pytest.raises(ValueError, match="alias"):
         sweeps.dslash(U, v, 0, out=v)
     assert _lib.load().su3g_dslash_f32(None, None, None, 4, 4, 4, 4, 0, 0, None) == _lib.SU3G_EINVAL
+
+
+@pytest.mark.parametrize("option", ["sweep_l2_hints", "sweep_prefetch"])
+def test_generic_kernel_knobs_keep_results_bitwise(option, precision):
+    """Cache-hint / prefetch knobs of the one-thread-per-site kernels never change a bit."""
+    from paper_1309_0551_b200 import _lib
+
+    dt = _dt(precision)
+    dims = (16, 16, 8, 4)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(9100)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    want = coracle.nn_sweep(U, v, dims)
+    from oracle import sweeps as OS
+
+    even = OS.parity_mask(dims)
+    _lib.set_option(option, 1)
+    _lib.set_option("nn_variant", 1)
+    try:
+        assert np.array_equal(sweeps.nn_sweep_aos(U, v, dims), want)
+        assert np.array_equal(sweeps.dslash_aos(U, v, dims, 0)[even], want[even])
+    finally:
+        _lib.set_option(option, 0)
+        _lib.set_option("nn_variant", 0)
