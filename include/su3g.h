@@ -70,8 +70,10 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "link_zc":      z-planes per visiting chunk of the link kernels (largest divisor of nz <= value;
  *                   0 = auto: 16 when a t-slice of links exceeds half of L2, else nz)
  *   "sweep_zc":     the same for the one-thread-per-site NN sweep and dslash kernels (auto: 8)
- *   "sweep_l2_hints": 1 = the one-thread-per-site NN / dslash kernels load backward (last-use) links
- *                   evict-first in L2 and store their output streaming (A/B)
+ *   "sweep_l2_hints": 1 (default) = the one-thread-per-site NN / dslash kernels load backward
+ *                   (last-use) links and v(t-1) evict-first in L2 and store their output streaming
+ *   "link_l2_hints": 1 = the link rows kernel marks each link's last-use gather evict-first (A/B;
+ *                   default register targets only)
  *   "sweep_prefetch": L2 prefetch distance of the one-thread-per-site kernels (generic NN, dslash,
  *                   link rows) in quarter waves of CTAs: thread 0 issues cp.async.bulk.prefetch.L2
  *                   for the sites of the CTA that far ahead (0 = off, max 16)

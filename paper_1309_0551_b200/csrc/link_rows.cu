@@ -16,8 +16,7 @@
 // mode is bit-identical to the reference composition.
 #include <algorithm>
 
-#include "sweep_common.cuh"
-#include "su3_math.cuh"
+#include "nn_site.cuh"
 
 namespace su3g {
 
@@ -50,9 +49,13 @@ __device__ __forceinline__ void dot3(PF p, QF q, T& re, T& im) {
 
 }  // namespace
 
-template <typename T, bool FUSED, int MINB, bool EARLY_C, bool PREF_B>
+template <typename T, bool FUSED, int MINB, bool EARLY_C, bool PREF_B, bool HINTS = false>
 __global__ void __launch_bounds__(128, MINB)
     k_link_rows(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC, int ahead) {
+    // HINTS: in the (z-chunk, t, z, y, x) order a link's last reader is: U_mu(y), mu < 3, its own site's
+    // A in the last plane of the mu group (planes 2, 4, 5); U_t(y) the B of plane (0,3) at y - x.
+    // Those gathers are marked L2 evict-first and the result is stored streaming.
+    const uint64_t pol = HINTS ? l2_evict_first_policy() : 0;
     if (ahead > 0 && threadIdx.x == 0)  // L2 prefetch of the CTA one wave ahead (sweep_prefetch)
         prefetch_cta_l2<T>(U, 72, g, blockIdx.x + int64_t(ahead), blockDim.x, 0, g.nt, ZC);
     __shared__ T sacc[18 * 128];
@@ -87,12 +90,20 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
                 for (int k = 0; k < 18; ++k) b[k] = bn[k];
             } else {
-                ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b);  // B = U_nu(x + mu)
+                if (HINTS && pl == 2) {
+                    const int64_t nb = shifted(g, x, y, z, t, mu), tn = nb / g.F;
+                    ld_soa_last<T, 18>(U + (tn * 72 + nu * 18) * g.F, g.F, nb - tn * g.F, b, pol);
+                } else {
+                    ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b);  // B = U_nu(x + mu)
+                }
             }
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 T a[6];
-                ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
+                if (HINTS && (pl == 2 || pl == 4 || pl == 5))
+                    ld_soa_last<T, 6>(U + (int64_t(t) * 72 + mu * 18 + 6 * i) * g.F, g.F, s3, a, pol);
+                else
+                    ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
 #pragma unroll
                 for (int k = 0; k < 3; ++k)  // t[i][k] = sum_j a[i][j] b[j][k]   (mat_nn)
                     dot3<T, FUSED, PLAIN>([&](int j, int q) { return a[2 * j + q]; },
@@ -123,11 +134,15 @@ __global__ void __launch_bounds__(128, MINB)
             }
     }
 #pragma unroll
-    for (int k = 0; k < 18; ++k) acc_out[(int64_t(t) * 18 + k) * g.F + s3] = acc[k * 128];
+    for (int k = 0; k < 18; ++k) {
+        if constexpr (HINTS) __stcs(acc_out + (int64_t(t) * 18 + k) * g.F + s3, acc[k * 128]);
+        else acc_out[(int64_t(t) * 18 + k) * g.F + s3] = acc[k * 128];
+    }
 }
 
 int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
 int g_link_early_c = -1;  // su3g_set_option("link_early_c"): gather C together with B (-1 = default)
+int g_link_hints = 0;     // su3g_set_option("link_l2_hints"): last-use gathers evict-first (A/B)
 int g_link_pref_b = 0;    // su3g_set_option("link_prefetch_b"): gather the next plane's B during this plane
 extern int g_sweep_prefetch;
 
@@ -155,7 +170,12 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     const int ahead = (g_sweep_prefetch > 0 && (int64_t(g.nx) * g.ny) % 128 == 0 && aligned16(U))
                           ? std::max(1, minb * device_info().num_sms * g_sweep_prefetch / 4)
                           : 0;
-    if (g_link_pref_b) {
+    if (g_link_hints && !g_link_pref_b) {
+        if (early_c) k_link_rows<T, FUSED, sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6, true, false, true>
+                         <<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead);
+        else k_link_rows<T, FUSED, sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6, false, false, true>
+                 <<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead);
+    } else if (g_link_pref_b) {
         if (early_c) launch_rows_minb<T, FUSED, true, true>(U, acc, g, s, ZC, grid, minb, ahead, st);
         else launch_rows_minb<T, FUSED, false, true>(U, acc, g, s, ZC, grid, minb, ahead, st);
     } else {

@@ -77,7 +77,9 @@ __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __rest
             T u[18], vn[6];
             if constexpr (HINTS) ld_soa_last<T, 18>(U + (int64_t(tp) * 72 + 3 * 18) * F, F, s3, u, pol);
             else ld_soa<T, 18>(U + (int64_t(tp) * 72 + 3 * 18) * F, F, s3, u);
-            ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vn);
+            // v(x, t-1): its last reader in the visiting order is this backward t term
+            if constexpr (HINTS) ld_soa_last<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vn, pol);
+            else ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vn);
             amv<T, FUSED>(u, vn, w);
         } else {
             ld_soa<T, 6>(w_lo, F, s3, w);

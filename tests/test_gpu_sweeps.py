@@ -425,8 +425,9 @@ def test_dslash_argument_errors():
     assert _lib.load().su3g_dslash_f32(None, None, None, 4, 4, 4, 4, 0, 0, None) == _lib.SU3G_EINVAL
 
 
-@pytest.mark.parametrize("option", ["sweep_l2_hints", "sweep_prefetch"])
-def test_generic_kernel_knobs_keep_results_bitwise(option, precision):
+@pytest.mark.parametrize("option,value,default", [("sweep_l2_hints", 0, 1), ("sweep_prefetch", 1, 0),
+                                                  ("link_l2_hints", 1, 0)])
+def test_generic_kernel_knobs_keep_results_bitwise(option, value, default, precision):
     """Cache-hint / prefetch knobs of the one-thread-per-site kernels never change a bit."""
     from paper_1309_0551_b200 import _lib
 
@@ -440,11 +441,12 @@ def test_generic_kernel_knobs_keep_results_bitwise(option, precision):
     from oracle import sweeps as OS
 
     even = OS.parity_mask(dims)
-    _lib.set_option(option, 1)
+    _lib.set_option(option, value)
     _lib.set_option("nn_variant", 1)
     try:
         assert np.array_equal(sweeps.nn_sweep_aos(U, v, dims), want)
         assert np.array_equal(sweeps.dslash_aos(U, v, dims, 0)[even], want[even])
+        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), coracle.link_product(U, dims, 1 / 6))
     finally:
-        _lib.set_option(option, 0)
+        _lib.set_option(option, default)
         _lib.set_option("nn_variant", 0)
