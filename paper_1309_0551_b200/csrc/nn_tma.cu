@@ -27,9 +27,11 @@
 #include <cstring>
 #include <mutex>
 
-#include "sweep_common.cuh"
+#include "nn_site.cuh"
 
 namespace su3g {
+
+int g_tma_hints = 0;  // su3g_set_option("nn_tma_l2_hints")
 
 namespace {
 
@@ -94,6 +96,7 @@ struct TmaParams {
     int nchunks;
     int64_t nitems;
     int has_vhi;   // v(t = nt) comes from the v_hi face
+    int hints;     // U_t gathers evict-first in L2 (read exactly once), output stored streaming
 };
 
 // item -> (block, t0, t1), chunk-major
@@ -251,8 +254,11 @@ __global__ void __launch_bounds__(NTHR, 1)
         enter(c);
         return c;
     };
+    const uint64_t pol_once = l2_evict_first_policy();
     auto load_ut = [&](const Cursor& c, T* r) {
-        if (c.valid) ld_soa<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, c.s3, r);
+        if (!c.valid) return;
+        if (p.hints) ld_soa_last<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, c.s3, r, pol_once);
+        else ld_soa<T, 18>(U + (int64_t(c.t) * 72 + 54) * F, F, c.s3, r);
     };
 
     T vc[6], wt[6], ut[18], ut1[18];
@@ -385,8 +391,13 @@ __global__ void __launch_bounds__(NTHR, 1)
             for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], wt[q]);
 
             T* o = out + int64_t(t) * 6 * F + s3;
+            if (p.hints) {
 #pragma unroll
-            for (int q = 0; q < 6; ++q) o[q * F] = acc[q];
+                for (int q = 0; q < 6; ++q) __stcs(o + q * F, acc[q]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 6; ++q) o[q * F] = acc[q];
+            }
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 vc[q] = vnext[q];
@@ -468,6 +479,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.nchunks = (t_end - t_begin + p.chunk - 1) / p.chunk;
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;
+    p.hints = g_tma_hints;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
     k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     note_kernel(std::string("k_nn_tma<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(nx) + "x" +
