@@ -238,3 +238,17 @@ def test_deterministic_across_calls():
     first = kernels.mult_su3_na(U[:, 0], U[:, 1])
     second = kernels.mult_su3_na(U[:, 0], U[:, 1])
     assert np.array_equal(first, second)
+
+
+def test_c_host_program_on_the_gpu(tmp_path):
+    """The plain-C ABI demo on device memory: identity links return v; the NN sweep of a constant field is 0."""
+    import subprocess
+    import sys
+
+    sys.path.insert(0, __import__("os").path.dirname(__file__))
+    from test_host import _build_c_demo
+
+    exe = _build_c_demo(tmp_path)
+    r = subprocess.run([str(exe), "gpu"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "abi_demo: ok (gpu)" in r.stdout

@@ -289,3 +289,30 @@ def test_p2p_abi_argument_checks():
     assert lib.su3g_p2p_prime_f64(None, None, 4, 4, 4, 4, None, None, None, 0, 0, None) == _lib.SU3G_EINVAL
     assert lib.su3g_ipc_get_handle(None, None) == _lib.SU3G_EINVAL
     assert lib.su3g_ipc_close(None) == _lib.SU3G_OK
+
+
+def _build_c_demo(tmp_path):
+    """Compile tests/c/abi_demo.c as plain C11 against include/su3g.h and libsu3g.so."""
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    exe = tmp_path / "abi_demo"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    cmd = [cc, "-std=c11", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tests", "c", "abi_demo.c"), "-o", str(exe), "-L", libdir, "-lsu3g",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{libdir}", "-Wl,-rpath,/usr/local/cuda/lib64"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_host_program_against_the_abi(tmp_path):
+    """A C program (no Python, no torch) includes su3g.h, links libsu3g.so and exercises the ABI."""
+    import subprocess
+
+    exe = _build_c_demo(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    assert "abi_demo: ok" in r.stdout
