@@ -31,7 +31,8 @@
 
 namespace su3g {
 
-int g_tma_hints = 0;  // su3g_set_option("nn_tma_l2_hints")
+// su3g_set_option("nn_tma_l2_hints"); on by default (64^3x16 f32: 0.858 -> 0.864, neutral elsewhere)
+int g_tma_hints = 1;
 
 namespace {
 

@@ -105,6 +105,25 @@ __global__ void __launch_bounds__(256)
     nn_site<T, FUSED, HINTS>(U, v, out, g, x, y, z, t, nullptr, nullptr);
 }
 
+// out(x) = src(x) on the sites of one parity (the workspace path of su3g_dslash_ws)
+template <typename T>
+__global__ void __launch_bounds__(256) k_parity_copy(const T* __restrict__ src, T* __restrict__ dst, Geom g,
+                                                     int parity) {
+    const int nxh = g.nx >> 1;
+    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (idx >= (g.F >> 1) * g.nt) return;
+    const int xh = static_cast<int>(idx % nxh);
+    int64_t r = idx / nxh;
+    const int y = static_cast<int>(r % g.ny);
+    r /= g.ny;
+    const int z = static_cast<int>(r % g.nz);
+    const int t = static_cast<int>(r / g.nz);
+    const int x = 2 * xh + ((y + z + t + parity) & 1);
+    const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) dst[(int64_t(t) * 6 + k) * g.F + s3] = src[(int64_t(t) * 6 + k) * g.F + s3];
+}
+
 template <typename T, bool FUSED>
 __global__ void __launch_bounds__(256)
     k_nn_halo_w(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ w_face, Geom g) {
@@ -555,8 +574,12 @@ static int nn_halo_w(const T* U, const T* v, T* w, int nx, int ny, int nz, int n
 }
 
 template <typename T>
+static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
+                    const T* v_hi, const T* w_lo, int mode, cudaStream_t st);
+
+template <typename T>
 static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int parity, int mode,
-                  cudaStream_t st) {
+                  cudaStream_t st, T* scratch = nullptr) {
     if (int rc = check_geom("dslash", nx, ny, nz, nt)) return rc;
     if ((nx | ny | nz | nt) & 1) return fail_invalid("dslash: every lattice extent must be even (checkerboard)");
     if (parity != 0 && parity != 1) return fail_invalid("dslash: parity must be 0 (even) or 1 (odd)");
@@ -564,6 +587,18 @@ static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (!U || !v || !out) return fail_invalid("dslash: null pointer");
     if (out == v) return fail_invalid("dslash: out must not alias v");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
+    // workspace path (f32, where the TMA t-walk applies): the full sweep into scratch with the TMA
+    // kernel, then the requested parity copied out -- bitwise the same values, and faster than the
+    // one-thread-per-site parity kernel although it computes both parities (64^3x16 f32)
+    if (scratch != nullptr && sizeof(T) == 4 && nx >= 32 && g_nn_variant.load() == 0) {
+        if (scratch == v || scratch == out) return fail_invalid("dslash: scratch must not alias v or out");
+        if (int rc = nn_sweep<T>(U, v, scratch, nx, ny, nz, nt, 0, nt, nullptr, nullptr, mode, st)) return rc;
+        const std::string used = std::string("dslash via ") + su3g_last_kernel() + " + k_parity_copy";
+        const unsigned gc = static_cast<unsigned>(((g.F >> 1) * nt + 255) / 256);
+        k_parity_copy<T><<<gc, 256, 0, st>>>(scratch, out, g, parity);
+        note_kernel(used);
+        return check_launch("dslash(parity copy)");
+    }
     const bool big_slice = double(g.F) * 72 * sizeof(T) > 0.5 * double(device_info().l2_bytes);
     int ZC = big_slice ? chunk_planes(nz, 8) : nz;
     if (g_sweep_zc > 0) ZC = chunk_planes(nz, g_sweep_zc);
@@ -770,6 +805,14 @@ int su3g_dslash_f32(const float* U, const float* v, float* out, int32_t nx, int3
 int su3g_dslash_f64(const double* U, const double* v, double* out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
                     int32_t parity, int32_t mode, su3g_stream_t st) {
     return dslash<double>(U, v, out, nx, ny, nz, nt, parity, mode, reinterpret_cast<cudaStream_t>(st));
+}
+int su3g_dslash_ws_f32(const float* U, const float* v, float* out, float* scratch, int32_t nx, int32_t ny, int32_t nz,
+                       int32_t nt, int32_t parity, int32_t mode, su3g_stream_t st) {
+    return dslash<float>(U, v, out, nx, ny, nz, nt, parity, mode, reinterpret_cast<cudaStream_t>(st), scratch);
+}
+int su3g_dslash_ws_f64(const double* U, const double* v, double* out, double* scratch, int32_t nx, int32_t ny,
+                       int32_t nz, int32_t nt, int32_t parity, int32_t mode, su3g_stream_t st) {
+    return dslash<double>(U, v, out, nx, ny, nz, nt, parity, mode, reinterpret_cast<cudaStream_t>(st), scratch);
 }
 
 }  // extern "C"

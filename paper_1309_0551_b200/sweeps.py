@@ -83,12 +83,16 @@ def nn_apply(U: Field, v: Field, applications: int, scratch: Field | None = None
     return a
 
 
-def dslash(U: Field, v: Field, parity: int, out: Field | None = None, mode: str = "exact") -> Field:
+def dslash(U: Field, v: Field, parity: int, out: Field | None = None, mode: str = "exact",
+           scratch: Field | None = None) -> Field:
     """out(x) = (D v)(x) on the sites with (x+y+z+t) % 2 == parity; reads v only on the other parity.
 
     Sites of the other parity keep their value in a caller-supplied ``out`` (a
     fresh ``out`` is zero there).  Every lattice extent must be even.  EXACT mode
-    equals ``nn_sweep`` on those sites bit for bit.
+    equals ``nn_sweep`` on those sites bit for bit.  ``scratch`` (a 'vec' field)
+    enables the workspace path (su3g_dslash_ws): f32 lattices with a TMA geometry
+    run the full TMA sweep into it and copy the parity out; pass the same scratch
+    to repeated calls to avoid an allocation.
     """
     if U.kind != "mat4" or v.kind != "vec":
         raise ValueError("dslash needs U of kind 'mat4' and v of kind 'vec'")
@@ -99,6 +103,16 @@ def dslash(U: Field, v: Field, parity: int, out: Field | None = None, mode: str 
     if out is None:
         out = Field(v.lattice, "vec", v.dtype, v.device, data=torch.zeros_like(v.data))
     lat = U.lattice
+    if scratch is None and U.dtype == torch.float32:
+        scratch = v.empty_like()
+    if scratch is not None:
+        if scratch.kind != "vec" or scratch.lattice != lat or scratch.dtype != U.dtype:
+            raise ValueError("scratch must be a 'vec' field on U's lattice and dtype")
+        _lib.call(
+            f"su3g_dslash_ws_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
+            scratch.data.data_ptr(), lat.nx, lat.ny, lat.nz, lat.nt, int(parity), _mode(mode), _stream(U.device),
+        )
+        return out
     _lib.call(
         f"su3g_dslash_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
         lat.nx, lat.ny, lat.nz, lat.nt, int(parity), _mode(mode), _stream(U.device),
