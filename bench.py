@@ -856,7 +856,7 @@ def run_reference(args, rank, world):
     threads = os.cpu_count() or 1
     fn, sites, state, desc = _cpu_sample(cfg, args.dtype, small=True)
     call = (lambda: _parallel_nn(state, threads)) if cfg["kind"] in ("nn", "dslash") else fn
-    if cfg["kind"] != "nn":
+    if cfg["kind"] not in ("nn", "dslash"):
         threads = 1
     for _ in range(args.warmup):
         call()
