@@ -508,7 +508,21 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if ((nx * int(sizeof(T))) % 16 != 0 || nx > 256) return 1;
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
     int BY = 0, BZ = 0;
-    if (!tma_shape(nx, ny, nz, NTHR, BY, BZ)) return 1;
+    if (!tma_shape(nx, ny, nz, NTHR, BY, BZ)) {
+        // x extents that do not divide 256 (48, 24, 96, 40, 80, ...): runtime geometries with
+        // 192- or 160-site blocks, so these lattices still get the TMA walk (one CTA per SM)
+        if constexpr (sizeof(T) == 4) {
+            if (tma_shape(nx, ny, nz, 192, BY, BZ))
+                return mode == SU3G_FMA
+                           ? run_tma<T, true, 192, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
+                           : run_tma<T, false, 192, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+            if (tma_shape(nx, ny, nz, 160, BY, BZ))
+                return mode == SU3G_FMA
+                           ? run_tma<T, true, 160, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
+                           : run_tma<T, false, 160, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+        }
+        return 1;
+    }
     if constexpr (sizeof(T) == 4) {  // the production geometries, specialised
         if (nx == 32 && BY == 2 && BZ == 4 && ny > 2 && nz > 4)
             return mode == SU3G_FMA

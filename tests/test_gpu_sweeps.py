@@ -450,3 +450,23 @@ def test_generic_kernel_knobs_keep_results_bitwise(option, value, default, preci
     finally:
         _lib.set_option(option, default)
         _lib.set_option("nn_variant", 0)
+
+
+@pytest.mark.parametrize("dims", [(48, 4, 4, 6), (24, 8, 4, 5), (40, 4, 2, 3), (96, 2, 2, 4), (12, 16, 4, 3)])
+def test_tma_runtime_geometries_for_x_extents_not_dividing_256(dims):
+    """192/160-site runtime TMA geometries: bitwise vs the oracle, and the TMA kernel is the one dispatched."""
+    from paper_1309_0551_b200 import _lib
+
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(9200 + V)
+    U = inputs.random_links(rng, V, 4, dtype=np.float32)
+    v = inputs.random_vectors(rng, V, None, dtype=np.float32)
+    got = sweeps.nn_sweep_aos(U, v, dims)
+    assert np.array_equal(got, coracle.nn_sweep(U, v, dims))
+    lat = Lattice4D(*dims)
+    Uf, vf = Field.from_aos(lat, "mat4", U), Field.from_aos(lat, "vec", v)
+    sweeps.nn_sweep(Uf, vf)
+    assert "k_nn_tma" in _lib.last_kernel(), _lib.last_kernel()
+    # 3 applications through the same kernel, and FMA within tolerance
+    assert np.array_equal(sweeps.nn_sweep_aos(U, v, dims, applications=3), coracle.nn_sweep_iterated(U, v, dims, 3))
+    assert floored_rel_err(sweeps.nn_sweep_aos(U, v, dims, mode="fma"), coracle.nn_sweep(U, v, dims)) <= 1e-5
