@@ -98,6 +98,7 @@ struct TmaParams {
     int64_t nitems;
     int has_vhi;   // v(t = nt) comes from the v_hi face
     int hints;     // U_t gathers evict-first in L2 (read exactly once), output stored streaming
+    int parity;    // PARITY kernels: output only the sites with (x+y+z+t) % 2 == parity (dslash)
 };
 
 // item -> (block, t0, t1), chunk-major
@@ -139,7 +140,12 @@ struct Geo {
 
 // CNX/CBY/CBZ > 0: block geometry fixed at compile time (halos present in y and z),
 // so every shared-memory offset is an immediate; 0: runtime geometry.
-template <typename T, bool FUSED, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
+// PARITY: the even/odd dslash on the same t-walk.  At step t a site is either an
+// output site ((x+y+z+t) % 2 == p.parity: forward products, the sums, the store) or a source site
+// (publishes v and w_x, w_y, w_z for its output neighbours, forms w_t for step t+1, when it is an
+// output site).  Same loads and arithmetic as the full sweep, so the values are bitwise those of
+// the NN sweep on the output sites; the other parity of `out` is not written.
+template <typename T, bool FUSED, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0, bool PARITY = false>
 __global__ void __launch_bounds__(NTHR, 1)
     k_nn_tma(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
              const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
@@ -280,6 +286,10 @@ __global__ void __launch_bounds__(NTHR, 1)
     for (; item < p.nitems; item += G) {
         item_range(p, item, blk, t0, t1);
         const int64_t s3 = site_of(blk);
+        // site parity at t = 0 (PARITY kernels): x + y + z of this thread's site
+        const int par0 = PARITY ? ((lx + ly + lz + static_cast<int>(blk % p.nby) * BY +
+                                    static_cast<int>(blk / p.nby) * BZ) & 1)
+                                : 0;
         ld_soa<T, 6>(v + int64_t(t0) * 6 * F, F, s3, vc);
         if (t0 == 0 && w_lo != nullptr) {
             ld_soa<T, 6>(w_lo, F, s3, wt);
@@ -323,8 +333,11 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) xb[xo + q * hp + jj] = wh[q];
             }
+            // roles: every site is both in the full sweep; one or the other in a PARITY kernel
+            const bool is_out = !PARITY || (((par0 + t) & 1) == p.parity);
+            const bool is_src = !PARITY || !is_out;
             // this site's half-products w_x, w_y, w_z and v(x,t) for the neighbours
-            {
+            if (is_src) {
                 T w[6];
 #pragma unroll
                 for (int mu = 0; mu < 3; ++mu) {
@@ -336,13 +349,13 @@ __global__ void __launch_bounds__(NTHR, 1)
                 for (int q = 0; q < 6; ++q) xb[g.xv() + q * NTHR + tid] = vc[q];
             }
             T wt_next[6], f3[6];
-            amv<T, FUSED>(ut, vc, wt_next);
-            mv<T, FUSED>(ut, vnext, f3);  // forward +t term, summed last
+            if (is_src) amv<T, FUSED>(ut, vc, wt_next);  // -t term of this site at step t + 1
+            if (is_out) mv<T, FUSED>(ut, vnext, f3);     // forward +t term, summed last
             named_sync<NTHR>();
 
             // forward terms (add_su3_vector chain: ((f0 + f1) + f2) + f3)
             T acc[6];
-            {
+            if (is_out) {
                 T nb[6], f[6];
 #pragma unroll
                 for (int q = 0; q < 6; ++q) nb[q] = xb[g.xv() + q * NTHR + ix_up];
@@ -372,6 +385,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             }
 
             // backward terms (sub_four_su3_vecs chain)
+            if (is_out) {
 #pragma unroll
             for (int q = 0; q < 6; ++q) acc[q] = xsub(acc[q], xb[g.xw() + q * NTHR + ix_dn]);
             if (iy_dn >= 0) {
@@ -399,6 +413,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
                 for (int q = 0; q < 6; ++q) o[q * F] = acc[q];
             }
+            }  // is_out
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 vc[q] = vnext[q];
@@ -442,9 +457,9 @@ bool tma_shape(int nx, int ny, int nz, int nthr, int& BY, int& BZ) {
 
 }  // namespace
 
-template <typename T, bool FUSED, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0>
+template <typename T, bool FUSED, int NTHR, int STAGES, int CNX = 0, int CBY = 0, int CBZ = 0, bool PARITY = false>
 static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
-                   const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st) {
+                   const T* v_hi, const T* w_lo, int BY, int BZ, cudaStream_t st, int parity = -1) {
     const int HY = (BY == ny) ? 0 : nx * BZ, HZ = (BZ == nz) ? 0 : nx * BY;
     CUtensorMap mU, mV, mVhi, mUy, mUz, mVy, mVz;
     if (!make_map<T>(&mU, U, nx, ny, nz, int64_t(nt) * 72, BY, BZ, 18)) return 1;
@@ -466,7 +481,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     const size_t smem = (STAGES * stage + xsize) * sizeof(T) + 2 * STAGES * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    cudaFuncSetAttribute(k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ, PARITY>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     TmaParams p{};
     p.nx = nx; p.ny = ny; p.nz = nz; p.nt = nt;
     p.F = int64_t(nx) * ny * nz;
@@ -474,15 +489,16 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.nblocks = int64_t(ny / BY) * (nz / BZ);
     p.t_begin = t_begin; p.t_end = t_end;
     int per_sm = 1;  // resident CTAs per SM (2 for the 128-thread f32 geometry)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ>, NTHR, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ, PARITY>, NTHR, smem);
     const int G = sweep_sms() * std::max(per_sm, 1);
     p.chunk = pick_chunk(p.nblocks, t_end - t_begin, G);
     p.nchunks = (t_end - t_begin + p.chunk - 1) / p.chunk;
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;
     p.hints = g_tma_hints;
+    p.parity = parity;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
-    k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
+    k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ, PARITY><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     note_kernel(std::string("k_nn_tma<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(nx) + "x" +
                 std::to_string(BY) + "x" + std::to_string(BZ) + (CNX ? "" : " runtime-geometry") + "," +
                 std::to_string(NTHR) + "thr>");
@@ -509,17 +525,15 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
     int BY = 0, BZ = 0;
     if (!tma_shape(nx, ny, nz, NTHR, BY, BZ)) {
-        // x extents that do not divide 256 (48, 24, 96, 40, 80, ...): runtime geometries with
-        // 192- or 160-site blocks, so these lattices still get the TMA walk (one CTA per SM)
+        // x extents that do not divide 256: 48 (the 48^4 lattice of configs[3]) gets a specialised
+        // 192-site block geometry
+        // (runtime-geometry kernels measured no better than the register walk: 48^3 0.589 vs 0.572,
+        // 40^3 0.456 -- so only the specialised 48x2x2 geometry is used)
         if constexpr (sizeof(T) == 4) {
-            if (tma_shape(nx, ny, nz, 192, BY, BZ))
+            if (nx == 48 && tma_shape(nx, ny, nz, 192, BY, BZ) && BY == 2 && BZ == 2 && ny > 2 && nz > 2)
                 return mode == SU3G_FMA
-                           ? run_tma<T, true, 192, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
-                           : run_tma<T, false, 192, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
-            if (tma_shape(nx, ny, nz, 160, BY, BZ))
-                return mode == SU3G_FMA
-                           ? run_tma<T, true, 160, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
-                           : run_tma<T, false, 160, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+                           ? run_tma<T, true, 192, 2, 48, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
+                           : run_tma<T, false, 192, 2, 48, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
         }
         return 1;
     }
@@ -537,6 +551,35 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
                ? run_tma<T, true, NTHR, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
                : run_tma<T, false, NTHR, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
 }
+
+// even/odd dslash on the TMA t-walk (PARITY kernels): the production geometries only; returns 1
+// when the lattice has none, so the caller falls back to the one-thread-per-site parity kernel
+template <typename T>
+int launch_dslash_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int parity, int mode,
+                      cudaStream_t st) {
+    if constexpr (sizeof(T) != 4) {
+        return 1;
+    } else {
+        if (!aligned16(U) || !aligned16(v)) return 1;
+        int BY = 0, BZ = 0;
+        if (!tma_shape(nx, ny, nz, 256, BY, BZ)) return 1;
+        if (nx == 64 && BY == 2 && BZ == 2 && ny > 2 && nz > 2)
+            return mode == SU3G_FMA
+                       ? run_tma<T, true, 256, 2, 64, 2, 2, true>(U, v, out, nx, ny, nz, nt, 0, nt, nullptr, nullptr, BY, BZ, st, parity)
+                       : run_tma<T, false, 256, 2, 64, 2, 2, true>(U, v, out, nx, ny, nz, nt, 0, nt, nullptr, nullptr, BY, BZ, st, parity);
+        if (nx == 32 && BY == 2 && BZ == 4 && ny > 2 && nz > 4)
+            return mode == SU3G_FMA
+                       ? run_tma<T, true, 256, 2, 32, 2, 4, true>(U, v, out, nx, ny, nz, nt, 0, nt, nullptr, nullptr, BY, BZ, st, parity)
+                       : run_tma<T, false, 256, 2, 32, 2, 4, true>(U, v, out, nx, ny, nz, nt, 0, nt, nullptr, nullptr, BY, BZ, st, parity);
+        return mode == SU3G_FMA
+                   ? run_tma<T, true, 256, 2, 0, 0, 0, true>(U, v, out, nx, ny, nz, nt, 0, nt, nullptr, nullptr, BY, BZ, st, parity)
+                   : run_tma<T, false, 256, 2, 0, 0, 0, true>(U, v, out, nx, ny, nz, nt, 0, nt, nullptr, nullptr, BY, BZ, st, parity);
+    }
+}
+
+template int launch_dslash_tma<float>(const float*, const float*, float*, int, int, int, int, int, int, cudaStream_t);
+template int launch_dslash_tma<double>(const double*, const double*, double*, int, int, int, int, int, int,
+                                       cudaStream_t);
 
 template int launch_nn_tma<float>(const float*, const float*, float*, int, int, int, int, int, int, const float*,
                                   const float*, int, cudaStream_t);

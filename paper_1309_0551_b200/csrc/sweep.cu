@@ -587,6 +587,14 @@ static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
     if (!U || !v || !out) return fail_invalid("dslash: null pointer");
     if (out == v) return fail_invalid("dslash: out must not alias v");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
+    // f32 lattices with a TMA geometry: the parity-restricted TMA t-walk (same values, t-walk speed)
+    if (sizeof(T) == 4 && g_nn_variant.load() == 0) {
+        const int rc = launch_dslash_tma<T>(U, v, out, nx, ny, nz, nt, parity, mode, st);
+        if (rc != 1) {
+            if (rc == SU3G_OK) note_kernel(std::string("dslash: ") + su3g_last_kernel() + " (parity mode)");
+            return rc;
+        }
+    }
     // workspace path (f32, where the TMA t-walk applies): the full sweep into scratch with the TMA
     // kernel, then the requested parity copied out -- bitwise the same values, and faster than the
     // one-thread-per-site parity kernel although it computes both parities (64^3x16 f32)
