@@ -530,10 +530,10 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
         // (runtime-geometry kernels measured no better than the register walk: 48^3 0.589 vs 0.572,
         // 40^3 0.456 -- so only the specialised 48x2x2 geometry is used)
         if constexpr (sizeof(T) == 4) {
-            if (nx == 48 && tma_shape(nx, ny, nz, 192, BY, BZ) && BY == 2 && BZ == 2 && ny > 2 && nz > 2)
+            if (nx == 48 && ny % 2 == 0 && nz % 2 == 0 && ny > 2 && nz > 2)
                 return mode == SU3G_FMA
-                           ? run_tma<T, true, 192, 2, 48, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st)
-                           : run_tma<T, false, 192, 2, 48, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, BY, BZ, st);
+                           ? run_tma<T, true, 192, 2, 48, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, 2, 2, st)
+                           : run_tma<T, false, 192, 2, 48, 2, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, 2, 2, st);
         }
         return 1;
     }
