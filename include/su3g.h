@@ -63,7 +63,7 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *                   6 generic capped at 3 CTAs/SM worth of registers (A/B)
  *   "link_variant": 0 auto (= 6), 1 generic one-thread-per-site, 2 block walk, 3 cp.async ring,
  *                   4 plane-split, 5 generic in plain t-major order (A/B), 6 low-register rows
- *                   (accumulator in smem)
+ *                   (accumulator in smem), 7 TMA-staged site tiles (3 threads per site)
  *   "link_minb":    CTAs/SM the rows kernel's register budget targets: 0 default (f64: 4 exact,
  *                   3 FMA; f32: 6), 3, 4, 5, 6 or 8
  *   "link_prefetch_b": 1 = the rows kernel gathers the next plane's U_nu(x+mu) during this plane (A/B)

@@ -677,6 +677,12 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     int ZC = link_chunk ? chunk_planes(nz, 16) : nz;
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
     if (g_link_zc > 0) ZC = chunk_planes(nz, g_link_zc);  // A/B knob: z-planes per chunk
+    if (lv == 7) {  // TMA-staged site tiles (A/B)
+        const int rc = mode == SU3G_FMA ? launch_link_tile<T, true>(U, acc, g, s, st)
+                                        : launch_link_tile<T, false>(U, acc, g, s, st);
+        if (rc != 1) return rc;
+        return fail_invalid("link_product: tile kernel not applicable to this lattice");
+    }
     // default (auto) = the low-register rows kernel: 16 warps/SM instead of 8 for f64
     // (48^4 f64, same box: exact 0.323 -> 0.426 of HBM, FMA 0.406 -> 0.465)
     if (lv == 0 || lv == 6) {
@@ -768,10 +774,10 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 6)
+        if (value < 0 || value > 7)
             return fail_invalid(
                 "set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring), 4 (planes), "
-                "5 (generic, natural order), 6 (low-register rows = auto)");
+                "5 (generic, natural order), 6 (low-register rows = auto), 7 (TMA site tiles)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -95,11 +95,12 @@ def test_link_product_config3_full_size():
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
     from paper_1309_0551_b200 import _lib
 
-    _lib.set_option("link_variant", 6)  # low-register rows kernel at full size (z-chunked order)
-    try:
-        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
-    finally:
-        _lib.set_option("link_variant", 0)
+    for variant in (6, 7):  # low-register rows (z-chunked order); TMA site tiles
+        _lib.set_option("link_variant", variant)
+        try:
+            assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+        finally:
+            _lib.set_option("link_variant", 0)
 
 
 @pytest.mark.parametrize("C", [6, 18, 24, 72])
@@ -244,9 +245,11 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
 
 
 @pytest.mark.parametrize(
-    "variant", [0, 1, 2, 3, 4, 6], ids=["auto", "generic", "block-walk", "ring", "planes", "rows"]
+    "variant", [0, 1, 2, 3, 4, 6, 7], ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile"]
 )
-@pytest.mark.parametrize("dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97)])
+@pytest.mark.parametrize(
+    "dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97), (16, 8, 4, 6), (8, 4, 2, 3)]
+)
 def test_link_product_variants_bitwise(variant, dims, precision):
     from paper_1309_0551_b200 import _lib
 
