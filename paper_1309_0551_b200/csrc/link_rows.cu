@@ -41,6 +41,29 @@ __device__ __forceinline__ void ld_link_part(const T* __restrict__ U, const Geom
     ld_soa<T, N>(U + (t * 72 + mu * 18 + c0) * g.F, g.F, s3, r);
 }
 
+// L1 eviction priorities for the L1HINT kernels: A (re-read in up to three planes) evict-last,
+// the single-use B/C gathers no-allocate
+__device__ __forceinline__ double ld_l1(const double* p, int keep) {
+    double r;
+    if (keep) asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    else asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float ld_l1(const float* p, int keep) {
+    float r;
+    if (keep) asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    return r;
+}
+template <typename T, int N>
+__device__ __forceinline__ void ld_part_l1(const T* __restrict__ U, const Geom& g, int64_t site, int mu, int c0, T* r,
+                                           int keep) {
+    const int64_t t = site / g.F, s3 = site - t * g.F;
+    const T* p = U + (t * 72 + mu * 18 + c0) * g.F + s3;
+#pragma unroll
+    for (int k = 0; k < N; ++k) r[k] = ld_l1(p + k * g.F, keep);
+}
+
 template <typename T, bool FUSED, int MODE, class PF, class QF>
 __device__ __forceinline__ void dot3(PF p, QF q, T& re, T& im) {
     if constexpr (FUSED) cdot_fma<T, MODE, 3>(p, q, re, im);
@@ -49,7 +72,7 @@ __device__ __forceinline__ void dot3(PF p, QF q, T& re, T& im) {
 
 }  // namespace
 
-template <typename T, bool FUSED, int MINB, bool EARLY_C, bool PREF_B, bool HINTS = false>
+template <typename T, bool FUSED, int MINB, bool EARLY_C, bool PREF_B, bool HINTS = false, bool L1HINT = false>
 __global__ void __launch_bounds__(128, MINB)
     k_link_rows(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC, int ahead) {
     // HINTS: in the (z-chunk, t, z, y, x) order a link's last reader is: U_mu(y), mu < 3, its own site's
@@ -93,6 +116,8 @@ __global__ void __launch_bounds__(128, MINB)
                 if (HINTS && pl == 2) {
                     const int64_t nb = shifted(g, x, y, z, t, mu), tn = nb / g.F;
                     ld_soa_last<T, 18>(U + (tn * 72 + nu * 18) * g.F, g.F, nb - tn * g.F, b, pol);
+                } else if (L1HINT) {
+                    ld_part_l1<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b, 0);
                 } else {
                     ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b);  // B = U_nu(x + mu)
                 }
@@ -102,6 +127,8 @@ __global__ void __launch_bounds__(128, MINB)
                 T a[6];
                 if (HINTS && (pl == 2 || pl == 4 || pl == 5))
                     ld_soa_last<T, 6>(U + (int64_t(t) * 72 + mu * 18 + 6 * i) * g.F, g.F, s3, a, pol);
+                else if (L1HINT)
+                    ld_part_l1<T, 6>(U, g, site, mu, 6 * i, a, 1);
                 else
                     ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
 #pragma unroll
@@ -115,7 +142,10 @@ __global__ void __launch_bounds__(128, MINB)
             if (pl < 5)
                 ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, c_plane_mu[pl + 1]), c_plane_nu[pl + 1], 0, bn);
         }
-        if constexpr (!EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);  // C = U_mu(x + nu)
+        if constexpr (!EARLY_C) {
+            if constexpr (L1HINT) ld_part_l1<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c, 0);
+            else ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);  // C = U_mu(x + nu)
+        }
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -142,7 +172,8 @@ __global__ void __launch_bounds__(128, MINB)
 
 int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
 int g_link_early_c = -1;  // su3g_set_option("link_early_c"): gather C together with B (-1 = default)
-int g_link_hints = 0;     // su3g_set_option("link_l2_hints"): last-use gathers evict-first (A/B)
+int g_link_hints = 0;
+int g_link_l1_hints = 0;  // su3g_set_option("link_l1_hints"): A evict-last in L1, B/C no-allocate (A/B)     // su3g_set_option("link_l2_hints"): last-use gathers evict-first (A/B)
 int g_link_pref_b = 0;    // su3g_set_option("link_prefetch_b"): gather the next plane's B during this plane
 extern int g_sweep_prefetch;
 
@@ -170,7 +201,11 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     const int ahead = (g_sweep_prefetch > 0 && (int64_t(g.nx) * g.ny) % 128 == 0 && aligned16(U))
                           ? std::max(1, minb * device_info().num_sms * g_sweep_prefetch / 4)
                           : 0;
-    if (g_link_hints && !g_link_pref_b) {
+    if (g_link_l1_hints && !g_link_pref_b) {
+        constexpr int MB = sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6;
+        if (early_c) k_link_rows<T, FUSED, MB, true, false, false, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead);
+        else k_link_rows<T, FUSED, MB, false, false, false, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead);
+    } else if (g_link_hints && !g_link_pref_b) {
         if (early_c) k_link_rows<T, FUSED, sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6, true, false, true>
                          <<<grid, 128, 0, st>>>(U, acc, g, s, ZC, ahead);
         else k_link_rows<T, FUSED, sizeof(T) == 8 ? (FUSED ? 3 : 4) : 6, false, false, true>

@@ -29,6 +29,7 @@ int g_sweep_prefetch = 0;  // su3g_set_option("sweep_prefetch"): L2 prefetch dis
 extern int g_link_early_c;
 extern int g_link_pref_b;
 extern int g_link_hints;
+extern int g_link_l1_hints;
 extern int g_tma_hints;
 
 // ---------------------------------------------------------------------------
@@ -736,6 +737,11 @@ int su3g_set_option(const char* name, int64_t value) {
     if (std::strcmp(name, "nn_tma_l2_hints") == 0) {
         if (value != 0 && value != 1) return fail_invalid("set_option: nn_tma_l2_hints must be 0 or 1");
         g_tma_hints = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "link_l1_hints") == 0) {
+        if (value != 0 && value != 1) return fail_invalid("set_option: link_l1_hints must be 0 or 1");
+        g_link_l1_hints = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_l2_hints") == 0) {

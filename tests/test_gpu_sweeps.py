@@ -429,7 +429,7 @@ def test_dslash_argument_errors():
 
 
 @pytest.mark.parametrize("option,value,default", [("sweep_l2_hints", 0, 1), ("sweep_prefetch", 1, 0),
-                                                  ("link_l2_hints", 1, 0)])
+                                                  ("link_l2_hints", 1, 0), ("link_l1_hints", 1, 0)])
 def test_generic_kernel_knobs_keep_results_bitwise(option, value, default, precision):
     """Cache-hint / prefetch knobs of the one-thread-per-site kernels never change a bit."""
     from paper_1309_0551_b200 import _lib
