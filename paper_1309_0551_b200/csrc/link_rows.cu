@@ -45,14 +45,14 @@ __device__ __forceinline__ void ld_link_part(const T* __restrict__ U, const Geom
 // the single-use B/C gathers no-allocate
 __device__ __forceinline__ double ld_l1(const double* p, int keep) {
     double r;
-    if (keep) asm volatile("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(r) : "l"(p));
-    else asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    if (keep) asm("ld.global.nc.L1::evict_last.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    else asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
     return r;
 }
 __device__ __forceinline__ float ld_l1(const float* p, int keep) {
     float r;
-    if (keep) asm volatile("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(r) : "l"(p));
-    else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    if (keep) asm("ld.global.nc.L1::evict_last.f32 %0, [%1];" : "=f"(r) : "l"(p));
+    else asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
     return r;
 }
 template <typename T, int N>

@@ -10,6 +10,7 @@ namespace su3g {
 
 // One site of the NN sweep: out(x) = sum_mu U_mu(x) v(x+mu) - sum_mu U_mu(x-mu)^dag v(x-mu), association of
 // the composed reference (add_su3_vector chain, then sub_four_su3_vecs).  v_hi / w_lo: t-slab halos (or null).
+// (non-volatile asm: the loads have no side effects, so the compiler may batch and hoist them)
 // L2 eviction hints (HINTS): in the one-thread-per-site visiting orders every link is read
 // twice -- first as a site's own forward link, last as the next site's backward link --
 // so the backward gathers are marked evict-first (their line has no further use) and the
@@ -21,12 +22,12 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 }
 __device__ __forceinline__ float ld_hint(const float* p, uint64_t pol) {
     float r;
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
     return r;
 }
 __device__ __forceinline__ double ld_hint(const double* p, uint64_t pol) {
     double r;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
     return r;
 }
 template <typename T, int N>
