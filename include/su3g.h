@@ -73,6 +73,7 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "sweep_l2_hints": 1 (default) = the one-thread-per-site NN / dslash kernels load backward
  *                   (last-use) links and v(t-1) evict-first in L2 and store their output streaming
  *   "nn_tma_l2_hints": 1 = the TMA NN kernel gathers U_t evict-first and stores streaming (A/B)
+ *   "sweep_l2_keep": 1 = the generic NN kernel also loads each site's own links evict-last (A/B)
  *   "link_l1_hints": 1 = the link rows kernel loads A evict-last in L1 and B/C no-allocate (A/B)
  *   "link_l2_hints": 1 = the link rows kernel marks each link's last-use gather evict-first (A/B;
  *                   default register targets only)

@@ -36,19 +36,27 @@ __device__ __forceinline__ void ld_soa_last(const T* __restrict__ p, int64_t F, 
     for (int k = 0; k < N; ++k) r[k] = ld_hint(p + k * F + s3, pol);
 }
 
-template <typename T, bool FUSED, bool HINTS = false>
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <typename T, bool FUSED, bool HINTS = false, bool KEEP = false>
 __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
                                         const Geom& g, int x, int y, int z, int t, const T* __restrict__ v_hi,
                                         const T* __restrict__ w_lo) {
     const int64_t F = g.F;
     const uint64_t pol = HINTS ? l2_evict_first_policy() : 0;
+    const uint64_t keep = KEEP ? l2_evict_last_policy() : 0;  // own links: first of their two reads
     const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
     T acc[6];
     // forward terms, mu = 0..3, summed left to right (add_su3_vector chain)
 #pragma unroll
     for (int mu = 0; mu < 4; ++mu) {
         T u[18], vn[6], f[6];
-        ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, s3, u);
+        if constexpr (KEEP) ld_soa_last<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, s3, u, keep);
+        else ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, s3, u);
         if (mu < 3) {
             ld_soa<T, 6>(v + int64_t(t) * 6 * F, F, step3(g, x, y, z, mu, +1), vn);
         } else if (t + 1 < g.nt) {

@@ -25,6 +25,7 @@ int g_sweep_zc = 0;  // su3g_set_option("sweep_zc"): z-planes per chunk of the g
 // su3g_set_option("sweep_l2_hints"): evict-first backward gathers, streaming stores.  Default on:
 // f64 64^3x16 0.686 -> 0.736 of HBM, 32^4 0.711 -> 0.777, dslash f64 0.569 -> 0.642 (same box A/B)
 int g_sweep_hints = 1;
+int g_sweep_keep = 0;      // su3g_set_option("sweep_l2_keep"): own-link loads evict-last (A/B)
 int g_sweep_prefetch = 0;  // su3g_set_option("sweep_prefetch"): L2 prefetch distance in quarter waves (0 = off)
 extern int g_link_early_c;
 extern int g_link_pref_b;
@@ -35,7 +36,7 @@ extern int g_tma_hints;
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
 // ---------------------------------------------------------------------------
-template <typename T, bool FUSED, bool HINTS = false>
+template <typename T, bool FUSED, bool HINTS = false, bool KEEP = false>
 __device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
                                               const Geom& g, int t_begin, int t_end, const T* __restrict__ v_hi,
                                               const T* __restrict__ w_lo, int ZC, int ahead = 0) {
@@ -56,15 +57,15 @@ __device__ __forceinline__ void nn_sweep_body(const T* __restrict__ U, const T* 
     r /= ZC;
     const int t = t_begin + static_cast<int>(r % nts);
     const int z = static_cast<int>(r / nts) * ZC + zl;
-    nn_site<T, FUSED, HINTS>(U, v, out, g, x, y, z, t, v_hi, w_lo);
+    nn_site<T, FUSED, HINTS, KEEP>(U, v, out, g, x, y, z, t, v_hi, w_lo);
 }
 
 // plain bounds: ptxas picks 64-98 registers; an explicit minBlocks of 1 would let it take 252
-template <typename T, bool FUSED, bool HINTS = false>
+template <typename T, bool FUSED, bool HINTS = false, bool KEEP = false>
 __global__ void __launch_bounds__(256)
     k_nn_sweep(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out, Geom g, int t_begin, int t_end,
                const T* __restrict__ v_hi, const T* __restrict__ w_lo, int ZC, int ahead) {
-    nn_sweep_body<T, FUSED, HINTS>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    nn_sweep_body<T, FUSED, HINTS, KEEP>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
 }
 
 // occupancy A/B (nn_variant 6): registers capped for MINB CTAs per SM
@@ -551,7 +552,10 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_sweep<T, false>, 256, 0);
         ahead = std::max(1, std::max(per_sm, 1) * device_info().num_sms * g_sweep_prefetch / 4);
     }
-    if (g_sweep_hints) {
+    if (g_sweep_hints && g_sweep_keep) {
+        if (mode == SU3G_FMA) k_nn_sweep<T, true, true, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+        else k_nn_sweep<T, false, true, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
+    } else if (g_sweep_hints) {
         if (mode == SU3G_FMA) k_nn_sweep<T, true, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
         else k_nn_sweep<T, false, true><<<gs, 256, 0, st>>>(U, v, out, g, t_begin, t_end, v_hi, w_lo, ZC, ahead);
     } else {
@@ -752,6 +756,11 @@ int su3g_set_option(const char* name, int64_t value) {
     if (std::strcmp(name, "sweep_l2_hints") == 0) {
         if (value != 0 && value != 1) return fail_invalid("set_option: sweep_l2_hints must be 0 or 1");
         g_sweep_hints = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "sweep_l2_keep") == 0) {
+        if (value != 0 && value != 1) return fail_invalid("set_option: sweep_l2_keep must be 0 or 1");
+        g_sweep_keep = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "sweep_prefetch") == 0) {
