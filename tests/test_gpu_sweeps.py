@@ -103,6 +103,26 @@ def test_link_product_config3_full_size():
             _lib.set_option("link_variant", 0)
 
 
+@pytest.mark.parametrize("chunk", [0, 1, 5, 48])
+def test_link_product_config3_f32_t_walk(chunk):
+    """configs[3] shape in complex64 through the TMA t-walk kernel (f32 default): bitwise vs the C oracle
+    for every work-item chunking (items that wrap the periodic t boundary included)."""
+    from paper_1309_0551_b200 import _lib
+
+    dims = (48, 48, 48, 48)
+    rng = inputs.config_rng(33)
+    U = inputs.random_links(rng, 48**4, 4, dtype=np.float32)
+    want = coracle.link_product(U, dims, 1 / 6)
+    _lib.set_option("link_variant", 8)
+    _lib.set_option("link_tw_chunk", chunk)
+    try:
+        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-5
+    finally:
+        _lib.set_option("link_variant", 0)
+        _lib.set_option("link_tw_chunk", 0)
+
+
 @pytest.mark.parametrize("C", [6, 18, 24, 72])
 def test_layout_round_trip(C, precision):
     tdt = torch.float32 if precision == "single" else torch.float64
@@ -245,10 +265,12 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
 
 
 @pytest.mark.parametrize(
-    "variant", [0, 1, 2, 3, 4, 6, 7], ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile"]
+    "variant", [0, 1, 2, 3, 4, 6, 7, 8], ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile", "t-walk"]
 )
 @pytest.mark.parametrize(
-    "dims", [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97), (16, 8, 4, 6), (8, 4, 2, 3)]
+    "dims",
+    [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97), (16, 8, 4, 6), (8, 4, 2, 3),
+     (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33)],
 )
 def test_link_product_variants_bitwise(variant, dims, precision):
     from paper_1309_0551_b200 import _lib

@@ -29,6 +29,32 @@ __global__ void k_packed_prmt(float* out, int n, float x) {
   float s = 0; for (int c = 0; c < CH; ++c) { float2 a = *reinterpret_cast<float2*>(&acc[c]); s += a.x + a.y; }
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+// packed multiply, scalar adds: ptxas does not contract FMUL2 into a scalar FADD (exact arithmetic)
+__global__ void k_mul2_sadd(float* out, int n, float x) {
+  uint64_t acc[CH], p[CH];
+  for (int c = 0; c < CH; ++c) { float2 a = make_float2(threadIdx.x + c, c); float2 q = make_float2(x + c, x); acc[c] = *reinterpret_cast<uint64_t*>(&a); p[c] = *reinterpret_cast<uint64_t*>(&q); }
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      uint64_t m = mul2(p[c], acc[c]);
+      float lo = __fadd_rn(__uint_as_float(uint32_t(acc[c])), __uint_as_float(uint32_t(m)));
+      float hi = __fadd_rn(__uint_as_float(uint32_t(acc[c] >> 32)), __uint_as_float(uint32_t(m >> 32)));
+      acc[c] = uint64_t(__float_as_uint(lo)) | (uint64_t(__float_as_uint(hi)) << 32);
+    }
+  }
+  float s = 0; for (int c = 0; c < CH; ++c) { float2 a = *reinterpret_cast<float2*>(&acc[c]); s += a.x + a.y; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_sfma(float* out, int n, float x) {
+  float acc[CH], p[CH];
+  for (int c = 0; c < CH; ++c) { acc[c] = threadIdx.x + c; p[c] = x + c; }
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc[c] = fmaf(p[c], acc[c], acc[c]);
+  }
+  float s = 0; for (int c = 0; c < CH; ++c) s += acc[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 __global__ void k_fma2(float* out, int n, float x) {
   uint64_t acc[CH], p[CH];
   for (int c = 0; c < CH; ++c) { float2 a = make_float2(threadIdx.x + c, c); float2 q = make_float2(x + c, x); acc[c] = *reinterpret_cast<uint64_t*>(&a); p[c] = *reinterpret_cast<uint64_t*>(&q); }
@@ -78,6 +104,8 @@ int main() {
   run("scalar f32", k_scalar, f, 1, 2);
   run("packed+prmt", k_packed_prmt, f, 2, 3);
   run("ffma2", k_fma2, f, 2, 1);
+  run("fmul2+2 fadd", k_mul2_sadd, f, 2, 3);
+  run("scalar ffma", k_sfma, f, 1, 1);
   run("scalar f64", k_dscalar, d, 1, 2);
   run("dfma", k_dfma, d, 1, 1);
   return 0;
