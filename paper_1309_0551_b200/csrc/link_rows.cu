@@ -170,6 +170,102 @@ __global__ void __launch_bounds__(128, MINB)
     }
 }
 
+// Three lanes per site (link_variant 9).  Lane (site, r) of a warp builds row r of T = A B and of
+// P = T C^dag for the six planes and accumulates row r of the result; ten sites per warp (lanes 30,
+// 31 idle).  The three lanes of a site gather the same B/C elements in one request (ten distinct
+// addresses), so a warp-wide gather costs one L1 wavefront for ten sites where the one-thread-per-site
+// kernel spends two (f64) for 32; in exchange the live set is a row instead of matrices (~70 registers,
+// 28 warps/SM instead of 16), so twice the gathers are in flight.  Row r of each product uses the
+// per-element arithmetic of mult_su3_nn / mult_su3_na (scalar.py:77-104) and the plane order of the
+// reference composition: EXACT mode is bit-identical.
+template <typename T, bool FUSED, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    k_link_rows3(const T* __restrict__ U, T* __restrict__ acc_out, Geom g, T s, int ZC) {
+    const int lane = threadIdx.x & 31;
+    if (lane >= 30) return;  // no block-level synchronisation below
+    const int sl = lane / 3, r = lane - 3 * sl;
+    const int64_t idx = (int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5)) * 10 + sl;
+    if (idx >= g.F * g.nt) return;
+    // (z-chunk, t, z, y, x) visiting order, as k_link_rows
+    const int x = static_cast<int>(idx % g.nx);
+    int64_t q = idx / g.nx;
+    const int y = static_cast<int>(q % g.ny);
+    q /= g.ny;
+    const int zl = static_cast<int>(q % ZC);
+    q /= ZC;
+    const int t = static_cast<int>(q % g.nt);
+    const int z = static_cast<int>(q / g.nt) * ZC + zl;
+    const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
+    const int64_t F = g.F;
+
+    T acc[6], a[6];
+#pragma unroll 1
+    for (int pl = 0; pl < 6; ++pl) {
+        const int mu = c_plane_mu[pl], nu = c_plane_nu[pl];
+        if (pl == 0 || pl == 3 || pl == 5)  // row r of A = U_mu(x), kept for the planes of one mu
+            ld_soa<T, 6>(U + (int64_t(t) * 72 + mu * 18 + 6 * r) * F, F, s3, a);
+        T tr[6];
+        {
+            const int64_t nb = shifted(g, x, y, z, t, mu), tn = nb / F;
+            const T* B = U + (tn * 72 + nu * 18) * F + (nb - tn * F);  // U_nu(x + mu)
+            T b[18];
+#pragma unroll
+            for (int e = 0; e < 18; ++e) b[e] = __ldg(B + e * F);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {  // t[r][k] = sum_j a[r][j] b[j][k]   (mat_nn)
+                auto pa = [&](int j, int c) { return a[2 * j + c]; };
+                auto pb = [&](int j, int c) { return b[(3 * j + k) * 2 + c]; };
+                if constexpr (FUSED) cdot_fma<T, PLAIN, 3>(pa, pb, tr[2 * k], tr[2 * k + 1]);
+                else cdot<T, PLAIN, 3>(pa, pb, tr[2 * k], tr[2 * k + 1]);
+            }
+        }
+        const int64_t nc = shifted(g, x, y, z, t, nu), tc = nc / F;
+        const T* C = U + (tc * 72 + mu * 18) * F + (nc - tc * F);  // U_mu(x + nu)
+        T c[18];
+#pragma unroll
+        for (int e = 0; e < 18; ++e) c[e] = __ldg(C + e * F);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {  // p[r][k] = sum_j t[r][j] conj(c[k][j])   (mat_na)
+            T pr, pi;
+            auto pt = [&](int j, int cc) { return tr[2 * j + cc]; };
+            auto pc = [&](int j, int cc) { return c[(3 * k + j) * 2 + cc]; };
+            if constexpr (FUSED) cdot_fma<T, CONJ_Q, 3>(pt, pc, pr, pi);
+            else cdot<T, CONJ_Q, 3>(pt, pc, pr, pi);
+            if (pl == 0) {  // acc = 0 + s*p, as the reference's zero-initialised accumulation
+                acc[2 * k] = FUSED ? fma(s, pr, T(0)) : xadd(T(0), xmul(s, pr));
+                acc[2 * k + 1] = FUSED ? fma(s, pi, T(0)) : xadd(T(0), xmul(s, pi));
+            } else {
+                acc[2 * k] = FUSED ? fma(s, pr, acc[2 * k]) : xadd(acc[2 * k], xmul(s, pr));
+                acc[2 * k + 1] = FUSED ? fma(s, pi, acc[2 * k + 1]) : xadd(acc[2 * k + 1], xmul(s, pi));
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 6; ++e) __stcs(acc_out + (int64_t(t) * 18 + 6 * r + e) * F + s3, acc[e]);
+}
+
+int g_link_rows3_minb = 0;  // su3g_set_option("link_rows3_minb"): CTAs/SM the register budget of variant 9 targets
+
+template <typename T, bool FUSED>
+int launch_link_rows3(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st) {
+    const int64_t n = g.F * g.nt;
+    const unsigned grid = static_cast<unsigned>((n + 39) / 40);  // 4 warps x 10 sites per CTA
+    // registers (ptxas): f64 exact 80 at 6 CTAs/SM (8 spills), f64 FMA 94 at 5 (6 spills), f32 64 at 8
+    const int minb = g_link_rows3_minb ? g_link_rows3_minb : (sizeof(T) == 4 ? 8 : (FUSED ? 5 : 6));
+    switch (minb) {
+        case 4: k_link_rows3<T, FUSED, 4><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 5: k_link_rows3<T, FUSED, 5><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        case 8: k_link_rows3<T, FUSED, 8><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+        default: k_link_rows3<T, FUSED, 6><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
+    }
+    return check_launch("link_product(rows3)");
+}
+
+template int launch_link_rows3<float, false>(const float*, float*, const Geom&, float, int, cudaStream_t);
+template int launch_link_rows3<float, true>(const float*, float*, const Geom&, float, int, cudaStream_t);
+template int launch_link_rows3<double, false>(const double*, double*, const Geom&, double, int, cudaStream_t);
+template int launch_link_rows3<double, true>(const double*, double*, const Geom&, double, int, cudaStream_t);
+
 int g_link_minb = 0;     // su3g_set_option("link_minb"): CTAs/SM the register budget targets (0 = default)
 int g_link_early_c = -1;  // su3g_set_option("link_early_c"): gather C together with B (-1 = default)
 int g_link_hints = 0;

@@ -21,6 +21,7 @@ void set_sm_reserve(int n);
 extern int g_tma_threads;
 extern int g_link_minb;
 extern int g_link_tw_chunk;
+extern int g_link_rows3_minb;
 int g_link_zc = 0;   // su3g_set_option("link_zc"): z-planes per visiting chunk of the link kernels (0 = auto)
 int g_sweep_zc = 0;  // su3g_set_option("sweep_zc"): z-planes per chunk of the generic NN / dslash kernels
 // su3g_set_option("sweep_l2_hints"): evict-first backward gathers, streaming stores.  Default on:
@@ -683,6 +684,11 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     int ZC = link_chunk ? chunk_planes(nz, 16) : nz;
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
     if (g_link_zc > 0) ZC = chunk_planes(nz, g_link_zc);  // A/B knob: z-planes per chunk
+    if (lv == 9) {  // three lanes per site (A/B)
+        note_kernel(std::string("k_link_rows3<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
+        return mode == SU3G_FMA ? launch_link_rows3<T, true>(U, acc, g, s, ZC, st)
+                                : launch_link_rows3<T, false>(U, acc, g, s, ZC, st);
+    }
     if (lv == 8) {  // TMA-staged t-walk (A/B)
         const int rc = mode == SU3G_FMA ? launch_link_tw<T, true>(U, acc, g, s, st)
                                         : launch_link_tw<T, false>(U, acc, g, s, st);
@@ -785,6 +791,12 @@ int su3g_set_option(const char* name, int64_t value) {
         g_link_pref_b = static_cast<int>(value);
         return SU3G_OK;
     }
+    if (std::strcmp(name, "link_rows3_minb") == 0) {
+        if (value != 0 && value != 4 && value != 5 && value != 6 && value != 8)
+            return fail_invalid("set_option: link_rows3_minb must be 0 (default 6), 4, 5, 6 or 8");
+        g_link_rows3_minb = static_cast<int>(value);
+        return SU3G_OK;
+    }
     if (std::strcmp(name, "link_tw_chunk") == 0) {
         if (value < 0 || value > (1 << 20)) return fail_invalid("set_option: link_tw_chunk must be >= 0");
         g_link_tw_chunk = static_cast<int>(value);
@@ -801,10 +813,11 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 8)
+        if (value < 0 || value > 9)
             return fail_invalid(
                 "set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring), 4 (planes), "
-                "5 (generic, natural order), 6 (low-register rows), 7 (TMA site tiles), 8 (TMA t-walk)");
+                "5 (generic, natural order), 6 (low-register rows), 7 (TMA site tiles), 8 (TMA t-walk), "
+                "9 (three lanes per site)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -106,6 +106,8 @@ int launch_link_tile(const T* U, T* acc, const Geom& g, T s, cudaStream_t st);
 template <typename T, bool FUSED>
 int launch_link_tw(const T* U, T* acc, const Geom& g, T s, cudaStream_t st);
 template <typename T, bool FUSED>
+int launch_link_rows3(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);
+template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);
 
 // f64 TMA t-walk with a register-staged main operand (nn_tma64.cu); 1 = not applicable.

@@ -95,7 +95,7 @@ def test_link_product_config3_full_size():
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
     from paper_1309_0551_b200 import _lib
 
-    for variant in (6, 7):  # low-register rows (z-chunked order); TMA site tiles
+    for variant in (6, 7, 9):  # low-register rows (z-chunked order); TMA site tiles; three lanes per site
         _lib.set_option("link_variant", variant)
         try:
             assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
@@ -265,7 +265,9 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
 
 
 @pytest.mark.parametrize(
-    "variant", [0, 1, 2, 3, 4, 6, 7, 8], ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile", "t-walk"]
+    "variant",
+    [0, 1, 2, 3, 4, 6, 7, 8, 9],
+    ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile", "t-walk", "rows3"],
 )
 @pytest.mark.parametrize(
     "dims",
