@@ -72,6 +72,9 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sites", type=int, default=64**4, help="sites for routine:<name> workloads")
+    p.add_argument("--streams", type=int, default=16,
+                   help="routine:<name> workloads below 2^20 sites: concurrent graph branches the independent "
+                        "batch calls are spread over (1 = one serial chain; 16 measured best at 4096 sites)")
     p.add_argument("--halo", choices=["nccl", "p2p"], default="nccl",
                    help="t-slab halo transport of the nn-* workloads: NCCL send/recv overlapped with the interior "
                         "(default), or the fused boundary kernel pushing halos over NVLink (csrc/p2p.cu)")
@@ -417,10 +420,26 @@ def run_b200(args, rank, world, local):
                 launch(i)  # warm the launch caches before capture
             torch.cuda.synchronize(dev)
             graph = torch.cuda.CUDAGraph()
+            # the R launches are independent batch calls: the graph forks them over args.streams
+            # branches so that several small batches are in flight at once (1 = one serial chain)
+            C = max(1, min(args.streams, R))
+            side = [torch.cuda.Stream(dev) for _ in range(C)] if C > 1 else []
             with torch.cuda.graph(graph):
-                for i in range(R):
-                    launch(i)
-            cfg["name"] = f"{r} on {n} sites (BASELINE configs[{0 if n <= 4096 else 1}] size), CUDA graph of {R} launches over rotating operand sets (> 2x L2)"
+                if C == 1:
+                    for i in range(R):
+                        launch(i)
+                else:
+                    cap = torch.cuda.current_stream(dev)
+                    for sb in side:
+                        sb.wait_stream(cap)
+                    for i in range(R):
+                        with torch.cuda.stream(side[i % C]):
+                            launch(i)
+                    for sb in side:
+                        cap.wait_stream(sb)
+            cfg["name"] = (f"{r} on {n} sites (BASELINE configs[{0 if n <= 4096 else 1}] size), CUDA graph of {R} "
+                           f"launches over rotating operand sets (> 2x L2), {C} concurrent branch{'es' if C > 1 else ''}")
+            cfg["graph_branches"] = C
 
         def step(record=False):
             if record:
