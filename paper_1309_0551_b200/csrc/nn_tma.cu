@@ -33,6 +33,7 @@ namespace su3g {
 
 // su3g_set_option("nn_tma_l2_hints"); on by default (64^3x16 f32: 0.858 -> 0.864, neutral elsewhere)
 int g_tma_hints = 1;
+int g_tma_chunk = 0;  // su3g_set_option("nn_tma_chunk"): t-chunk length of the work items (0 = auto)
 
 namespace {
 
@@ -491,7 +492,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     int per_sm = 1;  // resident CTAs per SM (2 for the 128-thread f32 geometry)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ, PARITY>, NTHR, smem);
     const int G = sweep_sms() * std::max(per_sm, 1);
-    p.chunk = pick_chunk(p.nblocks, t_end - t_begin, G);
+    p.chunk = g_tma_chunk > 0 ? std::min(g_tma_chunk, t_end - t_begin) : pick_chunk(p.nblocks, t_end - t_begin, G);
     p.nchunks = (t_end - t_begin + p.chunk - 1) / p.chunk;
     p.nitems = p.nblocks * p.nchunks;
     p.has_vhi = v_hi != nullptr;

@@ -34,6 +34,7 @@ extern int g_link_pref_b;
 extern int g_link_hints;
 extern int g_link_l1_hints;
 extern int g_tma_hints;
+extern int g_tma_chunk;
 
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
@@ -728,6 +729,11 @@ int su3g_set_option(const char* name, int64_t value) {
                 "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major), "
                 "5 (tma walk, register-staged), 6 (generic, 3 CTAs/SM register cap)");
         g_nn_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "nn_tma_chunk") == 0) {
+        if (value < 0 || value > (1 << 20)) return fail_invalid("set_option: nn_tma_chunk must be >= 0");
+        g_tma_chunk = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "chunk_prologue_x10") == 0) {
