@@ -78,6 +78,8 @@ def parse_args(argv=None):
     p.add_argument("--halo", choices=["nccl", "p2p"], default="nccl",
                    help="t-slab halo transport of the nn-* workloads: NCCL send/recv overlapped with the interior "
                         "(default), or the fused boundary kernel pushing halos over NVLink (csrc/p2p.cu)")
+    p.add_argument("--layout", choices=("eo", "soa"), default="eo",
+                   help="dslash workload: checkerboarded (eo) fields and su3g_dslash_eo, or t-sliced SoA fields")
     p.add_argument("--dims", default=None,
                    help="experiments only: override the lattice nx,ny,nz,nt of nn-*/dslash/link workloads "
                         "(for nn-weak, nt is per GPU)")
@@ -275,7 +277,7 @@ def run_b200(args, rank, world, local):
                      ("SU3G_LINK_ZC", "link_zc"), ("SU3G_LINK_TW_CHUNK", "link_tw_chunk"), ("SU3G_LINK_ROWS3_MINB", "link_rows3_minb"), ("SU3G_LINK_PREFETCH_B", "link_prefetch_b"),
                      ("SU3G_SWEEP_ZC", "sweep_zc"), ("SU3G_SWEEP_PREFETCH", "sweep_prefetch"),
                      ("SU3G_SWEEP_L2_HINTS", "sweep_l2_hints"), ("SU3G_LINK_L2_HINTS", "link_l2_hints"), ("SU3G_LINK_L1_HINTS", "link_l1_hints"), ("SU3G_SWEEP_L2_KEEP", "sweep_l2_keep"),
-                     ("SU3G_NN_TMA_L2_HINTS", "nn_tma_l2_hints"), ("SU3G_NN_TMA_CHUNK", "nn_tma_chunk")):
+                     ("SU3G_NN_TMA_L2_HINTS", "nn_tma_l2_hints"), ("SU3G_NN_TMA_CHUNK", "nn_tma_chunk"), ("SU3G_DSLASH_EO_ZC", "dslash_eo_zc"), ("SU3G_DSLASH_EO_HINTS", "dslash_eo_hints")):
         if os.environ.get(env):
             _l.set_option(opt, int(os.environ[env]))
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
@@ -338,6 +340,9 @@ def run_b200(args, rank, world, local):
         U = Field.from_aos(lat, "mat4", U_aos)
         del U_aos
         v = Field.from_aos(lat, "vec", inputs.random_vectors_torch(lat.volume, None, tdt, dev, gen))
+        if args.layout == "eo":  # checkerboarded fields: su3g_dslash_eo
+            U, v = U.to_eo(), v.to_eo()
+            torch.cuda.synchronize(dev)
         dout = v.empty_like()
         bytes_per_launch = lat.volume * DSLASH_BYTES[args.dtype]
         mode = args.mode
@@ -355,7 +360,7 @@ def run_b200(args, rank, world, local):
 
         launches_per_step = 2
         sites_per_step = lat.volume
-        cfg["name"] += f", {mode} arithmetic"
+        cfg["name"] += f", {mode} arithmetic, {'checkerboarded (eo)' if args.layout == 'eo' else 't-sliced SoA'} fields"
     elif cfg["kind"] == "link":
         lat = Lattice4D(*cfg["global_dims"])
         if world > 1:
@@ -379,7 +384,7 @@ def run_b200(args, rank, world, local):
 
         launches_per_step = 1
         sites_per_step = lat.volume
-        cfg["name"] += f", {mode} arithmetic"
+        cfg["name"] += f", {mode} arithmetic, {'checkerboarded (eo)' if args.layout == 'eo' else 't-sliced SoA'} fields"
     else:  # routine streaming batch
         r = cfg["routine"]
         n = cfg["nsites"]
@@ -679,13 +684,25 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
         of = vf.empty_like()
         mode = args.mode
 
+        eo = args.layout == "eo"
+        if eo:
+            Ue, ve = Field(lat, "mat4", tdt, dev, layout="eo"), Field(lat, "vec", tdt, dev, layout="eo")
+            oe = ve.empty_like()
+
         def step():
             U_d.copy_(U_h, non_blocking=True)
             v_d.copy_(v_h, non_blocking=True)
             Field.from_aos(lat, "mat4", U_d, out=Uf)
             Field.from_aos(lat, "vec", v_d, out=vf)
-            for parity in (0, 1):
-                sweeps.dslash(Uf, vf, parity, out=of, mode=mode)
+            if eo:
+                Uf.to_eo(out=Ue)
+                vf.to_eo(out=ve)
+                for parity in (0, 1):
+                    sweeps.dslash(Ue, ve, parity, out=oe, mode=mode)
+                oe.to_soa(out=of)
+            else:
+                for parity in (0, 1):
+                    sweeps.dslash(Uf, vf, parity, out=of, mode=mode)
             of.to_aos(out=o_d)
             out_h.copy_(o_d, non_blocking=True)
 

@@ -234,6 +234,26 @@ SU3G_API int su3g_dslash_ws_f32(const float *U, const float *v, float *out, floa
 SU3G_API int su3g_dslash_ws_f64(const double *U, const double *v, double *out, double *scratch, int32_t nx, int32_t ny,
                                 int32_t nz, int32_t nt, int32_t parity, int32_t mode, su3g_stream_t stream);
 
+/* ---- checkerboarded ("eo") fields and the dslash on them ----
+ * eo layout: each t-slice keeps the sites of one parity as a contiguous half,
+ *     eo[(t*C + c)*F + q*F/2 + h],  q = (x+y+z+t) & 1,  h = (x>>1) + (nx/2)*(y + ny*z),
+ * F = nx*ny*nz; every extent even.  su3g_soa_to_eo / su3g_eo_to_soa permute a t-sliced SoA field
+ * of C reals per site (src and dst must not alias).  su3g_dslash_eo computes, for the sites of
+ * one parity, the same values as su3g_dslash (bitwise in EXACT mode) from eo fields: it reads
+ * v's other-parity half and writes out's `parity` half only; whole sectors, no half-used lines. */
+SU3G_API int su3g_soa_to_eo_f32(const float *soa, float *eo, int32_t nx, int32_t ny, int32_t nz, int32_t nt, int32_t reals_per_site,
+                                su3g_stream_t stream);
+SU3G_API int su3g_soa_to_eo_f64(const double *soa, double *eo, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                                int32_t reals_per_site, su3g_stream_t stream);
+SU3G_API int su3g_eo_to_soa_f32(const float *eo, float *soa, int32_t nx, int32_t ny, int32_t nz, int32_t nt, int32_t reals_per_site,
+                                su3g_stream_t stream);
+SU3G_API int su3g_eo_to_soa_f64(const double *eo, double *soa, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                                int32_t reals_per_site, su3g_stream_t stream);
+SU3G_API int su3g_dslash_eo_f32(const float *U, const float *v, float *out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
+                                int32_t parity, int32_t mode, su3g_stream_t stream);
+SU3G_API int su3g_dslash_eo_f64(const double *U, const double *v, double *out, int32_t nx, int32_t ny, int32_t nz,
+                                int32_t nt, int32_t parity, int32_t mode, su3g_stream_t stream);
+
 /* ---- t-slab multi-GPU NN sweep over NCCL (BASELINE configs[4]) ----
  * One process (or thread) per GPU.  Rank r of G holds the t-slices
  * [r*nt_local, (r+1)*nt_local) of the global lattice; U, v, out are its slab in the

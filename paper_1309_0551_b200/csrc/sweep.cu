@@ -35,6 +35,8 @@ extern int g_link_hints;
 extern int g_link_l1_hints;
 extern int g_tma_hints;
 extern int g_tma_chunk;
+extern int g_eo_zc;
+extern int g_eo_hints;
 
 // ---------------------------------------------------------------------------
 // NN sweep, one thread per site
@@ -729,6 +731,16 @@ int su3g_set_option(const char* name, int64_t value) {
                 "set_option: nn_variant must be 0 (auto), 1 (generic), 2 (walk), 3 (tma walk), 4 (generic, t-major), "
                 "5 (tma walk, register-staged), 6 (generic, 3 CTAs/SM register cap)");
         g_nn_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "dslash_eo_zc") == 0) {
+        if (value < 0 || value > (1 << 20)) return fail_invalid("set_option: dslash_eo_zc must be >= 0");
+        g_eo_zc = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "dslash_eo_hints") == 0) {
+        if (value != 0 && value != 1) return fail_invalid("set_option: dslash_eo_hints must be 0 or 1");
+        g_eo_hints = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "nn_tma_chunk") == 0) {

@@ -92,9 +92,14 @@ _SFX = {torch.float32: "f32", torch.float64: "f64"}
 class Field:
     """A lattice field of `kind` ('vec', 'mat', 'mat4', ...) resident on the GPU in t-sliced SoA."""
 
-    def __init__(self, lattice: Lattice4D, kind: str, dtype=torch.float32, device=None, data=None):
+    def __init__(self, lattice: Lattice4D, kind: str, dtype=torch.float32, device=None, data=None, layout: str = "soa"):
         if kind not in OPERAND_SHAPES or kind == "scalar":
             raise ValueError(f"unknown field kind {kind!r}")
+        if layout not in ("soa", "eo"):
+            raise ValueError(f"unknown layout {layout!r}; expected 'soa' or 'eo'")
+        if layout == "eo" and any(d % 2 for d in lattice.dims):
+            raise ValueError("the checkerboarded ('eo') layout needs every lattice extent even")
+        self.layout = layout
         if dtype not in _SFX:
             raise ValueError(f"unsupported dtype {dtype}")
         self.lattice = lattice
@@ -120,7 +125,29 @@ class Field:
         return self.data[t * self.reals * F : (t + 1) * self.reals * F].view(self.reals, F)
 
     def empty_like(self) -> "Field":
-        return Field(self.lattice, self.kind, self.dtype, self.device)
+        return Field(self.lattice, self.kind, self.dtype, self.device, layout=self.layout)
+
+    # ---- t-sliced SoA <-> checkerboarded ('eo') ----------------------------
+    def to_eo(self, out: "Field | None" = None) -> "Field":
+        """The same field in the checkerboarded layout (each t-slice: parity-0 half, parity-1 half;
+        include/su3g.h "checkerboarded fields").  The dslash on eo fields reads whole sectors."""
+        if self.layout == "eo":
+            return self
+        f = out if out is not None else Field(self.lattice, self.kind, self.dtype, self.device, layout="eo")
+        lat = self.lattice
+        _lib.call(f"su3g_soa_to_eo_{_SFX[self.dtype]}", self.data.data_ptr(), f.data.data_ptr(), lat.nx, lat.ny,
+                  lat.nz, lat.nt, self.reals, torch.cuda.current_stream(self.device).cuda_stream)
+        return f
+
+    def to_soa(self, out: "Field | None" = None) -> "Field":
+        """The same field in the t-sliced SoA layout of the sweeps."""
+        if self.layout == "soa":
+            return self
+        f = out if out is not None else Field(self.lattice, self.kind, self.dtype, self.device)
+        lat = self.lattice
+        _lib.call(f"su3g_eo_to_soa_{_SFX[self.dtype]}", self.data.data_ptr(), f.data.data_ptr(), lat.nx, lat.ny,
+                  lat.nz, lat.nt, self.reals, torch.cuda.current_stream(self.device).cuda_stream)
+        return f
 
     # ---- AoS <-> SoA ------------------------------------------------------
     @classmethod
@@ -138,6 +165,8 @@ class Field:
         if device is None:
             device = t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
         src = t.to(device).contiguous()
+        if out is not None and out.layout != "soa":
+            raise ValueError("from_aos writes the t-sliced SoA layout; convert with .to_eo() afterwards")
         f = out if out is not None else cls(lattice, kind, src.dtype, device)
         _lib.call(
             f"su3g_aos_to_soa_{_SFX[f.dtype]}", src.data_ptr(), f.data.data_ptr(), lattice.slice_sites, lattice.nt,
@@ -147,6 +176,8 @@ class Field:
 
     def to_aos(self, out: torch.Tensor | None = None) -> torch.Tensor:
         """Transform back to the reference layout, as a device tensor (V,) + kind shape."""
+        if self.layout == "eo":
+            return self.to_soa().to_aos(out=out)
         shape = (self.lattice.volume,) + OPERAND_SHAPES[self.kind]
         if out is None:
             out = torch.empty(shape, dtype=self.dtype, device=self.device)

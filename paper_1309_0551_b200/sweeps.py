@@ -39,6 +39,11 @@ def _mode(mode: str) -> int:
     return MODES[mode]
 
 
+def _need_soa(what: str, *fields) -> None:
+    if any(f is not None and getattr(f, "layout", "soa") != "soa" for f in fields):
+        raise ValueError(f"{what} works on t-sliced SoA fields; convert checkerboarded fields with .to_soa()")
+
+
 def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=None, w_lo=None,
              mode: str = "exact") -> Field:
     """One application of D on the slices t in t_range (default: all).
@@ -50,6 +55,7 @@ def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=No
     """
     if U.kind != "mat4" or v.kind != "vec":
         raise ValueError("nn_sweep needs U of kind 'mat4' and v of kind 'vec'")
+    _need_soa("nn_sweep", U, v, out)
     if U.lattice != v.lattice or U.dtype != v.dtype:
         raise ValueError("U and v must share lattice and dtype")
     if out is None:
@@ -65,6 +71,7 @@ def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=No
 
 def nn_halo_w(U: Field, v: Field, w_face: torch.Tensor, mode: str = "exact") -> torch.Tensor:
     """w = U_t^dag v on the last local t-slice -> (6, F) SoA face (sent to the +t neighbour)."""
+    _need_soa("nn_halo_w", U, v)
     lat = U.lattice
     _lib.call(
         f"su3g_nn_halo_w_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), w_face.data_ptr(),
@@ -100,6 +107,18 @@ def dslash(U: Field, v: Field, parity: int, out: Field | None = None, mode: str 
         raise ValueError("U and v must share lattice and dtype")
     if parity not in (0, 1):
         raise ValueError("parity must be 0 (even) or 1 (odd)")
+    layouts = {U.layout, v.layout} | ({out.layout} if out is not None else set())
+    if layouts == {"eo"}:  # checkerboarded fields: su3g_dslash_eo (whole sectors)
+        lat = U.lattice
+        if out is None:
+            out = Field(lat, "vec", v.dtype, v.device, data=torch.zeros_like(v.data), layout="eo")
+        _lib.call(
+            f"su3g_dslash_eo_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
+            lat.nx, lat.ny, lat.nz, lat.nt, int(parity), _mode(mode), _stream(U.device),
+        )
+        return out
+    if layouts != {"soa"}:
+        raise ValueError("dslash: U, v and out must all be t-sliced SoA or all checkerboarded ('eo') fields")
     if out is None:
         out = Field(v.lattice, "vec", v.dtype, v.device, data=torch.zeros_like(v.data))
     lat = U.lattice
@@ -123,6 +142,7 @@ def dslash(U: Field, v: Field, parity: int, out: Field | None = None, mode: str 
 def link_product(U: Field, s: float = 1.0 / 6.0, mode: str = "exact", out: Field | None = None) -> Field:
     if U.kind != "mat4":
         raise ValueError("link_product needs U of kind 'mat4'")
+    _need_soa("link_product", U, out)
     if mode not in MODES:
         raise ValueError(f"mode must be one of {sorted(MODES)}")
     lat = U.lattice
@@ -165,9 +185,12 @@ def link_product_aos(U, dims, s: float = 1.0 / 6.0, mode: str = "exact"):
     return _back(link_product(Uf, s, mode).to_aos(), U)
 
 
-def dslash_aos(U, v, dims, parity: int, mode: str = "exact"):
-    """Reference-layout dslash: (V,3,2) result, D v on the parity sites and 0 elsewhere."""
+def dslash_aos(U, v, dims, parity: int, mode: str = "exact", layout: str = "soa"):
+    """Reference-layout dslash: (V,3,2) result, D v on the parity sites and 0 elsewhere.
+    layout="eo" runs it on checkerboarded copies of the fields (su3g_dslash_eo)."""
     lat = Lattice4D.from_dims(dims)
     Uf = Field.from_aos(lat, "mat4", U)
     vf = Field.from_aos(lat, "vec", v)
+    if layout == "eo":
+        Uf, vf = Uf.to_eo(), vf.to_eo()
     return _back(dslash(Uf, vf, parity, mode=mode).to_aos(), v)

@@ -452,6 +452,111 @@ def test_dslash_argument_errors():
     assert _lib.load().su3g_dslash_f32(None, None, None, 4, 4, 4, 4, 0, 0, None) == _lib.SU3G_EINVAL
 
 
+# ---- checkerboarded ('eo') fields and su3g_dslash_eo ------------------------------------
+
+
+@pytest.mark.parametrize("kind", ["vec", "mat4", "mat"])
+@pytest.mark.parametrize("dims", [(4, 4, 4, 4), (2, 4, 6, 2), (8, 6, 2, 4)])
+def test_eo_layout_is_the_documented_permutation(kind, dims, precision):
+    """soa_to_eo places site (x,y,z,t) at (t*C + c)*F + q*F/2 + (x>>1) + nx/2*(y + ny*z); eo_to_soa inverts it."""
+    tdt = torch.float32 if precision == "single" else torch.float64
+    lat = Lattice4D(*dims)
+    nx, ny, nz, nt = dims
+    F = nx * ny * nz
+    f = Field(lat, kind, tdt, torch.device("cuda"))
+    f.data.copy_(torch.arange(f.data.numel(), dtype=tdt, device="cuda"))
+    eo = f.to_eo()
+    assert eo.layout == "eo"
+    soa = f.data.cpu().numpy().reshape(nt, f.reals, F)
+    got = eo.data.cpu().numpy().reshape(nt, f.reals, F)
+    for t in range(nt):
+        for z in range(nz):
+            for y in range(ny):
+                for x in range(nx):
+                    q = (x + y + z + t) & 1
+                    j = q * (F // 2) + (x >> 1) + (nx // 2) * (y + ny * z)
+                    assert np.array_equal(got[t, :, j], soa[t, :, x + nx * (y + ny * z)])
+    assert torch.equal(eo.to_soa().data, f.data)
+    assert np.array_equal(eo.numpy(), f.numpy())  # to_aos goes through the SoA layout
+
+
+@pytest.mark.parametrize("parity", [0, 1])
+@pytest.mark.parametrize("tag", sorted(DSLASH_DIMS))
+def test_dslash_eo_golden_bitwise(golden_sweeps, tag, precision, parity):
+    g = golden_sweeps
+    U, v = g[f"dslash/{tag}/{precision}/U"], g[f"dslash/{tag}/{precision}/v"]
+    got = sweeps.dslash_aos(U, v, DSLASH_DIMS[tag], parity, layout="eo")
+    assert np.array_equal(got, g[f"dslash/{tag}/{precision}/p{parity}"])
+
+
+@pytest.mark.parametrize("zc", [0, 1, 3])
+@pytest.mark.parametrize("hints", [1, 0])
+@pytest.mark.parametrize("dims", [(16, 16, 16, 16), (32, 8, 4, 6), (64, 64, 16, 2), (2, 2, 2, 2), (64, 64, 64, 4)])
+def test_dslash_eo_vs_c_oracle(dims, hints, zc, precision):
+    """eo dslash equals the full sweep on its parity bit for bit (exact), FMA within tolerance, for every
+    z-chunking and with / without the L2 hints; the other parity of `out` is untouched."""
+    from oracle import sweeps as OS
+    from paper_1309_0551_b200 import _lib
+
+    if dims == (64, 64, 64, 4) and (hints, zc) != (0, 0):
+        pytest.skip("one configuration at the large size")
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(6100 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    full = coracle.nn_sweep(U, v, dims)
+    even = OS.parity_mask(dims)
+    _lib.set_option("dslash_eo_hints", hints)
+    _lib.set_option("dslash_eo_zc", zc)
+    try:
+        for parity, keep in ((0, even), (1, ~even)):
+            got = sweeps.dslash_aos(U, v, dims, parity, layout="eo")
+            assert np.array_equal(got[keep], full[keep])
+            assert not np.any(got[~keep])
+            tol = 1e-5 if dt == np.float32 else 1e-12
+            fm = sweeps.dslash_aos(U, v, dims, parity, mode="fma", layout="eo")
+            assert floored_rel_err(fm[keep], full[keep]) <= tol
+            assert np.array_equal(fm, sweeps.dslash_aos(U, v, dims, parity, mode="fma"))  # same FMA chains
+    finally:
+        _lib.set_option("dslash_eo_hints", 0)
+        _lib.set_option("dslash_eo_zc", 0)
+
+
+def test_dslash_eo_composes_and_checks_layouts(precision):
+    """D_eo D_oe on eo fields; out keeps its other parity; mixed layouts and eo inputs elsewhere raise."""
+    from oracle import sweeps as OS
+
+    dt = _dt(precision)
+    dims = (8, 4, 6, 4)
+    lat = Lattice4D(*dims)
+    V = lat.volume
+    rng = inputs.config_rng(62)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    even = OS.parity_mask(dims)
+    Ue = Field.from_aos(lat, "mat4", U).to_eo()
+    out = Field.from_aos(lat, "vec", np.full((V, 3, 2), 7.0, dtype=dt)).to_eo()
+    sweeps.dslash(Ue, Field.from_aos(lat, "vec", v).to_eo(), 0, out=out)
+    got = out.numpy()
+    assert np.all(got[~even] == 7.0)
+    assert np.array_equal(got[even], coracle.nn_sweep(U, v, dims)[even])
+    ve = np.where(even[:, None, None], v, 0).astype(dt)
+    w = sweeps.dslash(Ue, Field.from_aos(lat, "vec", ve).to_eo(), 1)
+    y = sweeps.dslash(Ue, w, 0).numpy()
+    want = coracle.nn_sweep(U, coracle.nn_sweep(U, ve, dims), dims)
+    assert np.array_equal(y[even], want[even])
+    vs = Field.from_aos(lat, "vec", v)
+    with pytest.raises(ValueError, match="all be"):
+        sweeps.dslash(Ue, vs, 0)
+    with pytest.raises(ValueError, match="SoA"):
+        sweeps.nn_sweep(Ue, vs.to_eo())
+    with pytest.raises(ValueError, match="SoA"):
+        sweeps.link_product(Ue)
+    with pytest.raises(ValueError, match="even"):
+        Field(Lattice4D(4, 4, 4, 3), "vec", layout="eo")
+
+
 @pytest.mark.parametrize("option,value,default", [("sweep_l2_hints", 0, 1), ("sweep_prefetch", 1, 0),
                                                   ("link_l2_hints", 1, 0), ("link_l1_hints", 1, 0)])
 def test_generic_kernel_knobs_keep_results_bitwise(option, value, default, precision):
