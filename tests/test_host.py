@@ -52,6 +52,12 @@ def test_invalid_arguments_rejected_without_touching_the_device():
         _lib.check(_lib.SU3G_EINVAL, "x")
     assert lib.su3g_sub_four_su3_vecs_f32(None, None, None, None, None, -2, None) == _lib.SU3G_EINVAL
     assert lib.su3g_mult_adj_su3_mat_4vec_f64(None, None, None, None, None, None, -1, None) == _lib.SU3G_EINVAL
+    # checkerboarded layout / dslash: odd extents, bad parity, null pointers
+    assert lib.su3g_soa_to_eo_f32(None, None, 4, 4, 4, 3, 6, None) == _lib.SU3G_EINVAL
+    assert b"even" in lib.su3g_last_error()
+    assert lib.su3g_eo_to_soa_f64(None, None, 4, 4, 4, 4, 6, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_dslash_eo_f32(None, None, None, 4, 4, 4, 4, 2, 0, None) == _lib.SU3G_EINVAL
+    assert lib.su3g_dslash_eo_f64(None, None, None, 4, 4, 4, 4, 0, 0, None) == _lib.SU3G_EINVAL
     # zero sites is a valid no-op
     assert lib.su3g_mult_su3_nn_f64(None, None, None, 0, None) == _lib.SU3G_OK
     assert lib.su3g_sub_four_su3_vecs_f64(None, None, None, None, None, 0, None) == _lib.SU3G_OK
@@ -316,3 +322,13 @@ def test_c_host_program_against_the_abi(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert r.returncode == 0, r.stderr
     assert "abi_demo: ok" in r.stdout
+
+
+def test_field_layout_validation_without_a_gpu():
+    """The checkerboarded ('eo') layout needs even extents; unknown layouts are rejected (before any allocation)."""
+    from paper_1309_0551_b200.lattice import Field, Lattice4D
+
+    with pytest.raises(ValueError, match="even"):
+        Field(Lattice4D(4, 4, 4, 3), "vec", layout="eo")
+    with pytest.raises(ValueError, match="layout"):
+        Field(Lattice4D(4, 4, 4, 4), "vec", layout="aos")
