@@ -688,6 +688,12 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     int ZC = link_chunk ? chunk_planes(nz, 16) : nz;
     if (g_link_variant.load() == 5) ZC = nz;  // natural t-major order (A/B knob)
     if (g_link_zc > 0) ZC = chunk_planes(nz, g_link_zc);  // A/B knob: z-planes per chunk
+    if (lv == 10) {  // 8x4x4 t-walk, U_3 through L2 (A/B)
+        const int rc = mode == SU3G_FMA ? launch_link_tw4<T, true>(U, acc, g, s, st)
+                                        : launch_link_tw4<T, false>(U, acc, g, s, st);
+        if (rc != 1) return rc;
+        return fail_invalid("link_product: 8x4x4 t-walk kernel not applicable to this lattice");
+    }
     if (lv == 9) {  // three lanes per site (A/B)
         note_kernel(std::string("k_link_rows3<") + (sizeof(T) == 4 ? "f32" : "f64") + ",zchunk " + std::to_string(ZC) + ">");
         return mode == SU3G_FMA ? launch_link_rows3<T, true>(U, acc, g, s, ZC, st)
@@ -837,11 +843,11 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 9)
+        if (value < 0 || value > 10)
             return fail_invalid(
                 "set_option: link_variant must be 0 (auto), 1 (generic), 2 (block walk), 3 (ring), 4 (planes), "
                 "5 (generic, natural order), 6 (low-register rows), 7 (TMA site tiles), 8 (TMA t-walk), "
-                "9 (three lanes per site)");
+                "9 (three lanes per site), 10 (8x4x4 t-walk, U_3 via L2)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

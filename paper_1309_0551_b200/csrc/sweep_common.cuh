@@ -104,6 +104,8 @@ int launch_dslash_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, in
 template <typename T, bool FUSED>
 int launch_link_tile(const T* U, T* acc, const Geom& g, T s, cudaStream_t st);
 template <typename T, bool FUSED>
+int launch_link_tw4(const T* U, T* acc, const Geom& g, T s, cudaStream_t st);
+template <typename T, bool FUSED>
 int launch_link_tw(const T* U, T* acc, const Geom& g, T s, cudaStream_t st);
 template <typename T, bool FUSED>
 int launch_link_rows3(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);

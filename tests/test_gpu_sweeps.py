@@ -82,6 +82,25 @@ def test_link_product_vs_c_oracle(dims, precision):
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
 
 
+@pytest.mark.parametrize("chunk", [0, 7])
+def test_link_product_config3_f64_t_walk4(chunk):
+    """configs[3] through the 8x4x4 t-walk (U_3 via L2), complex128: exact bitwise, FMA within 1e-12."""
+    from paper_1309_0551_b200 import _lib
+
+    dims = (48, 48, 48, 48)
+    rng = inputs.config_rng(3)
+    U = inputs.random_links(rng, 48**4, 4, dtype=np.float64)
+    want = coracle.link_product(U, dims, 1 / 6)
+    _lib.set_option("link_variant", 10)
+    _lib.set_option("link_tw_chunk", chunk)
+    try:
+        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
+    finally:
+        _lib.set_option("link_variant", 0)
+        _lib.set_option("link_tw_chunk", 0)
+
+
 def test_link_product_config3_full_size():
     """BASELINE configs[3]: 48^4 link product, complex128 -- exact bitwise, FMA within 1e-12."""
     dims = (48, 48, 48, 48)
@@ -95,7 +114,7 @@ def test_link_product_config3_full_size():
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
     from paper_1309_0551_b200 import _lib
 
-    for variant in (6, 7, 9):  # low-register rows (z-chunked order); TMA site tiles; three lanes per site
+    for variant in (6, 7, 9, 10):  # low-register rows (z-chunked order); TMA site tiles; three lanes per site; 8x4x4 t-walk
         _lib.set_option("link_variant", variant)
         try:
             assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
@@ -103,8 +122,9 @@ def test_link_product_config3_full_size():
             _lib.set_option("link_variant", 0)
 
 
+@pytest.mark.parametrize("variant", [8, 10])
 @pytest.mark.parametrize("chunk", [0, 1, 5, 48])
-def test_link_product_config3_f32_t_walk(chunk):
+def test_link_product_config3_f32_t_walk(chunk, variant):
     """configs[3] shape in complex64 through the TMA t-walk kernel (f32 default): bitwise vs the C oracle
     for every work-item chunking (items that wrap the periodic t boundary included)."""
     from paper_1309_0551_b200 import _lib
@@ -113,7 +133,7 @@ def test_link_product_config3_f32_t_walk(chunk):
     rng = inputs.config_rng(33)
     U = inputs.random_links(rng, 48**4, 4, dtype=np.float32)
     want = coracle.link_product(U, dims, 1 / 6)
-    _lib.set_option("link_variant", 8)
+    _lib.set_option("link_variant", variant)
     _lib.set_option("link_tw_chunk", chunk)
     try:
         assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
@@ -266,13 +286,13 @@ def test_walk_variant_required_fails_loudly_when_inapplicable():
 
 @pytest.mark.parametrize(
     "variant",
-    [0, 1, 2, 3, 4, 6, 7, 8, 9],
-    ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile", "t-walk", "rows3"],
+    [0, 1, 2, 3, 4, 6, 7, 8, 9, 10],
+    ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile", "t-walk", "rows3", "t-walk4"],
 )
 @pytest.mark.parametrize(
     "dims",
     [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97), (16, 8, 4, 6), (8, 4, 2, 3),
-     (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33)],
+     (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33), (8, 4, 4, 3), (16, 8, 12, 5), (24, 4, 8, 1)],
 )
 def test_link_product_variants_bitwise(variant, dims, precision):
     from paper_1309_0551_b200 import _lib
