@@ -33,8 +33,7 @@ namespace su3g {
 
 // su3g_set_option("nn_tma_l2_hints"); on by default (64^3x16 f32: 0.858 -> 0.864, neutral elsewhere)
 int g_tma_hints = 1;
-int g_tma_chunk = 0;
-int g_tma_prologue_prefetch = 1;  // su3g_set_option("nn_tma_prologue_prefetch")  // su3g_set_option("nn_tma_chunk"): t-chunk length of the work items (0 = auto)
+int g_tma_chunk = 0;  // su3g_set_option("nn_tma_chunk"): t-chunk length of the work items (0 = auto)
 
 namespace {
 
@@ -101,12 +100,7 @@ struct TmaParams {
     int has_vhi;   // v(t = nt) comes from the v_hi face
     int hints;     // U_t gathers evict-first in L2 (read exactly once), output stored streaming
     int parity;    // PARITY kernels: output only the sites with (x+y+z+t) % 2 == parity (dslash)
-    int prologue_prefetch;  // L2-prefetch the next work item's prologue operands two steps ahead
 };
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 
 // item -> (block, t0, t1), chunk-major
 __device__ __forceinline__ void item_range(const TmaParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
@@ -309,24 +303,6 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
 
         for (int t = t0; t < t1; ++t, ++k) {
-            // two steps before the item ends (or at its start if shorter): pull the next item's
-            // prologue operands -- v(t0'), U_t(t0'-1), v(t0'-1) of this thread's site -- into L2,
-            // so its synchronous prologue loads are L2 hits instead of DRAM round trips
-            if (p.prologue_prefetch && t == max(t0, t1 - 2) && item + G < p.nitems) {
-                int64_t nblk;
-                int n0, n1;
-                item_range(p, item + G, nblk, n0, n1);
-                const int64_t ns3 = site_of(nblk);
-#pragma unroll
-                for (int q = 0; q < 6; ++q) prefetch_l2(v + (int64_t(n0) * 6 + q) * F + ns3);
-                if (!(n0 == 0 && w_lo != nullptr)) {
-                    const int np = (n0 > 0) ? n0 - 1 : p.nt - 1;
-#pragma unroll
-                    for (int q = 0; q < 18; ++q) prefetch_l2(U + (int64_t(np) * 72 + 54 + q) * F + ns3);
-#pragma unroll
-                    for (int q = 0; q < 6; ++q) prefetch_l2(v + (int64_t(np) * 6 + q) * F + ns3);
-                }
-            }
             T ut2[18];
             const Cursor c2 = ahead;  // step k + 2
             load_ut(c2, ut2);
@@ -522,7 +498,6 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.has_vhi = v_hi != nullptr;
     p.hints = g_tma_hints;
     p.parity = parity;
-    p.prologue_prefetch = g_tma_prologue_prefetch;
     const int grid = static_cast<int>(std::min<int64_t>(G, p.nitems));
     k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ, PARITY><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     note_kernel(std::string("k_nn_tma<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(nx) + "x" +

@@ -35,7 +35,6 @@ extern int g_link_hints;
 extern int g_link_l1_hints;
 extern int g_tma_hints;
 extern int g_tma_chunk;
-extern int g_tma_prologue_prefetch;
 extern int g_eo_zc;
 extern int g_eo_hints;
 
@@ -748,11 +747,6 @@ int su3g_set_option(const char* name, int64_t value) {
     if (std::strcmp(name, "dslash_eo_hints") == 0) {
         if (value != 0 && value != 1) return fail_invalid("set_option: dslash_eo_hints must be 0 or 1");
         g_eo_hints = static_cast<int>(value);
-        return SU3G_OK;
-    }
-    if (std::strcmp(name, "nn_tma_prologue_prefetch") == 0) {
-        if (value != 0 && value != 1) return fail_invalid("set_option: nn_tma_prologue_prefetch must be 0 or 1");
-        g_tma_prologue_prefetch = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "nn_tma_chunk") == 0) {
