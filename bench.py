@@ -384,7 +384,7 @@ def run_b200(args, rank, world, local):
 
         launches_per_step = 1
         sites_per_step = lat.volume
-        cfg["name"] += f", {mode} arithmetic, {'checkerboarded (eo)' if args.layout == 'eo' else 't-sliced SoA'} fields"
+        cfg["name"] += f", {mode} arithmetic"
     else:  # routine streaming batch
         r = cfg["routine"]
         n = cfg["nsites"]

@@ -59,6 +59,8 @@ def main():
         run(["--workload", "link", "--dtype", "f32"], steps="5")
         run(["--workload", "dslash", "--dtype", "f32"])
         run(["--workload", "dslash", "--dtype", "f64"])
+        run(["--workload", "dslash", "--dtype", "f32", "--layout", "soa"])
+        run(["--workload", "dslash", "--dtype", "f64", "--layout", "soa"])
 
 
 if __name__ == "__main__":
