@@ -127,12 +127,19 @@ class Field:
     def empty_like(self) -> "Field":
         return Field(self.lattice, self.kind, self.dtype, self.device, layout=self.layout)
 
+    def _check_out(self, out: "Field", layout: str) -> None:
+        if (out.layout != layout or out.kind != self.kind or out.lattice != self.lattice or out.dtype != self.dtype
+                or out.data.data_ptr() == self.data.data_ptr()):
+            raise ValueError(f"out must be a distinct {layout!r} field of the same lattice, kind and dtype")
+
     # ---- t-sliced SoA <-> checkerboarded ('eo') ----------------------------
     def to_eo(self, out: "Field | None" = None) -> "Field":
         """The same field in the checkerboarded layout (each t-slice: parity-0 half, parity-1 half;
         include/su3g.h "checkerboarded fields").  The dslash on eo fields reads whole sectors."""
         if self.layout == "eo":
             return self
+        if out is not None:
+            self._check_out(out, "eo")
         f = out if out is not None else Field(self.lattice, self.kind, self.dtype, self.device, layout="eo")
         lat = self.lattice
         _lib.call(f"su3g_soa_to_eo_{_SFX[self.dtype]}", self.data.data_ptr(), f.data.data_ptr(), lat.nx, lat.ny,
@@ -143,6 +150,8 @@ class Field:
         """The same field in the t-sliced SoA layout of the sweeps."""
         if self.layout == "soa":
             return self
+        if out is not None:
+            self._check_out(out, "soa")
         f = out if out is not None else Field(self.lattice, self.kind, self.dtype, self.device)
         lat = self.lattice
         _lib.call(f"su3g_eo_to_soa_{_SFX[self.dtype]}", self.data.data_ptr(), f.data.data_ptr(), lat.nx, lat.ny,

@@ -575,6 +575,10 @@ def test_dslash_eo_composes_and_checks_layouts(precision):
         sweeps.link_product(Ue)
     with pytest.raises(ValueError, match="even"):
         Field(Lattice4D(4, 4, 4, 3), "vec", layout="eo")
+    with pytest.raises(ValueError, match="distinct"):
+        vs.to_eo(out=vs.empty_like())  # an SoA field as the eo destination
+    with pytest.raises(ValueError, match="distinct"):
+        Ue.to_soa(out=vs)  # wrong kind
 
 
 @pytest.mark.parametrize("option,value,default", [("sweep_l2_hints", 0, 1), ("sweep_prefetch", 1, 0),
