@@ -491,10 +491,24 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     p.t_begin = t_begin; p.t_end = t_end;
     int per_sm = 1;  // resident CTAs per SM (2 for the 128-thread f32 geometry)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ, PARITY>, NTHR, smem);
-    const int G = sweep_sms() * std::max(per_sm, 1);
-    p.chunk = g_tma_chunk > 0 ? std::min(g_tma_chunk, t_end - t_begin) : pick_chunk(p.nblocks, t_end - t_begin, G);
-    p.nchunks = (t_end - t_begin + p.chunk - 1) / p.chunk;
+    // SMs left free for NCCL's kernels (su3g "sm_reserve", set by the t-slab drivers at N > 1): this
+    // persistent kernel fills every SM, so a concurrent NCCL kernel would wait for it to finish.  A
+    // free SM costs a whole extra round when it pushes the single wave over a round boundary
+    // (64^3x14 interior: 1024 items, 7 rounds on 148 CTAs, 8 on 144), so the reservation is trimmed
+    // to what the last round's slack absorbs, and dropped when not even one SM fits.
+    const int per = std::max(per_sm, 1);
+    const int G_full = device_info().num_sms * per;
+    const int L = t_end - t_begin;
+    p.chunk = g_tma_chunk > 0 ? std::min(g_tma_chunk, L) : pick_chunk(p.nblocks, L, G_full);
+    p.nchunks = (L + p.chunk - 1) / p.chunk;
     p.nitems = p.nblocks * p.nchunks;
+    int G = G_full;
+    if (sm_reserve() > 0) {
+        const int64_t rounds = (p.nitems + G_full - 1) / G_full;
+        const int64_t g_same = (p.nitems + rounds - 1) / rounds;  // fewest CTAs that keep the round count
+        const int g_res = std::max(per, sweep_sms() * per);
+        if (g_same <= G_full - per) G = static_cast<int>(std::max<int64_t>(g_res, g_same));
+    }
     p.has_vhi = v_hi != nullptr;
     p.hints = g_tma_hints;
     p.parity = parity;
@@ -502,7 +516,7 @@ static int run_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     k_nn_tma<T, FUSED, NTHR, STAGES, CNX, CBY, CBZ, PARITY><<<grid, NTHR, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     note_kernel(std::string("k_nn_tma<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(nx) + "x" +
                 std::to_string(BY) + "x" + std::to_string(BZ) + (CNX ? "" : " runtime-geometry") + "," +
-                std::to_string(NTHR) + "thr>");
+                std::to_string(NTHR) + "thr>" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
     return check_launch("nn_sweep(tma)");
 }
 
