@@ -322,12 +322,15 @@ def run_b200(args, rank, world, local):
                 per_launch_sites = lat.volume
             else:
                 per_launch_sites = max(ntl - 2, 0) * lat.slice_sites
-            launches_per_app = slab.launches_per_apply()
+            launches_per_app = slab.launches_per_apply(chained=True)  # steady state: the halo pack is fused
+            chained = [False]  # va is the previous application's out from the second application on
 
             def step(record=False):
                 nonlocal va, vb
                 for _ in range(apps):
-                    slab.apply(va, vb, timer=(lambda: _EventTimer(stream, dominant_events)) if record else None)
+                    slab.apply(va, vb, timer=(lambda: _EventTimer(stream, dominant_events)) if record else None,
+                               chain=chained[0])
+                    chained[0] = True
                     va, vb = vb, va
         bytes_per_launch = per_launch_sites * NN_BYTES[args.dtype]
 

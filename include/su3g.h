@@ -213,6 +213,17 @@ SU3G_API int su3g_nn_halo_w_f32(const float *U, const float *v, float *w_face, i
 SU3G_API int su3g_nn_halo_w_f64(const double *U, const double *v, double *w_face, int32_t nx, int32_t ny, int32_t nz,
                        int32_t nt, int32_t mode, su3g_stream_t stream);
 
+/* The two boundary slices t = 0 and t = nt-1 of a t-slab application in one launch (same values
+ * as su3g_nn_sweep on those slices, with the same v_hi / w_lo halos).  w_next (6*F reals, SoA
+ * face, may be NULL) receives U_t^dag out on slice nt-1: the halo the next application sends to
+ * rank r+1, identical to su3g_nn_halo_w(U, out) -- the t-slab drivers skip that pack kernel. */
+SU3G_API int su3g_nn_sweep_edges_f32(const float *U, const float *v, float *out, int32_t nx, int32_t ny, int32_t nz,
+                                     int32_t nt, const float *v_hi, const float *w_lo, float *w_next, int32_t mode,
+                                     su3g_stream_t stream);
+SU3G_API int su3g_nn_sweep_edges_f64(const double *U, const double *v, double *out, int32_t nx, int32_t ny, int32_t nz,
+                                     int32_t nt, const double *v_hi, const double *w_lo, double *w_next, int32_t mode,
+                                     su3g_stream_t stream);
+
 /* ---- even/odd dslash -----------------------------------
  * out(x) = sum_mu U_mu(x) v(x+mu) - sum_mu U_mu(x-mu)^dag v(x-mu) for the sites of one
  * parity, (x+y+z+t) % 2 == parity, only; those read v on the other parity only.  Fused:

@@ -81,6 +81,7 @@ def _signatures():
         sig[f"su3g_slab_nn_sweep_{sfx}"] = ([_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_dslash_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_dslash_ws_{sfx}"] = ([_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
+        sig[f"su3g_nn_sweep_edges_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp], ctypes.c_int)
         sig[f"su3g_soa_to_eo_{sfx}"] = ([_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_eo_to_soa_{sfx}"] = ([_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)
         sig[f"su3g_dslash_eo_{sfx}"] = ([_vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp], ctypes.c_int)

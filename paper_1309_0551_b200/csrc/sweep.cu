@@ -262,6 +262,34 @@ __global__ void __launch_bounds__(128)
 }
 
 
+// The two boundary slices of a t-slab application, t = 0 and t = nt-1, in one launch (the t-slab
+// drivers run them after the halo exchange).  With w_next, the threads of slice nt-1 also form
+// w = U_t(x)^dag out(x) -- the halo the NEXT application sends to rank r+1 -- from the value they
+// just stored, with nn_halo_w's arithmetic, so the next application needs no separate pack kernel.
+template <typename T, bool FUSED, bool HINTS>
+__global__ void __launch_bounds__(256)
+    k_nn_edges(const T* __restrict__ U, const T* __restrict__ v, T* out, Geom g, const T* __restrict__ v_hi,
+               const T* __restrict__ w_lo, T* __restrict__ w_next, int nedge) {
+    const int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (idx >= nedge * g.F) return;
+    const int e = idx >= g.F;  // 0: t = 0, 1: t = nt - 1
+    const int64_t s3 = idx - e * g.F;
+    const int x = static_cast<int>(s3 % g.nx);
+    const int y = static_cast<int>((s3 / g.nx) % g.ny);
+    const int z = static_cast<int>(s3 / (int64_t(g.nx) * g.ny));
+    const int t = e ? g.nt - 1 : 0;
+    nn_site<T, FUSED, HINTS>(U, v, out, g, x, y, z, t, v_hi, w_lo);
+    if (w_next != nullptr && t == g.nt - 1) {
+        T u[18], o[6], w[6];
+        ld_soa<T, 18>(U + (int64_t(t) * 72 + 54) * g.F, g.F, s3, u);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) o[k] = out[(int64_t(t) * 6 + k) * g.F + s3];  // this thread's own store
+        amv<T, FUSED>(u, o, w);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) w_next[k * g.F + s3] = w[k];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // NN sweep, t-walk kernel (the fast path)
 //
@@ -588,6 +616,28 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
                     const T* v_hi, const T* w_lo, int mode, cudaStream_t st);
 
 template <typename T>
+static int nn_edges(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, const T* v_hi, const T* w_lo,
+                    T* w_next, int mode, cudaStream_t st) {
+    if (int rc = check_geom("nn_edges", nx, ny, nz, nt)) return rc;
+    if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("nn_edges: mode must be SU3G_EXACT or SU3G_FMA");
+    if (!U || !v || !out) return fail_invalid("nn_edges: null pointer");
+    if (out == v) return fail_invalid("nn_edges: out must not alias v");
+    Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
+    const int nedge = nt > 1 ? 2 : 1;
+    const unsigned gs = static_cast<unsigned>((nedge * g.F + 255) / 256);
+    const bool fma = mode == SU3G_FMA;
+    if (g_sweep_hints) {
+        if (fma) k_nn_edges<T, true, true><<<gs, 256, 0, st>>>(U, v, out, g, v_hi, w_lo, w_next, nedge);
+        else k_nn_edges<T, false, true><<<gs, 256, 0, st>>>(U, v, out, g, v_hi, w_lo, w_next, nedge);
+    } else {
+        if (fma) k_nn_edges<T, true, false><<<gs, 256, 0, st>>>(U, v, out, g, v_hi, w_lo, w_next, nedge);
+        else k_nn_edges<T, false, false><<<gs, 256, 0, st>>>(U, v, out, g, v_hi, w_lo, w_next, nedge);
+    }
+    note_kernel(std::string("k_nn_edges<") + (sizeof(T) == 4 ? "f32" : "f64") + ">");
+    return check_launch("nn_edges");
+}
+
+template <typename T>
 static int dslash(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int parity, int mode,
                   cudaStream_t st, T* scratch = nullptr) {
     if (int rc = check_geom("dslash", nx, ny, nz, nt)) return rc;
@@ -875,6 +925,16 @@ int su3g_link_product_f32(const float* U, float* acc, int32_t nx, int32_t ny, in
 int su3g_link_product_f64(const double* U, double* acc, int32_t nx, int32_t ny, int32_t nz, int32_t nt, double s,
                           int32_t mode, su3g_stream_t st) {
     return link_product<double>(U, acc, nx, ny, nz, nt, s, mode, reinterpret_cast<cudaStream_t>(st));
+}
+int su3g_nn_sweep_edges_f32(const float* U, const float* v, float* out, int32_t nx, int32_t ny, int32_t nz,
+                            int32_t nt, const float* v_hi, const float* w_lo, float* w_next, int32_t mode,
+                            su3g_stream_t st) {
+    return nn_edges<float>(U, v, out, nx, ny, nz, nt, v_hi, w_lo, w_next, mode, reinterpret_cast<cudaStream_t>(st));
+}
+int su3g_nn_sweep_edges_f64(const double* U, const double* v, double* out, int32_t nx, int32_t ny, int32_t nz,
+                            int32_t nt, const double* v_hi, const double* w_lo, double* w_next, int32_t mode,
+                            su3g_stream_t st) {
+    return nn_edges<double>(U, v, out, nx, ny, nz, nt, v_hi, w_lo, w_next, mode, reinterpret_cast<cudaStream_t>(st));
 }
 int su3g_dslash_f32(const float* U, const float* v, float* out, int32_t nx, int32_t ny, int32_t nz, int32_t nt,
                     int32_t parity, int32_t mode, su3g_stream_t st) {

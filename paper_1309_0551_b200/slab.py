@@ -14,10 +14,13 @@ Per application of D, rank r needs two one-site halos:
     single-GPU sweep; 6 reals cross the link per face site instead of 24.
 
 Schedule per application (compute stream C, NCCL's stream N):
-  C: pack w_last                        (su3g_nn_halo_w)
+  C: pack w_last                        (su3g_nn_halo_w; skipped when chained, see below)
   N: send v_first -> r-1, recv v_hi <- r+1, send w_last -> r+1, recv w_lo <- r-1
   C: interior slices t in [1, nt_local-1)    -- overlaps the exchange
-  C: wait(N); boundary slices t = 0 and t = nt_local-1
+  C: wait(N); boundary slices t = 0 and t = nt_local-1 in one launch (su3g_nn_sweep_edges), which
+     also packs w_last of its result for the next application
+Chained applications (apply_n, or apply(..., chain=True) when v is the previous call's out) reuse
+that packed w instead of launching the pack kernel again.
 
 The compute is pluggable (``kernels``) so the exchange logic can be exercised
 on CPU ranks over gloo in the tests; the product default is the CUDA kernels.
@@ -52,6 +55,10 @@ class CudaSlabKernels:
 
     def sweep(self, U: Field, v: Field, out: Field, t_range, v_hi, w_lo) -> None:
         sweeps.nn_sweep(U, v, out=out, t_range=t_range, v_hi=v_hi, w_lo=w_lo, mode=self.mode)
+
+    def edges(self, U: Field, v: Field, out: Field, v_hi, w_lo, w_next) -> None:
+        """Both boundary slices in one launch; w_next <- w_last of out (the next application's halo)."""
+        sweeps.nn_edges(U, v, out, v_hi=v_hi, w_lo=w_lo, w_next=w_next, mode=self.mode)
 
     def nt(self, v: Field) -> int:
         return v.lattice.nt
@@ -99,6 +106,7 @@ class SlabSweep:
         else:
             self.rank, self.world = 0, 1
         self._faces = None
+        self._w_of = None  # the Field whose w_last the face buffer holds (packed by the edges launch)
         if hasattr(self.k, "prepare"):
             self.k.prepare(self.world)
 
@@ -128,41 +136,52 @@ class SlabSweep:
         ]
         return dist.batch_isend_irecv(ops)
 
-    def apply(self, v, out, timer=None):
+    def apply(self, v, out, timer=None, chain=False):
         """out = D v on this slab (periodic in t across the ranks).
 
         ``timer`` (optional) is a context-manager factory wrapped around the
         dominant kernel launch -- the whole sweep on one rank, the interior
         slices otherwise (bench.py records CUDA events with it).
+        ``chain=True`` promises that v is the unmodified ``out`` of the previous
+        call: its w_last was packed by that call's boundary launch.
         """
         if self.world == 1:
             with _maybe(timer):
                 self.k.sweep(self.U, v, out, (0, self.k.nt(v)), None, None)
             return out
         w_send, v_hi, w_lo = self._buffers(v)
-        self.k.halo_w(self.U, v, w_send)
+        fused = hasattr(self.k, "edges")
+        if not (fused and chain and self._w_of is v):
+            self.k.halo_w(self.U, v, w_send)
+        self._w_of = None
         reqs = self.exchange(v, w_send, v_hi, w_lo)
         interior, edges = boundary_ranges(self.k.nt(v))
         if interior is not None:
             with _maybe(timer):
                 self.k.sweep(self.U, v, out, interior, v_hi, w_lo)
         for r in reqs:
-            r.wait()
-        for rng in edges:
-            self.k.sweep(self.U, v, out, rng, v_hi, w_lo)
+            r.wait()  # the sends have left w_send: the edges launch may overwrite it
+        if fused:
+            self.k.edges(self.U, v, out, v_hi, w_lo, w_send)
+            self._w_of = out
+        else:
+            for rng in edges:
+                self.k.sweep(self.U, v, out, rng, v_hi, w_lo)
         return out
 
-    def launches_per_apply(self) -> int:
-        """Kernel launches of one application (halo pack + interior + boundary slices)."""
+    def launches_per_apply(self, chained: bool = False) -> int:
+        """Kernel launches of one application (halo pack unless chained, interior, boundary slices)."""
         if self.world == 1:
             return 1
         interior, edges = boundary_ranges(self.k.nt(self.U))
+        if hasattr(self.k, "edges"):
+            return (0 if chained else 1) + (interior is not None) + 1
         return 1 + (interior is not None) + len(edges)
 
     def apply_n(self, v, scratch, applications: int):
         """v <- D v `applications` times (ping-pong); returns the buffer holding the result."""
         a, b = v, scratch
-        for _ in range(applications):
-            self.apply(a, b)
+        for i in range(applications):
+            self.apply(a, b, chain=i > 0)
             a, b = b, a
         return a

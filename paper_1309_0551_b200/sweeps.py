@@ -80,6 +80,21 @@ def nn_halo_w(U: Field, v: Field, w_face: torch.Tensor, mode: str = "exact") -> 
     return w_face
 
 
+def nn_edges(U: Field, v: Field, out: Field, v_hi=None, w_lo=None, w_next: torch.Tensor | None = None,
+             mode: str = "exact") -> Field:
+    """The boundary slices t = 0 and t = nt-1 of a t-slab application in one launch; with w_next
+    (a (6, F) face), also w = U_t^dag out on slice nt-1 for the next application's exchange."""
+    if U.kind != "mat4" or v.kind != "vec" or out.kind != "vec":
+        raise ValueError("nn_edges needs U of kind 'mat4' and v, out of kind 'vec'")
+    _need_soa("nn_edges", U, v, out)
+    lat = U.lattice
+    _lib.call(
+        f"su3g_nn_sweep_edges_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
+        lat.nx, lat.ny, lat.nz, lat.nt, _ptr(v_hi), _ptr(w_lo), _ptr(w_next), _mode(mode), _stream(U.device),
+    )
+    return out
+
+
 def nn_apply(U: Field, v: Field, applications: int, scratch: Field | None = None, mode: str = "exact") -> Field:
     """v <- D v, `applications` times, ping-ponging between two buffers; returns the final field."""
     a = v

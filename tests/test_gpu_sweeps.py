@@ -213,6 +213,51 @@ def test_slab_halo_path_equals_periodic_sweep(ranks, precision, dims=(8, 4, 4, 8
     assert np.array_equal(w0, R.mult_adj_su3_mat_vec(U[(ntl - 1) * F : ntl * F, 3], v[(ntl - 1) * F : ntl * F]))
 
 
+@pytest.mark.parametrize("ranks,dims", [(1, (8, 4, 4, 6)), (2, (8, 4, 4, 8)), (4, (16, 4, 2, 8)), (4, (8, 4, 4, 4)),
+                                         (2, (64, 4, 4, 6)), (3, (8, 4, 2, 9))])
+def test_slab_edges_launch_chained(ranks, dims, precision):
+    """su3g_nn_sweep_edges: both boundary slices in one launch, plus the next application's w_last --
+    chained over 4 applications of emulated ranks, bitwise the periodic iterated sweep; the packed
+    w equals su3g_nn_halo_w of the result."""
+    dt = _dt(precision)
+    lat = Lattice4D(*dims)
+    rng = inputs.config_rng(55)
+    U = inputs.random_links(rng, lat.volume, 4, dtype=dt)
+    v = inputs.random_vectors(rng, lat.volume, None, dtype=dt)
+    apps = 4
+    want = coracle.nn_sweep_iterated(U, v, dims, apps)
+    F = lat.slice_sites
+    ntl = lat.nt // ranks
+    local = lat.slab(ranks, 0)
+    Uf = [Field.from_aos(local, "mat4", U[r * ntl * F : (r + 1) * ntl * F]) for r in range(ranks)]
+    vf = [Field.from_aos(local, "vec", v[r * ntl * F : (r + 1) * ntl * F]) for r in range(ranks)]
+    w = []
+    for r in range(ranks):
+        w.append(torch.empty((6, F), dtype=vf[r].dtype, device="cuda"))
+        sweeps.nn_halo_w(Uf[r], vf[r], w[r])
+    from paper_1309_0551_b200.slab import boundary_ranges
+
+    for _ in range(apps):
+        outs, wn = [], []
+        for r in range(ranks):
+            v_hi = vf[(r + 1) % ranks].face(0).contiguous()
+            w_lo = w[(r - 1) % ranks]
+            out = vf[r].empty_like()
+            interior, _ = boundary_ranges(ntl)
+            if interior:
+                sweeps.nn_sweep(Uf[r], vf[r], out=out, t_range=interior, v_hi=v_hi, w_lo=w_lo)
+            w_next = torch.empty_like(w[r])
+            sweeps.nn_edges(Uf[r], vf[r], out, v_hi=v_hi, w_lo=w_lo, w_next=w_next)
+            ref_w = torch.empty_like(w_next)
+            sweeps.nn_halo_w(Uf[r], out, ref_w)
+            assert torch.equal(w_next, ref_w)
+            outs.append(out)
+            wn.append(w_next)
+        vf, w = outs, wn
+    got = np.concatenate([f.numpy() for f in vf])
+    assert np.array_equal(got, want)
+
+
 @pytest.fixture(params=[0, 1, 2, 3, 5], ids=["auto", "generic", "walk", "tma", "tma64"])
 def nn_variant(request):
     from paper_1309_0551_b200 import _lib

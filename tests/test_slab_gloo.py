@@ -56,13 +56,32 @@ class OracleSlabKernels:
         return self.dims[3]
 
 
+class OracleEdgesKernels(OracleSlabKernels):
+    """The fused boundary launch of CudaSlabKernels.edges: both edge slices + the next w_last.
+    Counts halo_w calls so the tests see the chained applications skip the pack."""
+
+    halo_w_calls = 0
+
+    def halo_w(self, U, v, w):
+        OracleEdgesKernels.halo_w_calls += 1
+        super().halo_w(U, v, w)
+
+    def edges(self, U, v, out, v_hi, w_lo, w_next):
+        nt = self.dims[3]
+        full = S.nn_sweep_slab(U, v, self.dims, self._aos(v_hi), self._aos(w_lo))
+        for t in sorted({0, nt - 1}):
+            out[t * self.F : (t + 1) * self.F] = full[t * self.F : (t + 1) * self.F]
+        last = slice((nt - 1) * self.F, nt * self.F)
+        w_next.copy_(self._soa(R.mult_adj_su3_mat_vec(U[last, 3], out[last])))
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, dims, dtype, apps, outdir):
+def _worker(rank, world, port, dims, dtype, apps, outdir, fused=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -79,19 +98,26 @@ def _worker(rank, world, port, dims, dtype, apps, outdir):
         ntl = nt // world
         sl = slice(rank * ntl * F, (rank + 1) * ntl * F)
         Ul, vl = np.ascontiguousarray(U[sl]), np.ascontiguousarray(v[sl])
-        slab = SlabSweep(Ul, kernels=OracleSlabKernels((nx, ny, nz, ntl)))
+        kern = (OracleEdgesKernels if fused else OracleSlabKernels)((nx, ny, nz, ntl))
+        slab = SlabSweep(Ul, kernels=kern)
         res = slab.apply_n(vl.copy(), np.empty_like(vl), apps)
         np.save(os.path.join(outdir, f"r{rank}.npy"), res)
+        if fused:  # one pack for the first application; the edges launch packs every later one
+            np.save(os.path.join(outdir, f"packs{rank}.npy"), np.array([OracleEdgesKernels.halo_w_calls]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims,apps", [(2, (3, 4, 2, 6), 2), (3, (2, 3, 4, 6), 1), (2, (4, 2, 2, 2), 3), (4, (2, 2, 2, 12), 2)])
-def test_slab_sweep_over_gloo_equals_unsharded(world, dims, apps):
+@pytest.mark.parametrize("fused", [False, True], ids=["per-slice", "edges-launch"])
+@pytest.mark.parametrize("world,dims,apps", [(2, (3, 4, 2, 6), 2), (3, (2, 3, 4, 6), 1), (2, (4, 2, 2, 2), 3), (4, (2, 2, 2, 12), 2),
+                                             (2, (2, 2, 2, 2), 3)])
+def test_slab_sweep_over_gloo_equals_unsharded(world, dims, apps, fused):
     dtype = np.float64 if world % 2 else np.float32
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), dims, dtype, apps, d), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), dims, dtype, apps, d, fused), nprocs=world, join=True)
         got = np.concatenate([np.load(os.path.join(d, f"r{r}.npy")) for r in range(world)])
+        if fused:
+            assert all(int(np.load(os.path.join(d, f"packs{r}.npy"))[0]) == 1 for r in range(world))
     from paper_1309_0551_b200 import inputs
 
     V = int(np.prod(dims))
