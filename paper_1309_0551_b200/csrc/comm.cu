@@ -173,9 +173,16 @@ int slab_sweep(su3g_comm_t c, const T* U, const T* v, T* out, int nx, int ny, in
     }
     // 4. boundary slices once the halos are in
     if (cudaError_t e = cudaStreamWaitEvent(st, c->ev_halo, 0)) return cuda_fail("slab_nn_sweep: wait", e);
-    if ((rc = sweep(0, 1, v_hi, w_lo))) return rc;
-    if (nt > 1 && (rc = sweep(nt - 1, nt, v_hi, w_lo))) return rc;
-    return SU3G_OK;
+    // both boundary slices in one launch (su3g_nn_sweep_edges)
+    if (F32)
+        return su3g_nn_sweep_edges_f32(reinterpret_cast<const float*>(U), reinterpret_cast<const float*>(v),
+                                       reinterpret_cast<float*>(out), nx, ny, nz, nt,
+                                       reinterpret_cast<const float*>(v_hi), reinterpret_cast<const float*>(w_lo),
+                                       nullptr, mode, st);
+    return su3g_nn_sweep_edges_f64(reinterpret_cast<const double*>(U), reinterpret_cast<const double*>(v),
+                                   reinterpret_cast<double*>(out), nx, ny, nz, nt,
+                                   reinterpret_cast<const double*>(v_hi), reinterpret_cast<const double*>(w_lo),
+                                   nullptr, mode, st);
 }
 
 }  // namespace
