@@ -131,6 +131,17 @@ def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
 
 
+_fns: dict = {}
+
+
+def fn(name: str):
+    """The declared ctypes function `name` (cached lookup for per-call hot paths)."""
+    f = _fns.get(name)
+    if f is None:
+        f = _fns[name] = getattr(load(), name)
+    return f
+
+
 def last_kernel() -> str:
     """Kernel (with geometry) the calling thread's last libsu3g launch dispatched to."""
     return load().su3g_last_kernel().decode(errors="replace")

@@ -208,6 +208,42 @@ def _scalar_operand(s, rdtype, prefix, device):
     return 0.0, torch.from_numpy(np.ascontiguousarray(s_arr).reshape(-1)).to(device)
 
 
+def _fast_path(name: str, kinds, result_kind: str, a, b, out, s=None):
+    """Launch directly for the common device case -- contiguous real CUDA tensors of one dtype on the
+    current device, batch shape (n,), a contiguous real CUDA `out` of the result shape (or none), a
+    0-d scalar -- with the general path's semantics; None when the call needs the general path.
+    (Measured: the general path costs ~15 us of host time per call, this one ~5.)"""
+    T = torch.Tensor
+    if type(a) is not T or type(b) is not T or not a.is_cuda or not b.is_cuda:
+        return None
+    rdtype = a.dtype
+    if rdtype not in _SFX or b.dtype != rdtype or not a.is_contiguous() or not b.is_contiguous():
+        return None
+    sa, sb = OPERAND_SHAPES[kinds[0]], OPERAND_SHAPES[kinds[1]]
+    if a.dim() != len(sa) + 1 or b.dim() != len(sb) + 1 or tuple(a.shape[1:]) != sa or tuple(b.shape[1:]) != sb:
+        return None
+    n = a.shape[0]
+    if b.shape[0] != n or a.device != b.device or a.device.index != torch.cuda.current_device():
+        return None
+    if out is None:
+        out = torch.empty((n,) + OPERAND_SHAPES[result_kind], dtype=rdtype, device=a.device)
+    elif (type(out) is not T or not out.is_cuda or out.dtype != rdtype or not out.is_contiguous()
+          or out.device != a.device or tuple(out.shape) != (n,) + OPERAND_SHAPES[result_kind]):
+        return None
+    elif validation.enabled():
+        return None  # the debug alias checks live on the general path
+    if n:
+        fn = _lib.fn(f"su3g_{name}_{_SFX[rdtype]}")
+        st = torch.cuda.current_stream(a.device).cuda_stream
+        if s is None:
+            rc = fn(a.data_ptr(), b.data_ptr(), out.data_ptr(), n, st)
+        else:
+            rc = fn(a.data_ptr(), b.data_ptr(), s, None, out.data_ptr(), n, st)
+        if rc:
+            _lib.check(rc, f"su3g_{name}_{_SFX[rdtype]}")
+    return out
+
+
 def _make(name: str):
     spec = routine_spec(name)
     kinds = spec.operands
@@ -215,6 +251,9 @@ def _make(name: str):
     like_index = 1 if spec.result in ("vec", "vec4", "hwvec") else 0
 
     def routine(a, b, out=None):
+        res = _fast_path(name, kinds, spec.result, a, b, out)
+        if res is not None:
+            return res
         labelled = [(a, kinds[0]), (b, kinds[1])]
         probe = [_Arg(a, kinds[0]), _Arg(b, kinds[1])]
         return _run(name, labelled, spec.result, probe[like_index], out)
@@ -239,6 +278,12 @@ su3_projector = _make("su3_projector")
 
 
 def _smadd(name: str, kind: str, a, b, s, out):
+    if isinstance(s, (int, float)) and not isinstance(s, bool):  # 0-d host scalar: cast to the operand dtype
+        if type(a) is torch.Tensor and a.dtype in _SFX:
+            sc = float(np.float32(s)) if a.dtype == torch.float32 else float(s)
+            res = _fast_path(name, (kind, kind), kind, a, b, out, s=sc)
+            if res is not None:
+                return res
     probe_a = _Arg(a, kind)
     nd = len(OPERAND_SHAPES[kind])
     prefix = tuple(probe_a.shape[:-nd]) if len(probe_a.shape) >= nd else ()
