@@ -582,6 +582,85 @@ def _interior_kernel(sweeps, U, va, vb, nt, mode) -> str:
     return _lib.last_kernel()
 
 
+def _pipelined_e2e(hosts, out_host, compute, steps, world, dev, stream):
+    """Time `steps` end-to-end steps, pipelined across steps without skipping any copy: step i+1's
+    inputs stream host->device on a copy-in stream while step i computes, and step i's result leaves
+    device->host on a third stream (PCIe is full duplex).  Double-buffered device staging; events
+    order buffer reuse.  compute(dev_inputs, dev_out) enqueues the step's work on `stream`.
+    Returns the elapsed milliseconds (max over ranks)."""
+    import torch
+
+    cin, cout = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    d_in = [[torch.empty_like(h, device=dev) for h in hosts] for _ in range(2)]
+    d_out = [torch.empty_like(out_host, device=dev) for _ in range(2)]
+    outs_h = [out_host, torch.empty_like(out_host).pin_memory()]
+    ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("h2d", "comp", "d2h")}
+
+    def enqueue(i):
+        b = i % 2
+        with torch.cuda.stream(cin):
+            if i >= 2:
+                cin.wait_event(ev["comp"][b])  # step i-2 has finished reading this input buffer
+            for d, h in zip(d_in[b], hosts):
+                d.copy_(h, non_blocking=True)
+            ev["h2d"][b].record(cin)
+        stream.wait_event(ev["h2d"][b])
+        if i >= 2:
+            stream.wait_event(ev["d2h"][b])  # step i-2's result has left this output buffer
+        compute(d_in[b], d_out[b])
+        ev["comp"][b].record(stream)
+        with torch.cuda.stream(cout):
+            cout.wait_event(ev["comp"][b])
+            outs_h[b].copy_(d_out[b], non_blocking=True)
+            ev["d2h"][b].record(cout)
+
+    for i in range(3):  # warm-up
+        enqueue(i)
+    torch.cuda.synchronize(dev)
+    barrier(world, dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(cin)
+    stream.wait_event(e0)
+    for i in range(steps):
+        enqueue(i)
+    for b in range(2):
+        stream.wait_event(ev["d2h"][b])
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world, dev)
+    return max_over_ranks(e0.elapsed_time(e1), world, dev)
+
+
+def _sequential_e2e(hosts, out_host, compute, steps, world, dev, stream):
+    """The same steps on one stream, copy-in -> compute -> copy-out: for small steps, where the
+    host cost of the pipelined form's extra streams and events outweighs the overlap."""
+    import torch
+
+    d_in = [torch.empty_like(h, device=dev) for h in hosts]
+    d_out = torch.empty_like(out_host, device=dev)
+
+    def step():
+        for d, h in zip(d_in, hosts):
+            d.copy_(h, non_blocking=True)
+        compute(d_in, d_out)
+        out_host.copy_(d_out, non_blocking=True)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize(dev)
+    barrier(world, dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(world, dev)
+    return max_over_ranks(e0.elapsed_time(e1), world, dev)
+
+
 def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
     """Same metric through the reference-facing path: pinned host AoS in, host AoS out, copies timed."""
     import torch
@@ -591,15 +670,14 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
     from paper_1309_0551_b200.slab import CudaSlabKernels, SlabSweep
 
     steps = max(3, min(args.steps, 10))
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99 + rank)
+    path = ("pinned host AoS -> H2D (copy stream, overlapping the previous step) -> {} -> D2H (its own stream)")
     if cfg["kind"] == "nn":
         lat = Lattice4D(*cfg["global_dims"]).slab(world, rank)
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(99 + rank)
         U_h = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen).cpu().pin_memory()
         v_h = inputs.random_vectors_torch(lat.volume, None, tdt, dev, gen).cpu().pin_memory()
         out_h = torch.empty_like(v_h).pin_memory()
-        U_d = torch.empty_like(U_h, device=dev)
-        v_d = torch.empty_like(v_h, device=dev)
         Uf = Field(lat, "mat4", tdt, dev)
         va, vb = Field(lat, "vec", tdt, dev), Field(lat, "vec", tdt, dev)
         if args.halo == "p2p":
@@ -615,183 +693,94 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
             def run_apps(a, b, n):
                 return slab.apply_n(a, b, n)
 
-        h2d = U_h.numel() * U_h.element_size() + v_h.numel() * v_h.element_size()
-        d2h = out_h.numel() * out_h.element_size()
-        sites = lat.volume * cfg["apps"]
-        # Pipelined across steps: step i+1's inputs stream in (copy-in stream) while step i
-        # computes, and step i's result streams out on a third stream (PCIe is full duplex).
-        # Every step still moves its own inputs host->device and its result device->host.
-        del U_d, v_d
-        cin, cout = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-        U_ds = [torch.empty_like(U_h, device=dev) for _ in range(2)]
-        v_ds = [torch.empty_like(v_h, device=dev) for _ in range(2)]
-        o_ds = [torch.empty_like(v_h, device=dev) for _ in range(2)]
-        out_hs = [out_h, torch.empty_like(v_h).pin_memory()]
-        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("h2d", "comp", "d2h")}
+        def compute(d_in, d_out):
+            Field.from_aos(lat, "mat4", d_in[0], out=Uf)
+            Field.from_aos(lat, "vec", d_in[1], out=va)
+            run_apps(va, vb, cfg["apps"]).to_aos(out=d_out)
 
-        def enqueue(i):
-            b = i % 2
-            with torch.cuda.stream(cin):
-                if i >= 2:
-                    cin.wait_event(ev["comp"][b])  # step i-2 has finished reading this input buffer
-                U_ds[b].copy_(U_h, non_blocking=True)
-                v_ds[b].copy_(v_h, non_blocking=True)
-                ev["h2d"][b].record(cin)
-            stream.wait_event(ev["h2d"][b])
-            if i >= 2:
-                stream.wait_event(ev["d2h"][b])  # step i-2's result has left this output buffer
-            Field.from_aos(lat, "mat4", U_ds[b], out=Uf)
-            Field.from_aos(lat, "vec", v_ds[b], out=va)
-            res = run_apps(va, vb, cfg["apps"])
-            res.to_aos(out=o_ds[b])
-            ev["comp"][b].record(stream)
-            with torch.cuda.stream(cout):
-                cout.wait_event(ev["comp"][b])
-                out_hs[b].copy_(o_ds[b], non_blocking=True)
-                ev["d2h"][b].record(cout)
-
-        for i in range(3):  # warm-up
-            enqueue(i)
-        torch.cuda.synchronize(dev)
-        barrier(world, dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(cin)
-        stream.wait_event(e0)
-        for i in range(steps):
-            enqueue(i)
-        for b in range(2):
-            stream.wait_event(ev["d2h"][b])
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier(world, dev)
-        ms = max_over_ranks(e0.elapsed_time(e1), world, dev)
-        return {
-            "value": sites * world * steps / (ms / 1e3),
-            "unit": UNIT,
-            "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h),
-            "steps": steps,
-            "path": "pinned host AoS -> H2D (copy stream, overlapping the previous step) -> AoS->SoA -> kernels "
-                    "(+halos) -> SoA->AoS -> D2H (its own stream)",
-        }
+        hosts, sites = [U_h, v_h], lat.volume * cfg["apps"]
+        what = "AoS->SoA -> kernels (+halos) -> SoA->AoS"
     elif cfg["kind"] == "dslash":
         lat = Lattice4D(*cfg["global_dims"])
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(98)
         U_h = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen).cpu().pin_memory()
         v_h = inputs.random_vectors_torch(lat.volume, None, tdt, dev, gen).cpu().pin_memory()
         out_h = torch.empty_like(v_h).pin_memory()
-        U_d, v_d, o_d = torch.empty_like(U_h, device=dev), torch.empty_like(v_h, device=dev), torch.empty_like(v_h, device=dev)
         Uf, vf = Field(lat, "mat4", tdt, dev), Field(lat, "vec", tdt, dev)
         of = vf.empty_like()
-        mode = args.mode
-
         eo = args.layout == "eo"
         if eo:
             Ue, ve = Field(lat, "mat4", tdt, dev, layout="eo"), Field(lat, "vec", tdt, dev, layout="eo")
             oe = ve.empty_like()
 
-        def step():
-            U_d.copy_(U_h, non_blocking=True)
-            v_d.copy_(v_h, non_blocking=True)
-            Field.from_aos(lat, "mat4", U_d, out=Uf)
-            Field.from_aos(lat, "vec", v_d, out=vf)
+        def compute(d_in, d_out):
+            Field.from_aos(lat, "mat4", d_in[0], out=Uf)
+            Field.from_aos(lat, "vec", d_in[1], out=vf)
             if eo:
                 Uf.to_eo(out=Ue)
                 vf.to_eo(out=ve)
                 for parity in (0, 1):
-                    sweeps.dslash(Ue, ve, parity, out=oe, mode=mode)
+                    sweeps.dslash(Ue, ve, parity, out=oe, mode=args.mode)
                 oe.to_soa(out=of)
             else:
                 for parity in (0, 1):
-                    sweeps.dslash(Uf, vf, parity, out=of, mode=mode)
-            of.to_aos(out=o_d)
-            out_h.copy_(o_d, non_blocking=True)
+                    sweeps.dslash(Uf, vf, parity, out=of, mode=args.mode)
+            of.to_aos(out=d_out)
 
-        h2d = U_h.numel() * U_h.element_size() + v_h.numel() * v_h.element_size()
-        d2h = out_h.numel() * out_h.element_size()
-        sites = lat.volume
+        hosts, sites = [U_h, v_h], lat.volume
+        what = "AoS->SoA" + (" -> eo" if eo else "") + " -> both parities -> SoA->AoS"
     elif cfg["kind"] == "link":
         lat = Lattice4D(*cfg["global_dims"])
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(99)
         U_h = inputs.random_links_torch(lat.volume, 4, tdt, dev, gen).cpu().pin_memory()
         out_h = torch.empty((lat.volume, 3, 3, 2), dtype=tdt).pin_memory()
-        U_d = torch.empty_like(U_h, device=dev)
-        o_d = torch.empty_like(out_h, device=dev)
         Uf = Field(lat, "mat4", tdt, dev)
-        mode = args.mode
+        acc = Field(lat, "mat", tdt, dev)
 
-        def step():
-            U_d.copy_(U_h, non_blocking=True)
-            Field.from_aos(lat, "mat4", U_d, out=Uf)
-            sweeps.link_product(Uf, 1.0 / 6.0, mode=mode).to_aos(out=o_d)
-            out_h.copy_(o_d, non_blocking=True)
+        def compute(d_in, d_out):
+            Field.from_aos(lat, "mat4", d_in[0], out=Uf)
+            sweeps.link_product(Uf, 1.0 / 6.0, mode=args.mode, out=acc).to_aos(out=d_out)
 
-        h2d = U_h.numel() * U_h.element_size()
-        d2h = out_h.numel() * out_h.element_size()
-        sites = lat.volume
+        hosts, sites = [U_h], lat.volume
+        what = "AoS->SoA -> link product -> SoA->AoS"
     else:
         from paper_1309_0551_b200 import kernels
+        from paper_1309_0551_b200 import types as T
 
         r = cfg["routine"]
         n = cfg["nsites"]
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(99)
-        from paper_1309_0551_b200 import types as T
-
+        gen_c = torch.Generator(device=dev)
+        gen_c.manual_seed(99)
         spec = T.routine_spec(r)
         kinds = [k for k in spec.operands if k != "scalar"]
-        hosts = [torch.randn((n,) + T.OPERAND_SHAPES[k], dtype=tdt, generator=gen, device=dev).cpu().pin_memory()
+        hosts = [torch.randn((n,) + T.OPERAND_SHAPES[k], dtype=tdt, generator=gen_c, device=dev).cpu().pin_memory()
                  for k in kinds]
-        devs = [torch.empty_like(h, device=dev) for h in hosts]
-        res_shape = (n,) + T.OPERAND_SHAPES[spec.result]
-        c_d = torch.empty(res_shape, dtype=tdt, device=dev)
-        out_h = torch.empty(res_shape, dtype=tdt).pin_memory()
+        out_h = torch.empty((n,) + T.OPERAND_SHAPES[spec.result], dtype=tdt).pin_memory()
         fn = kernels.KERNELS[r]
 
-        def step():
-            for h, d in zip(hosts, devs):
-                d.copy_(h, non_blocking=True)
+        def compute(d_in, d_out):
             if r in SMADD_ROUTINES:
-                fn(devs[0], devs[1], 0.5, out=c_d)
-                res = c_d
+                fn(d_in[0], d_in[1], 0.5, out=d_out)
             elif r == "mult_adj_su3_mat_4vec":
-                fn(devs[0], devs[1], outs=[c_d[:, d] for d in range(4)])  # strided views: staged + copied
-                res = c_d
+                fn(d_in[0], d_in[1], outs=[d_out[:, d] for d in range(4)])  # strided views: staged + copied
             elif r == "sub_four_su3_vecs":
-                res = fn(*devs)
+                d_out.copy_(fn(*d_in))  # in place on its first operand
             else:
-                fn(devs[0], devs[1], out=c_d)
-                res = c_d
-            out_h.copy_(res, non_blocking=True)
+                fn(d_in[0], d_in[1], out=d_out)
 
-        h2d = sum(h.numel() for h in hosts) * hosts[0].element_size()
-        d2h = out_h.numel() * out_h.element_size()
         sites = n
-
-    for _ in range(3):
-        step()
-    torch.cuda.synchronize(dev)
-    barrier(world, dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    barrier(world, dev)
-    ms = max_over_ranks(e0.elapsed_time(e1), world, dev)
+        what = "drop-in routine (AoS, C ABI)"
+    step_bytes = sum(h.numel() * h.element_size() for h in hosts) + out_h.numel() * out_h.element_size()
+    if step_bytes >= (4 << 20):  # copies long enough to hide behind each other (65536-site routines: +13%)
+        ms = _pipelined_e2e(hosts, out_h, compute, steps, world, dev, stream)
+    else:
+        ms = _sequential_e2e(hosts, out_h, compute, steps, world, dev, stream)
+        path = path.replace(" (copy stream, overlapping the previous step)", "").replace(" (its own stream)", "")
     return {
         "value": sites * world * steps / (ms / 1e3),
         "unit": UNIT,
-        "h2d_bytes_per_step": int(h2d),
-        "d2h_bytes_per_step": int(d2h),
+        "h2d_bytes_per_step": int(sum(h.numel() * h.element_size() for h in hosts)),
+        "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()),
         "steps": steps,
-        "path": ("pinned host AoS -> H2D -> drop-in routine (AoS, C ABI) -> D2H" if cfg["kind"] == "routine" else
-                 "pinned host AoS -> H2D -> AoS->SoA -> kernels (+NCCL halos) -> SoA->AoS -> D2H"),
+        "path": path.format(what),
     }
 
 
