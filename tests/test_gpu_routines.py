@@ -146,6 +146,48 @@ def test_torch_device_tensors_and_out(precision):
     assert_parity(host_out, R.mult_su3_nn(U[:, 0], U[:, 1]))
 
 
+def test_device_fast_path_keeps_the_general_semantics(precision):
+    """Contiguous real CUDA tensors take the direct launch; everything else falls back to the general
+    path with the same results and the same errors (wrong shapes, mixed precisions, aliasing under
+    debug validation, non-contiguous views, multi-axis batches, scalars of either kind)."""
+    from paper_1309_0551_b200 import validation
+
+    dt = np.float32 if precision == "single" else np.float64
+    tdt = torch.float32 if precision == "single" else torch.float64
+    rng = inputs.config_rng(81)
+    U = inputs.random_links(rng, 300, 2, dtype=dt)
+    v = inputs.random_vectors(rng, 300, None, dtype=dt)
+    a = torch.from_numpy(np.ascontiguousarray(U[:, 0])).cuda()
+    b = torch.from_numpy(np.ascontiguousarray(U[:, 1])).cuda()
+    vd = torch.from_numpy(v).cuda()
+    # fast path: fresh result and out=
+    assert_parity(kernels.mult_su3_nn(a, b).cpu().numpy(), R.mult_su3_nn(U[:, 0], U[:, 1]))
+    assert_parity(kernels.mult_su3_mat_vec(a, vd).cpu().numpy(), R.mult_su3_mat_vec(U[:, 0], v))
+    got = kernels.scalar_mult_add_su3_matrix(a, b, 0.1)
+    assert_parity(got.cpu().numpy(), R.scalar_mult_add_su3_matrix(U[:, 0], U[:, 1], dt(0.1)))
+    # per-site scalar, non-contiguous operand, multi-axis batch: general path, same values
+    s = np.linspace(-1, 1, 300).astype(dt)
+    assert_parity(kernels.scalar_mult_add_su3_matrix(a, b, torch.from_numpy(s).cuda()).cpu().numpy(),
+                  R.scalar_mult_add_su3_matrix(U[:, 0], U[:, 1], s))
+    Ud = torch.from_numpy(U).cuda()
+    assert_parity(kernels.mult_su3_na(Ud[:, 0], Ud[:, 1]).cpu().numpy(), R.mult_su3_na(U[:, 0], U[:, 1]))
+    assert_parity(kernels.mult_su3_an(a.view(20, 15, 3, 3, 2), b.view(20, 15, 3, 3, 2)).reshape(300, 3, 3, 2).cpu().numpy(),
+                  R.mult_su3_an(U[:, 0], U[:, 1]))
+    # errors as on the general path
+    with pytest.raises(ValueError, match="shape"):
+        kernels.mult_su3_nn(a, b, out=torch.empty((299, 3, 3, 2), dtype=tdt, device="cuda"))
+    with pytest.raises(ValueError, match="precision|mix"):
+        kernels.mult_su3_nn(a, b.double() if tdt == torch.float32 else b.float())
+    with pytest.raises(ValueError):
+        kernels.mult_su3_mat_vec(a, b)
+    validation.debug_validation(True)
+    try:
+        with pytest.raises(ValueError, match="alias"):
+            kernels.mult_su3_nn(a, b, out=a)
+    finally:
+        validation.debug_validation(False)
+
+
 def test_complex_inputs(precision):
     dt = np.float32 if precision == "single" else np.float64
     rng = inputs.config_rng(9)
