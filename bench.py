@@ -788,6 +788,20 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
 # CPU side: the reference algorithm (pinned numpy port in oracle/) on host cores
 # ----------------------------------------------------------------------------
 
+def _host_info() -> dict:
+    """CPU model and numpy version of the host the CPU baseline ran on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "numpy": np.__version__}
+
+
 def _cpu_sample(cfg, dtype, small=False):
     """A bounded sample of the workload for the host CPU: (callable, site-ops per call, state, description)."""
     from oracle import routines as R
@@ -874,6 +888,7 @@ def cpu_baseline(args, cfg, threads=1, budget_s=10.0):
         "kind": "port",
         "sample": f"{desc}; {n} calls in {el:.2f} s",
         "host_cpus": os.cpu_count(),
+        **_host_info(),
     }
 
 
@@ -910,7 +925,7 @@ def run_reference(args, rank, world):
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{desc} per step; reference association (numpy restatement pinned bitwise to su3bench)",
-                         "host_cpus": os.cpu_count()},
+                         "host_cpus": os.cpu_count(), **_host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
