@@ -79,7 +79,31 @@ static void gpu_checks(void) {
     CHECK(su3g_nn_sweep_f32(dL, ds, dout, 4, 4, 4, 4, 0, 4, NULL, NULL, SU3G_EXACT, NULL) == SU3G_OK);
     cudaMemcpy(ho, dout, sizeof(float) * V * 6, cudaMemcpyDeviceToHost);
     for (int k = 0; k < V * 6; ++k) CHECK(ho[k] == 0.0f);
+
+    /* the same operator on checkerboarded fields: permute to eo, dslash both parities, permute back */
+    float *dLe, *dse, *doe, *dback;
+    cudaMalloc((void **)&dLe, sizeof(float) * V * 72);
+    cudaMalloc((void **)&dse, sizeof(float) * V * 6);
+    cudaMalloc((void **)&doe, sizeof(float) * V * 6);
+    cudaMalloc((void **)&dback, sizeof(float) * V * 6);
+    cudaMemset(doe, 0xff, sizeof(float) * V * 6); /* NaN: every site must be written by one parity */
+    CHECK(su3g_soa_to_eo_f32(dL, dLe, 4, 4, 4, 4, 72, NULL) == SU3G_OK);
+    CHECK(su3g_soa_to_eo_f32(ds, dse, 4, 4, 4, 4, 6, NULL) == SU3G_OK);
+    CHECK(su3g_dslash_eo_f32(dLe, dse, doe, 4, 4, 4, 4, 0, SU3G_EXACT, NULL) == SU3G_OK);
+    CHECK(su3g_dslash_eo_f32(dLe, dse, doe, 4, 4, 4, 4, 1, SU3G_EXACT, NULL) == SU3G_OK);
+    CHECK(su3g_eo_to_soa_f32(doe, dback, 4, 4, 4, 4, 6, NULL) == SU3G_OK);
+    cudaMemcpy(ho, dback, sizeof(float) * V * 6, cudaMemcpyDeviceToHost);
+    for (int k = 0; k < V * 6; ++k) CHECK(ho[k] == 0.0f);
+    /* the t-slab boundary launch on a one-slab lattice with zero halos: slice 0 loses its -t term
+     * (4v - 3v = 0.5), slice 3 its +t term (3v - 4v = -0.5) */
+    float *dz;
+    cudaMalloc((void **)&dz, sizeof(float) * 64 * 6);
+    cudaMemset(dz, 0, sizeof(float) * 64 * 6);
+    CHECK(su3g_nn_sweep_edges_f32(dL, ds, dout, 4, 4, 4, 4, dz, dz, NULL, SU3G_EXACT, NULL) == SU3G_OK);
+    cudaMemcpy(ho, dout, sizeof(float) * V * 6, cudaMemcpyDeviceToHost);
+    for (int k = 0; k < 64 * 6; ++k) CHECK(ho[k] == 0.5f && ho[3 * 64 * 6 + k] == -0.5f);
     CHECK(cudaDeviceSynchronize() == cudaSuccess);
+    cudaFree(dLe); cudaFree(dse); cudaFree(doe); cudaFree(dback); cudaFree(dz);
     cudaFree(dU); cudaFree(dv); cudaFree(dc); cudaFree(dL); cudaFree(ds); cudaFree(dout);
     free(hU); free(hv); free(hc); free(hL); free(hs); free(ho);
 }
