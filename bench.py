@@ -272,12 +272,10 @@ def run_b200(args, rank, world, local):
     from paper_1309_0551_b200 import _lib as _l
 
     for env, opt in (("SU3G_NN_VARIANT", "nn_variant"), ("SU3G_CHUNK_PROLOGUE_X10", "chunk_prologue_x10"),
-                     ("SU3G_NN_TMA_THREADS", "nn_tma_threads"), ("SU3G_LINK_VARIANT", "link_variant"),
-                     ("SU3G_LINK_MINB", "link_minb"), ("SU3G_LINK_EARLY_C", "link_early_c"),
-                     ("SU3G_LINK_ZC", "link_zc"), ("SU3G_LINK_TW_CHUNK", "link_tw_chunk"), ("SU3G_LINK_ROWS3_MINB", "link_rows3_minb"), ("SU3G_LINK_PREFETCH_B", "link_prefetch_b"),
-                     ("SU3G_SWEEP_ZC", "sweep_zc"), ("SU3G_SWEEP_PREFETCH", "sweep_prefetch"),
-                     ("SU3G_SWEEP_L2_HINTS", "sweep_l2_hints"), ("SU3G_LINK_L2_HINTS", "link_l2_hints"), ("SU3G_LINK_L1_HINTS", "link_l1_hints"), ("SU3G_SWEEP_L2_KEEP", "sweep_l2_keep"),
-                     ("SU3G_NN_TMA_L2_HINTS", "nn_tma_l2_hints"), ("SU3G_NN_TMA_CHUNK", "nn_tma_chunk"), ("SU3G_DSLASH_EO_ZC", "dslash_eo_zc"), ("SU3G_DSLASH_EO_HINTS", "dslash_eo_hints")):
+                     ("SU3G_NN_TMA_THREADS", "nn_tma_threads"), ("SU3G_SWEEP_ZC", "sweep_zc"),
+                     ("SU3G_SWEEP_L2_HINTS", "sweep_l2_hints"), ("SU3G_NN_TMA_L2_HINTS", "nn_tma_l2_hints"),
+                     ("SU3G_NN_TMA_CHUNK", "nn_tma_chunk"), ("SU3G_DSLASH_EO_ZC", "dslash_eo_zc"),
+                     ("SU3G_DSLASH_EO_HINTS", "dslash_eo_hints")):
         if os.environ.get(env):
             _l.set_option(opt, int(os.environ[env]))
     tdt = torch.float32 if args.dtype == "f32" else torch.float64

@@ -58,30 +58,16 @@ SU3G_API const char *su3g_last_kernel(void);
 SU3G_API int su3g_device_sm_count(void);
 SU3G_API int64_t su3g_device_l2_bytes(void);
 /* process-wide tuning/debug knobs (not needed for normal use):
- *   "nn_variant":   0 auto, 1 generic (z-chunked order), 2 register t-walk, 3 TMA t-walk,
- *                   4 generic in plain t-major order (A/B), 5 register-staged f64 TMA walk,
- *                   6 generic capped at 3 CTAs/SM worth of registers (A/B)
- *   "link_variant": 0 auto (= 6), 1 generic one-thread-per-site, 2 block walk, 3 cp.async ring,
- *                   4 plane-split, 5 generic in plain t-major order (A/B), 6 low-register rows
- *                   (accumulator in smem), 7 TMA-staged site tiles (3 threads per site)
- *   "link_minb":    CTAs/SM the rows kernel's register budget targets: 0 default (f64: 4 exact,
- *                   3 FMA; f32: 6), 3, 4, 5, 6 or 8
- *   "link_prefetch_b": 1 = the rows kernel gathers the next plane's U_nu(x+mu) during this plane (A/B)
- *   "link_zc":      z-planes per visiting chunk of the link kernels (largest divisor of nz <= value;
- *                   0 = auto: 16 when a t-slice of links exceeds half of L2, else nz)
- *   "sweep_zc":     the same for the one-thread-per-site NN sweep and dslash kernels (auto: 8)
+ *   "nn_variant":   0 auto, 1 generic one-thread-per-site (z-chunked order), 3 TMA t-walk
+ *   "nn_tma_chunk": t-chunk length of the TMA walk's work items (0 = auto, balances the wave)
+ *   "nn_tma_threads": 0 auto, 128 or 256 threads per TMA-walk CTA
+ *   "chunk_prologue_x10": relative cost of a work-item prologue, in tenths of a step (chunk picker)
+ *   "sweep_zc":     z-planes per visiting chunk of the one-thread-per-site NN sweep and dslash kernels
+ *                   (largest divisor of nz <= value; 0 = auto: 8 when a t-slice exceeds half of L2)
  *   "sweep_l2_hints": 1 (default) = the one-thread-per-site NN / dslash kernels load backward
  *                   (last-use) links and v(t-1) evict-first in L2 and store their output streaming
- *   "nn_tma_l2_hints": 1 = the TMA NN kernel gathers U_t evict-first and stores streaming (A/B)
- *   "sweep_l2_keep": 1 = the generic NN kernel also loads each site's own links evict-last (A/B)
- *   "link_l1_hints": 1 = the link rows kernel loads A evict-last in L1 and B/C no-allocate (A/B)
- *   "link_l2_hints": 1 = the link rows kernel marks each link's last-use gather evict-first (A/B;
- *                   default register targets only)
- *   "sweep_prefetch": L2 prefetch distance of the one-thread-per-site kernels (generic NN, dslash,
- *                   link rows) in quarter waves of CTAs: thread 0 issues cp.async.bulk.prefetch.L2
- *                   for the sites of the CTA that far ahead (0 = off, max 16)
- *   "link_early_c": 1 = the rows kernel gathers U_mu(x+nu) together with U_nu(x+mu), 0 = after
- *                   T = A B is built, -1 = default (1 for f32, 0 for f64)
+ *   "nn_tma_l2_hints": 1 (default) = the TMA NN kernel gathers U_t evict-first and stores streaming
+ *   "dslash_eo_zc", "dslash_eo_hints": the same two knobs for the checkerboarded dslash
  *   "sm_reserve":   SMs the persistent sweep kernels leave free for concurrent kernels
  *                   (NCCL halo exchange of a t-slab sweep); default 0 */
 SU3G_API int su3g_set_option(const char *name, int64_t value);

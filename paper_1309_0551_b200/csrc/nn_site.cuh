@@ -36,33 +36,46 @@ __device__ __forceinline__ void ld_soa_last(const T* __restrict__ p, int64_t F, 
     for (int k = 0; k < N; ++k) r[k] = ld_hint(p + k * F + s3, pol);
 }
 
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
+// Halo faces that a peer writes while the reading kernel is resident (p2p.cu): coherent
+// system-scope loads, ordered after the CTA's acquire of the peer's flag by the CTA barrier --
+// never the non-coherent (.nc / __ldg) path, which is only defined for data that stays
+// read-only for the kernel's lifetime.
+__device__ __forceinline__ float ld_coherent(const float* p) {
+    float r;
+    asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ double ld_coherent(const double* p) {
+    double r;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(r) : "l"(p) : "memory");
+    return r;
+}
+template <typename T, int N, bool COHERENT>
+__device__ __forceinline__ void ld_halo(const T* p, int64_t F, int64_t s3, T* r) {
+#pragma unroll
+    for (int k = 0; k < N; ++k) r[k] = COHERENT ? ld_coherent(p + k * F + s3) : __ldg(p + k * F + s3);
 }
 
-template <typename T, bool FUSED, bool HINTS = false, bool KEEP = false>
+// COHERENT_HALO: v_hi / w_lo are peer-written windows (see ld_coherent)
+template <typename T, bool FUSED, bool HINTS = false, bool COHERENT_HALO = false>
 __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __restrict__ v, T* __restrict__ out,
-                                        const Geom& g, int x, int y, int z, int t, const T* __restrict__ v_hi,
-                                        const T* __restrict__ w_lo) {
+                                        const Geom& g, int x, int y, int z, int t, const T* v_hi,
+                                        const T* w_lo) {
     const int64_t F = g.F;
     const uint64_t pol = HINTS ? l2_evict_first_policy() : 0;
-    const uint64_t keep = KEEP ? l2_evict_last_policy() : 0;  // own links: first of their two reads
     const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
     T acc[6];
     // forward terms, mu = 0..3, summed left to right (add_su3_vector chain)
 #pragma unroll
     for (int mu = 0; mu < 4; ++mu) {
         T u[18], vn[6], f[6];
-        if constexpr (KEEP) ld_soa_last<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, s3, u, keep);
-        else ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, s3, u);
+        ld_soa<T, 18>(U + (int64_t(t) * 72 + mu * 18) * F, F, s3, u);
         if (mu < 3) {
             ld_soa<T, 6>(v + int64_t(t) * 6 * F, F, step3(g, x, y, z, mu, +1), vn);
         } else if (t + 1 < g.nt) {
             ld_soa<T, 6>(v + int64_t(t + 1) * 6 * F, F, s3, vn);
         } else if (v_hi != nullptr) {
-            ld_soa<T, 6>(v_hi, F, s3, vn);
+            ld_halo<T, 6, COHERENT_HALO>(v_hi, F, s3, vn);
         } else {
             ld_soa<T, 6>(v, F, s3, vn);
         }
@@ -91,7 +104,7 @@ __device__ __forceinline__ void nn_site(const T* __restrict__ U, const T* __rest
             else ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vn);
             amv<T, FUSED>(u, vn, w);
         } else {
-            ld_soa<T, 6>(w_lo, F, s3, w);
+            ld_halo<T, 6, COHERENT_HALO>(w_lo, F, s3, w);
         }
 #pragma unroll
         for (int k = 0; k < 6; ++k) acc[k] = xsub(acc[k], w[k]);

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256)
         const int x = static_cast<int>(s3 % g.nx);
         const int y = static_cast<int>((s3 / g.nx) % g.ny);
         const int z = static_cast<int>(s3 / (int64_t(g.nx) * g.ny));
-        nn_site<T, FUSED>(U, v, out, g, x, y, z, t, me.vhi[par], me.wlo[par]);
+        nn_site<T, FUSED, false, true>(U, v, out, g, x, y, z, t, me.vhi[par], me.wlo[par]);
         // next application's halos, computed from this application's output (own thread's stores)
         if (t == 0) {
 #pragma unroll

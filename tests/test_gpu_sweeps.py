@@ -82,25 +82,6 @@ def test_link_product_vs_c_oracle(dims, precision):
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
 
 
-@pytest.mark.parametrize("chunk", [0, 7])
-def test_link_product_config3_f64_t_walk4(chunk):
-    """configs[3] through the 8x4x4 t-walk (U_3 via L2), complex128: exact bitwise, FMA within 1e-12."""
-    from paper_1309_0551_b200 import _lib
-
-    dims = (48, 48, 48, 48)
-    rng = inputs.config_rng(3)
-    U = inputs.random_links(rng, 48**4, 4, dtype=np.float64)
-    want = coracle.link_product(U, dims, 1 / 6)
-    _lib.set_option("link_variant", 10)
-    _lib.set_option("link_tw_chunk", chunk)
-    try:
-        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
-        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
-    finally:
-        _lib.set_option("link_variant", 0)
-        _lib.set_option("link_tw_chunk", 0)
-
-
 def test_link_product_config3_full_size():
     """BASELINE configs[3]: 48^4 link product, complex128 -- exact bitwise, FMA within 1e-12."""
     dims = (48, 48, 48, 48)
@@ -112,35 +93,16 @@ def test_link_product_config3_full_size():
     assert np.array_equal(got, want)
     del got
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
-    from paper_1309_0551_b200 import _lib
-
-    for variant in (6, 7, 9, 10):  # low-register rows (z-chunked order); TMA site tiles; three lanes per site; 8x4x4 t-walk
-        _lib.set_option("link_variant", variant)
-        try:
-            assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
-        finally:
-            _lib.set_option("link_variant", 0)
 
 
-@pytest.mark.parametrize("variant", [8, 10])
-@pytest.mark.parametrize("chunk", [0, 1, 5, 48])
-def test_link_product_config3_f32_t_walk(chunk, variant):
-    """configs[3] shape in complex64 through the TMA t-walk kernel (f32 default): bitwise vs the C oracle
-    for every work-item chunking (items that wrap the periodic t boundary included)."""
-    from paper_1309_0551_b200 import _lib
-
+def test_link_product_config3_f32_full_size():
+    """configs[3] shape in complex64: bitwise vs the C oracle, FMA within 1e-5."""
     dims = (48, 48, 48, 48)
     rng = inputs.config_rng(33)
     U = inputs.random_links(rng, 48**4, 4, dtype=np.float32)
     want = coracle.link_product(U, dims, 1 / 6)
-    _lib.set_option("link_variant", variant)
-    _lib.set_option("link_tw_chunk", chunk)
-    try:
-        assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
-        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-5
-    finally:
-        _lib.set_option("link_variant", 0)
-        _lib.set_option("link_tw_chunk", 0)
+    assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+    assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-5
 
 
 @pytest.mark.parametrize("C", [6, 18, 24, 72])
@@ -258,7 +220,11 @@ def test_slab_edges_launch_chained(ranks, dims, precision):
     assert np.array_equal(got, want)
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 5], ids=["auto", "generic", "walk", "tma", "tma64"])
+NN_VARIANTS = [0, 1, 3]
+NN_VARIANT_IDS = ["auto", "generic", "tma"]
+
+
+@pytest.fixture(params=NN_VARIANTS, ids=NN_VARIANT_IDS)
 def nn_variant(request):
     from paper_1309_0551_b200 import _lib
 
@@ -280,7 +246,7 @@ def test_nn_kernel_variants_bitwise(dims, precision, nn_variant):
     try:
         got = sweeps.nn_sweep_aos(U, v, dims)
     except ValueError as e:
-        if nn_variant in (2, 3, 5) and "not applicable" in str(e):
+        if nn_variant == 3 and "not applicable" in str(e):
             pytest.skip(f"variant {nn_variant} not applicable to {dims}")
         raise
     assert np.array_equal(got, want)
@@ -296,73 +262,57 @@ def test_nn_kernel_variants_bitwise(dims, precision, nn_variant):
     assert np.array_equal(out.numpy(), want)
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 5])
+@pytest.mark.parametrize("variant", [1, 3])
 def test_slab_halo_path_all_variants(variant, precision):
     from paper_1309_0551_b200 import _lib
 
     _lib.set_option("nn_variant", variant)
     try:
         if variant == 3 and precision == "double":
-            pytest.skip("the f32-style TMA walk does not fit shared memory for f64 on these lattices")
-        if variant != 5:
-            test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(16, 4, 4, 8))
-            test_slab_halo_path_equals_periodic_sweep(4, precision, dims=(16, 4, 4, 8))
+            pytest.skip("the f32 TMA walk does not fit shared memory for f64 on these lattices")
+        test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(16, 4, 4, 8))
+        test_slab_halo_path_equals_periodic_sweep(4, precision, dims=(16, 4, 4, 8))
         test_slab_halo_path_equals_periodic_sweep(8, precision, dims=(64, 4, 2, 8))
         test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(64, 4, 4, 8))
     finally:
         _lib.set_option("nn_variant", 0)
 
 
-def test_walk_variant_required_fails_loudly_when_inapplicable():
+def test_tma_variant_required_fails_loudly_when_inapplicable():
     from paper_1309_0551_b200 import _lib
 
-    _lib.set_option("nn_variant", 2)
+    _lib.set_option("nn_variant", 3)
     try:
         lat = Lattice4D(512, 1, 1, 2)  # x extent larger than a CTA
         U = Field(lat, "mat4", torch.float32, torch.device("cuda"))
         v = Field(lat, "vec", torch.float32, torch.device("cuda"))
-        with pytest.raises(ValueError, match="walk kernel not applicable"):
+        with pytest.raises(ValueError, match="TMA kernel not applicable"):
             sweeps.nn_sweep(U, v)
     finally:
         _lib.set_option("nn_variant", 0)
     with pytest.raises(ValueError):
         _lib.set_option("no_such_option", 1)
+    with pytest.raises(ValueError):
+        _lib.set_option("nn_variant", 2)  # the register walk was removed (measured slower)
 
 
-@pytest.mark.parametrize(
-    "variant",
-    [0, 1, 2, 3, 4, 6, 7, 8, 9, 10],
-    ids=["auto", "generic", "block-walk", "ring", "planes", "rows", "tile", "t-walk", "rows3", "t-walk4"],
-)
 @pytest.mark.parametrize(
     "dims",
     [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97), (16, 8, 4, 6), (8, 4, 2, 3),
      (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33), (8, 4, 4, 3), (16, 8, 12, 5), (24, 4, 8, 1)],
 )
-def test_link_product_variants_bitwise(variant, dims, precision):
-    from paper_1309_0551_b200 import _lib
-
+def test_link_product_bitwise(dims, precision):
     dt = _dt(precision)
     V = int(np.prod(dims))
     rng = inputs.config_rng(4000 + V)
     U = inputs.random_links(rng, V, 4, dtype=dt)
     want = coracle.link_product(U, dims, 1 / 6)
-    _lib.set_option("link_variant", variant)
-    try:
-        try:
-            got = sweeps.link_product_aos(U, dims, 1 / 6)
-        except ValueError as e:
-            if "not applicable" in str(e):
-                pytest.skip(f"link variant {variant} not applicable to {dims}")
-            raise
-        assert np.array_equal(got, want)
-        tol = 1e-5 if dt == np.float32 else 1e-12
-        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
-    finally:
-        _lib.set_option("link_variant", 0)
+    assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+    tol = 1e-5 if dt == np.float32 else 1e-12
+    assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 5], ids=["generic", "walk", "tma", "tma64"])
+@pytest.mark.parametrize("variant", [1, 3], ids=["generic", "tma"])
 @pytest.mark.parametrize("dims", [(64, 4, 4, 6), (32, 8, 4, 5), (8, 8, 8, 8)])
 def test_nn_fma_mode_within_tolerance(variant, dims, precision):
     """SU3G_FMA arithmetic: within the north-star tolerance of the reference, and every kernel variant
@@ -406,7 +356,7 @@ def test_nn_tma_multi_item_schedules(dims, precision):
     U = inputs.random_links(rng, V, 4, dtype=dt)
     v = inputs.random_vectors(rng, V, None, dtype=dt)
     want = coracle.nn_sweep(U, v, dims)
-    for variant in (0, 2, 3, 5):
+    for variant in NN_VARIANTS:
         _lib.set_option("nn_variant", variant)
         try:
             try:
@@ -626,8 +576,7 @@ def test_dslash_eo_composes_and_checks_layouts(precision):
         Ue.to_soa(out=vs)  # wrong kind
 
 
-@pytest.mark.parametrize("option,value,default", [("sweep_l2_hints", 0, 1), ("sweep_prefetch", 1, 0),
-                                                  ("link_l2_hints", 1, 0), ("link_l1_hints", 1, 0)])
+@pytest.mark.parametrize("option,value,default", [("sweep_l2_hints", 0, 1), ("sweep_zc", 3, 0)])
 def test_generic_kernel_knobs_keep_results_bitwise(option, value, default, precision):
     """Cache-hint / prefetch knobs of the one-thread-per-site kernels never change a bit."""
     from paper_1309_0551_b200 import _lib
@@ -655,7 +604,7 @@ def test_generic_kernel_knobs_keep_results_bitwise(option, value, default, preci
 
 @pytest.mark.parametrize("dims", [(48, 4, 4, 6), (48, 2, 6, 3), (24, 8, 4, 5), (40, 4, 2, 3), (96, 2, 2, 4), (12, 16, 4, 3)])
 def test_sweeps_for_x_extents_not_dividing_256(dims):
-    """nx = 48 takes the specialised 48x2x2 TMA geometry (when ny, nz > 2); others the register walk;
+    """nx = 48 takes the specialised 48x2x2 TMA geometry (when ny, nz > 2); others the generic kernel;
     all bitwise vs the oracle."""
     from paper_1309_0551_b200 import _lib
 
