@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "SU(3) site-ops/s and HBM GB/s as % of peak (fp32/fp64), 1–8 GPUs"
 UNIT = "site-ops/s"
 FALLBACK_HBM_GBS = 6650.0
+DATASHEET_HBM_GBS = 8000.0  # B200 datasheet HBM3e bandwidth (reported beside the measured peak)
 
 # algorithmic (compulsory) HBM bytes per site: read each input object once, write each output once
 NN_BYTES = {"f32": 336, "f64": 672}        # U 72 reals + v 6 + out 6
@@ -71,6 +72,7 @@ def parse_args(argv=None):
                         "for the NN sweep); fma = FMA chains within the north-star tolerance")
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-parity", action="store_true", help="skip the parity check of the timed path against the C oracle")
     p.add_argument("--sites", type=int, default=64**4, help="sites for routine:<name> workloads")
     p.add_argument("--streams", type=int, default=16,
                    help="routine:<name> workloads below 2^20 sites: concurrent graph branches the independent "
@@ -221,8 +223,7 @@ def init_dist(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("--gpus > 1 must be launched with torch.distributed.run (one rank per GPU)")
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "b200" or world > 1:
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
@@ -305,14 +306,17 @@ def run_b200(args, rank, world, local):
             per_launch_sites = lat.volume  # timed unit: one application (boundary + interior launches)
             launches_per_app = 2 if ntl > 2 else 1
 
+            p2p_chained = [False]
+
             def step(record=False):
                 nonlocal va, vb
                 for _ in range(apps):
                     if record:
                         with _EventTimer(stream, dominant_events):
-                            p2p.apply(va, vb)
+                            p2p.apply(va, vb, chain=p2p_chained[0])
                     else:
-                        p2p.apply(va, vb)
+                        p2p.apply(va, vb, chain=p2p_chained[0])
+                    p2p_chained[0] = True
                     va, vb = vb, va
         else:
             slab = SlabSweep(U, kernels=CudaSlabKernels(args.mode))
@@ -331,6 +335,30 @@ def run_b200(args, rank, world, local):
                     chained[0] = True
                     va, vb = vb, va
         bytes_per_launch = per_launch_sites * NN_BYTES[args.dtype]
+
+        def parity_fn():
+            """One more application of the timed path (chained, as in the steady state) from the current
+            field, against the C oracle on every rank's slab (halo faces from the neighbour ranks)."""
+            from oracle import coracle
+
+            out = va.empty_like()
+            if args.halo == "p2p":
+                p2p.apply(va, out, chain=True)
+                p2p.check()
+            else:
+                slab.apply(va, out, chain=True)
+            torch.cuda.synchronize(dev)
+            U_h, v_h, got = U.numpy(), va.numpy(), out.numpy()
+            if world == 1:
+                want = coracle.nn_sweep(U_h, v_h, lat.dims)
+            else:
+                F = lat.slice_sites
+                w_last = coracle.routine("mult_adj_su3_mat_vec", U_h[-F:, 3], v_h[-F:])
+                v_hi, w_lo = _exchange_faces(v_h[:F], w_last, rank, world, dev)
+                want = coracle.nn_sweep_slab(U_h, v_h, lat.dims, v_hi, w_lo)
+            return got, want, (f"one application of the timed path (chained) on every rank's full "
+                               f"{'x'.join(map(str, lat.dims))} slab, vs the C oracle "
+                               f"({'periodic sweep' if world == 1 else 'slab with the neighbours halo faces'})")
 
         launches_per_step = apps * launches_per_app
         sites_per_step = lat.volume * apps  # per rank
@@ -359,6 +387,14 @@ def run_b200(args, rank, world, local):
                     e1.record(stream)
                     dominant_events.append((e0, e1))
 
+        def parity_fn():
+            from oracle import coracle
+
+            step()
+            torch.cuda.synchronize(dev)
+            want = coracle.nn_sweep(U.numpy(), v.numpy(), lat.dims)
+            return dout.numpy(), want, "both parities of one timed step (D = D_eo + D_oe) vs the C oracle NN sweep"
+
         launches_per_step = 2
         sites_per_step = lat.volume
         cfg["name"] += f", {mode} arithmetic, {'checkerboarded (eo)' if args.layout == 'eo' else 't-sliced SoA'} fields"
@@ -383,6 +419,14 @@ def run_b200(args, rank, world, local):
                 e1.record(stream)
                 dominant_events.append((e0, e1))
 
+        def parity_fn():
+            from oracle import coracle
+
+            step()
+            torch.cuda.synchronize(dev)
+            want = coracle.link_product(U.numpy(), lat.dims, 1.0 / 6.0)
+            return acc.numpy(), want, "the accumulator of one timed step at full size vs the C oracle link product"
+
         launches_per_step = 1
         sites_per_step = lat.volume
         cfg["name"] += f", {mode} arithmetic"
@@ -391,6 +435,7 @@ def run_b200(args, rank, world, local):
         n = cfg["nsites"]
         rin, rout = ROUTINE_REALS[r]
         from paper_1309_0551_b200 import _lib
+        from paper_1309_0551_b200 import types as T
 
         ins, _ = ROUTINE_LAYOUT[r]
         sfx = args.dtype
@@ -460,6 +505,30 @@ def run_b200(args, rank, world, local):
                 e1.record(stream)
                 dominant_events.append((e0, e1))
 
+        def parity_fn():
+            """Operand set 0 through the same launch, against the oracle (first 2^20 sites)."""
+            from oracle import coracle
+            from oracle import routines as OR
+
+            m = min(n, 1 << 20)
+            spec_ = T.routine_spec(r)
+            shapes = [T.OPERAND_SHAPES[k] for k in spec_.operands if k != "scalar"]
+            before = [b[: n * k].view((n,) + sh)[:m].cpu().numpy() for b, k, sh in zip(bufs, ins, shapes)]
+            launch(0)
+            torch.cuda.synchronize(dev)
+            if r == "sub_four_su3_vecs":
+                got = bufs[0][: n * 6].view(n, 3, 2)[:m].cpu().numpy()
+            elif r == "mult_adj_su3_mat_4vec":
+                got = np.stack([c[d * n * 6 : (d + 1) * n * 6].view(n, 3, 2)[:m].cpu().numpy() for d in range(4)], 1)
+            else:
+                got = c[: n * rout].view((n,) + T.OPERAND_SHAPES[spec_.result])[:m].cpu().numpy()
+            ops = before[:2] + [before[0].dtype.type(0.5)] if r in SMADD_ROUTINES else before
+            if r in coracle.ROUTINE_IDS:
+                want = coracle.routine(r, *ops)
+            else:
+                want = OR.ALL_ROUTINES[r](*ops)
+            return got, want, f"operand set 0 of the timed launch ({m} sites) vs the oracle"
+
         launches_per_step = R
         sites_per_step = n * R
         launches_per_event = R  # one timed event brackets R graph-replayed launches
@@ -494,6 +563,17 @@ def run_b200(args, rank, world, local):
     value = total_sites / (elapsed_ms / 1e3)
     peak, peak_src = peak_hbm()
     achieved = bytes_per_launch / (kern_avg_ms / 1e3) / 1e9 if kern_ms else None
+    from paper_1309_0551_b200 import flops as _flops
+
+    intensity = _flops.intensity(cfg["routine"] if cfg["kind"] == "routine" else cfg["kind"], args.dtype)
+
+    if cfg["kind"] == "nn" and args.halo == "p2p":
+        p2p.check()  # a timed-out halo wait voids the run
+
+    # ---- parity (the checker, outside the timed region) ----------------------
+    parity = None
+    if not args.no_parity:
+        parity = _parity(parity_fn, args, cfg, world, dev)
 
     # ---- e2e through the host-buffer path ---------------------------------
     e2e = None
@@ -533,18 +613,57 @@ def run_b200(args, rank, world, local):
             "peak_source": peak_src,
             "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None,
+            "peak_datasheet": DATASHEET_HBM_GBS,
+            "frac_datasheet": (achieved / DATASHEET_HBM_GBS) if achieved else None,
             "traffic": traffic_for(args.workload, args.dtype),
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kernel_avg_ms": kern_avg_ms,
         },
+        "flops_per_site": intensity["flops_per_site"],
+        "ai_flop_per_byte": intensity["ai_flop_per_byte"],
+        "parity": parity,
         "gpu_launches": launches_per_step * args.steps,
         "launches_per_step": launches_per_step,
         "clocks": clocks.summary(),
         "e2e": e2e,
     }
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(args, cfg, threads=1)
+        line["cpu_baseline"] = cpu_baseline(args, cfg)
     return line
+
+
+def _exchange_faces(v_first, w_last, rank, world, dev):
+    """Parity check at N > 1: v on this rank's first slice goes to rank r-1, the oracle's w on its
+    last slice to rank r+1 (the t-slab halos); returns (v_hi, w_lo) as numpy."""
+    import torch
+    import torch.distributed as dist
+
+    sv = torch.from_numpy(np.ascontiguousarray(v_first)).to(dev)
+    sw = torch.from_numpy(np.ascontiguousarray(w_last)).to(dev)
+    v_hi, w_lo = torch.empty_like(sv), torch.empty_like(sw)
+    up, dn = (rank + 1) % world, (rank - 1) % world
+    ops = [dist.P2POp(dist.isend, sv, dn), dist.P2POp(dist.irecv, v_hi, up),
+           dist.P2POp(dist.isend, sw, up), dist.P2POp(dist.irecv, w_lo, dn)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    torch.cuda.synchronize(dev)
+    return v_hi.cpu().numpy(), w_lo.cpu().numpy()
+
+
+def _parity(parity_fn, args, cfg, world, dev):
+    """Run the workload's parity check on every rank; rank 0 reports the worst."""
+    from oracle.compare import parity_record
+
+    got, want, what = parity_fn()
+    exact = not (cfg["kind"] in ("nn", "link", "dslash") and args.mode == "fma")
+    rec = parity_record(got, want, exact, what)
+    del got, want
+    if world > 1:
+        rec["max_floored_rel_err"] = max_over_ranks(rec["max_floored_rel_err"], world, dev)
+        rec["bitwise"] = max_over_ranks(0.0 if rec["bitwise"] else 1.0, world, dev) == 0.0
+        rec["pass"] = max_over_ranks(0.0 if rec["pass"] else 1.0, world, dev) == 0.0
+        rec["ranks_checked"] = world
+    return rec
 
 
 class _EventTimer:
@@ -783,8 +902,35 @@ def measure_e2e(args, cfg, rank, world, dev, tdt, stream):
 
 
 # ----------------------------------------------------------------------------
-# CPU side: the reference algorithm (pinned numpy port in oracle/) on host cores
+# CPU side: the reference's own implementation of the path on host cores
 # ----------------------------------------------------------------------------
+#
+# The reference (su3bench) is pure Python + numpy.  It is installed offline into the git-ignored
+# baseline/_ref/ (__graft_entry__.build(); it travels to the GPU box with the snapshot) and driven
+# through its own public API: SiteBuffer for the fields, simd routines for the arithmetic, and
+# bench.run for the per-routine streaming rows (bench.py:229-271).  The sweeps have no reference
+# function; they are the composition of the reference's routines fixed by SURVEY.md 8(c).  When
+# baseline/_ref is missing, the numpy restatement in oracle/ (bit-identical to su3bench, pinned by
+# tests/test_oracle_golden.py) stands in and the record says kind "port".
+
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _su3bench():
+    """The installed reference package, or None."""
+    if not os.path.isdir(os.path.join(REF_PATH, "su3bench")):
+        return None
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    try:
+        import su3bench.bench  # noqa: F401
+        import su3bench.lattice  # noqa: F401
+        import su3bench.simd  # noqa: F401
+
+        return sys.modules["su3bench"]
+    except Exception:  # noqa: BLE001
+        return None
+
 
 def _host_info() -> dict:
     """CPU model and numpy version of the host the CPU baseline ran on."""
@@ -797,116 +943,205 @@ def _host_info() -> dict:
                     break
     except OSError:
         pass
-    return {"cpu_model": model, "numpy": np.__version__}
+    return {"cpu_model": model, "numpy": np.__version__, "host_cpus": os.cpu_count()}
 
 
-def _cpu_sample(cfg, dtype, small=False):
-    """A bounded sample of the workload for the host CPU: (callable, site-ops per call, state, description)."""
+class _Pinned:
+    """Pin the process to one CPU for the timed region, as the reference's bench does (bench.py:134-152)."""
+
+    def __enter__(self):
+        self.prev = None
+        try:
+            self.prev = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {min(self.prev)})
+        except (AttributeError, OSError):
+            self.prev = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            try:
+                os.sched_setaffinity(0, self.prev)
+            except OSError:
+                pass
+        return False
+
+
+class RefSweep:
+    """The composed reference sweep on output t-slices [t0, t0+k) of the workload's full lattice.
+
+    Fields live in the reference's own SiteBuffer (randomize: the reference's uniform draw; timing does
+    not depend on values).  Each output slice is computed exactly once per call: x, y, z shifts are
+    periodic rolls inside the window, t neighbours come from the slices on either side, so a sample of
+    k slices is k x F site-ops of the real workload (SURVEY.md 8(c) association).
+    """
+
+    def __init__(self, cfg, dtype: str):
+        self.kind = cfg["kind"]
+        self.dims = cfg["global_dims"]
+        prec = "single" if dtype == "f32" else "double"
+        ref = _su3bench()
+        fields = {"U": "mat4"} if self.kind == "link" else {"U": "mat4", "v": "vec"}
+        if ref is not None:
+            from su3bench import simd
+            from su3bench.lattice import Lattice4D as RLat
+            from su3bench.lattice import SiteBuffer
+
+            buf = SiteBuffer(RLat(*self.dims), fields, precision=prec)
+            buf.randomize(12345)
+            self.U = buf["U"]
+            self.v = buf["v"] if "v" in fields else None
+            self.ops = simd
+            self.source = "reference"
+            self.impl = "su3bench (baseline/_ref): SiteBuffer + simd routines, composed as SURVEY.md 8(c)"
+        else:
+            from oracle import routines as R
+            from oracle import sitebuffer as OS
+
+            V = int(np.prod(self.dims))
+            f = OS.randomize(V, fields, np.float32 if dtype == "f32" else np.float64, 12345)
+            self.U, self.v = f["U"], f.get("v")
+            self.ops = R
+            self.source = "port"
+            self.impl = "numpy restatement in oracle/ (bit-identical to su3bench), composed as SURVEY.md 8(c)"
+        nx, ny, nz, nt = self.dims
+        self.F = nx * ny * nz
+        self.s = self.U.dtype.type(1.0 / 6.0)
+
+    def _sh(self, f, k, mu, step):
+        nx, ny, nz, _ = self.dims
+        g = f.reshape((k, nz, ny, nx) + f.shape[1:])
+        return np.roll(g, -step, axis=3 - mu).reshape(f.shape)
+
+    def _slices(self, f, t, k):
+        nt, F = self.dims[3], self.F
+        if t + k <= nt and t >= 0:
+            return f[t * F : (t + k) * F]
+        return np.concatenate([f[((t + j) % nt) * F : ((t + j) % nt + 1) * F] for j in range(k)])
+
+    def __call__(self, t0: int, k: int):
+        o, F = self.ops, self.F
+        Uw = self._slices(self.U, t0, k)
+        if self.kind == "link":
+            Unext = self._slices(self.U, t0 + 1, k)
+            acc = np.zeros((k * F, 3, 3, 2), dtype=self.U.dtype)
+            for mu, nu in ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3)):
+                b = self._sh(Uw[:, nu], k, mu, +1)
+                c = self._sh(Uw[:, mu], k, nu, +1) if nu < 3 else Unext[:, mu]
+                acc = o.scalar_mult_add_su3_matrix(acc, o.mult_su3_na(o.mult_su3_nn(Uw[:, mu], b), c), self.s)
+            return acc
+        vw = self._slices(self.v, t0, k)
+        fw = [o.mult_su3_mat_vec(Uw[:, mu], self._sh(vw, k, mu, +1)) for mu in range(3)]
+        fw.append(o.mult_su3_mat_vec(Uw[:, 3], self._slices(self.v, t0 + 1, k)))
+        bw = [o.mult_adj_su3_mat_vec(self._sh(Uw[:, mu], k, mu, -1), self._sh(vw, k, mu, -1)) for mu in range(3)]
+        bw.append(o.mult_adj_su3_mat_vec(self._slices(self.U, t0 - 1, k)[:, 3], self._slices(self.v, t0 - 1, k)))
+        acc = o.add_su3_vector(o.add_su3_vector(o.add_su3_vector(fw[0], fw[1]), fw[2]), fw[3])
+        return o.sub_four_su3_vecs(acc, bw[0], bw[1], bw[2], bw[3])
+
+
+def _sample_slices(cfg) -> int:
+    """t-slices per timed call: about 1-3 s of single-core work on the full-size workloads."""
+    nx, ny, nz, nt = cfg["global_dims"]
+    per_slice = nx * ny * nz * (8 if cfg["kind"] == "link" else 1)
+    k = max(1, min(nt, (1 << 19) // max(per_slice, 1)))
+    while nt % k:
+        k -= 1
+    return k
+
+
+def _ref_routine_rate(cfg, dtype: str, budget_s: float):
+    """Per-routine streaming rows through su3bench.bench.run (backend 'vector', bench.py:229-271)."""
+    ref = _su3bench()
+    prec = "single" if dtype == "f32" else "double"
+    n = min(cfg["nsites"], 1 << 16)
+    dims = {4096: (8, 8, 8, 8), 65536: (16, 16, 16, 16)}.get(n, (16, 16, 16, 16))
+    V = int(np.prod(dims))
+    if ref is not None:
+        from su3bench.bench import BenchConfig, run
+
+        rec = run(BenchConfig(routine=cfg["routine"], backend="vector", precision=prec, mode="streaming", dims=dims,
+                              repetitions=1, warmup=3, min_region_s=budget_s))
+        return rec.invocations, rec.elapsed_s, "reference", (
+            f"su3bench.bench.run(BenchConfig(routine={cfg['routine']!r}, backend='vector', mode='streaming', "
+            f"dims={dims})) -- the reference's own streaming timer, pinned to one CPU")
     from oracle import routines as R
-    from oracle import sweeps as S
-    from paper_1309_0551_b200 import inputs
-
-    dt = np.float32 if dtype == "f32" else np.float64
-    rng = inputs.config_rng(424242)
-    if cfg["kind"] in ("nn", "dslash"):  # dslash: both parities = one NN application's site-ops
-        nx, ny, nz = cfg["global_dims"][:3]
-        if small:
-            nx, ny, nz = min(nx, 32), min(ny, 32), min(nz, 32)
-        dims = (nx, ny, nz, 4)
-        V = nx * ny * nz * 4
-        U = inputs.random_links(rng, V, 4, dtype=dt)
-        v = inputs.random_vectors(rng, V, None, dtype=dt)
-        return (lambda: S.nn_sweep(U, v, dims)), V, (dims, U, v), f"composed reference NN sweep on a {nx}x{ny}x{nz}x4 sample, 1 application"
-    if cfg["kind"] == "link":
-        dims = (48, 48, 8, 4)
-        V = int(np.prod(dims))
-        U = inputs.random_links(rng, V, 4, dtype=dt)
-        return (lambda: S.link_product(U, dims, 1 / 6)), V, (dims, U, None), "composed reference link product on a 48x48x8x4 sample"
     from paper_1309_0551_b200 import types as T
 
-    r = cfg["routine"]
-    n = min(cfg["nsites"], 1 << 18)
-    spec = T.routine_spec(r)
-    ops = []
-    for k in spec.operands:
-        if k == "scalar":
-            ops.append(dt(0.5))
-        elif k in ("mat", "mat4"):
-            ops.append(inputs.random_links(rng, n, None if k == "mat" else 4, dtype=dt))
-        else:
-            ops.append(rng.standard_normal((n,) + T.OPERAND_SHAPES[k]).astype(dt))
-    fn = R.ALL_ROUTINES[r]
-    return (lambda: fn(*ops)), n, None, f"reference {r} (numpy restatement) on {n} sites"
-
-
-def _parallel_nn(state, threads):
-    """The composed reference sweep split into t-slabs with explicit halos, one slab per host thread."""
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import routines as R
-    from oracle import sweeps as S
-
-    dims, U, v = state
-    nx, ny, nz, nt = dims
-    F = nx * ny * nz
-    parts = min(threads, nt)
-    while nt % parts:
-        parts -= 1
-
-    def one(r):
-        t0, t1 = S.slab_bounds(nt, parts, r)
-        nxt, prv = (t1 % nt) * F, ((t0 - 1) % nt) * F
-        w_lo = R.mult_adj_su3_mat_vec(U[prv : prv + F, 3], v[prv : prv + F])
-        return S.nn_sweep_slab(U[t0 * F : t1 * F], v[t0 * F : t1 * F], (nx, ny, nz, t1 - t0), v[nxt : nxt + F], w_lo)
-
-    with ThreadPoolExecutor(parts) as ex:
-        return list(ex.map(one, range(parts)))
-
-
-def cpu_baseline(args, cfg, threads=1, budget_s=10.0):
-    fn, sites, state, desc = _cpu_sample(cfg, args.dtype)
-    if threads > 1 and cfg["kind"] in ("nn", "dslash"):
-        def call():
-            return _parallel_nn(state, threads)
-    else:
-        threads = 1
-        call = fn
-    call()  # warm
-    n, t0 = 0, time.perf_counter()
-    while True:
-        call()
-        n += 1
+    rng = np.random.default_rng(12345)
+    dt = np.float32 if dtype == "f32" else np.float64
+    spec = T.routine_spec(cfg["routine"])
+    ops = [dt(0.5) if k == "scalar" else rng.uniform(-1, 1, (V,) + T.OPERAND_SHAPES[k]).astype(dt) for k in spec.operands]
+    fn = R.ALL_ROUTINES[cfg["routine"]]
+    with _Pinned():
+        fn(*ops)
+        n_calls, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < budget_s:
+            fn(*ops)
+            n_calls += 1
         el = time.perf_counter() - t0
-        if el >= budget_s or n >= 50:
-            break
+    return n_calls * V, el, "port", f"numpy restatement of {cfg['routine']} on {dims} ({V} sites), one CPU"
+
+
+def cpu_baseline(args, cfg, budget_s=12.0):
+    """The b200 line's cpu_baseline: the reference on one pinned core over a bounded sample (N=1, rank 0)."""
+    if cfg["kind"] == "routine":
+        ops, el, kind, desc = _ref_routine_rate(cfg, args.dtype, budget_s)
+        return {"value": ops / el, "unit": UNIT, "cores": 1, "kind": kind, "sample": desc, **_host_info()}
+    rs = RefSweep(cfg, args.dtype)
+    k = _sample_slices(cfg)
+    nt = cfg["global_dims"][3]
+    with _Pinned():
+        rs(0, k)  # warm
+        n, t = 0, time.perf_counter()
+        while True:
+            rs((n * k) % nt, k)
+            n += 1
+            el = time.perf_counter() - t
+            if el >= budget_s or n >= 50:
+                break
+    sites = n * k * rs.F
     return {
-        "value": sites * n / el,
-        "unit": UNIT,
-        "cores": threads,
-        "kind": "port",
-        "sample": f"{desc}; {n} calls in {el:.2f} s",
-        "host_cpus": os.cpu_count(),
+        "value": sites / el, "unit": UNIT, "cores": 1, "kind": rs.source,
+        "sample": (f"{rs.impl}; {n} calls of {k} output t-slice(s) each ({sites} site-ops) of the full "
+                   f"{'x'.join(map(str, cfg['global_dims']))} lattice in {el:.2f} s, one pinned CPU"),
         **_host_info(),
     }
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation on this box's host cores, on the b200 arm's
+    workload and metric.  Rank 0 alone runs it (the other ranks exit without work)."""
     cfg = workload_config(args, world)
     if rank != 0:
         return None
-    threads = os.cpu_count() or 1
-    fn, sites, state, desc = _cpu_sample(cfg, args.dtype, small=True)
-    call = (lambda: _parallel_nn(state, threads)) if cfg["kind"] in ("nn", "dslash") else fn
-    if cfg["kind"] not in ("nn", "dslash"):
-        threads = 1
-    for _ in range(args.warmup):
-        call()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        call()
-    el = time.perf_counter() - t0
-    value = sites * args.steps / el
-    return {
+    if cfg["kind"] == "routine":
+        budget = max(0.05, 20.0 / max(args.steps + args.warmup, 1))
+        tot_ops, tot_el = 0, 0.0
+        for i in range(args.warmup + args.steps):
+            ops, el, kind, desc = _ref_routine_rate(cfg, args.dtype, budget)
+            if i >= args.warmup:
+                tot_ops += ops
+                tot_el += el
+        value, el = tot_ops / tot_el, tot_el
+        sample, upper = desc + f"; {args.steps} timed calls", None
+    else:
+        rs = RefSweep(cfg, args.dtype)
+        kind = rs.source
+        k = _sample_slices(cfg)
+        nt = cfg["global_dims"][3]
+        with _Pinned():
+            for i in range(args.warmup):
+                rs((i * k) % nt, k)
+            t0 = time.perf_counter()
+            for i in range(args.steps):
+                rs((i * k) % nt, k)
+            el = time.perf_counter() - t0
+        value = args.steps * k * rs.F / el
+        sample = (f"{rs.impl}; each step = {k} output t-slice(s) ({k * rs.F} site-ops) of the full "
+                  f"{'x'.join(map(str, cfg['global_dims']))} lattice, windows cycling over t; one pinned CPU "
+                  f"(the reference is single-threaded numpy)")
+        upper = _upper_bound_aggregate(rs, cfg)
+    line = {
         "metric": METRIC,
         "value": value,
         "unit": UNIT,
@@ -915,21 +1150,69 @@ def run_reference(args, rank, world):
         "warmup": args.warmup,
         "ms_per_step": el * 1e3 / args.steps,
         "higher_is_better": True,
-        "scaling": "weak" if args.workload == "nn-weak" else "strong",
+        "scaling": "weak" if args.workload == "nn-weak" else ("strong" if args.workload == "nn-strong" else "weak"),
         "vs_baseline": None,
         "dtype": args.dtype,
-        "data": "synthetic (seeded SU(3) links + complex-Gaussian vectors)",
-        "config": {"workload": cfg["name"], "lattice": list(cfg.get("global_dims", [])) or None},
+        "data": "synthetic (the reference's SiteBuffer.randomize uniform fields; timing is value-independent)",
+        "config": {"workload": cfg["name"], "lattice": list(cfg.get("global_dims", [])) or None,
+                   "same_config": not args.dims},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{desc} per step; reference association (numpy restatement pinned bitwise to su3bench)",
-                         "host_cpus": os.cpu_count(), **_host_info()},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample, **_host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if upper is not None:
+        line["upper_bound_aggregate"] = upper
+    return line
+
+
+def _upper_bound_aggregate(rs, cfg, max_s=20.0):
+    """All host threads on disjoint t-windows at once -- labelled an upper bound, NOT the reference
+    (which is one single-threaded process); numpy releases the GIL inside its loops."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    threads = os.cpu_count() or 1
+    nt = cfg["global_dims"][3]
+    k = _sample_slices(cfg)
+    windows = [(t, k) for t in range(0, nt, k)]
+    if len(windows) < threads:
+        k1 = max(1, nt // threads)
+        while nt % k1:
+            k1 -= 1
+        windows = [(t, k1) for t in range(0, nt, k1)]
+    with ThreadPoolExecutor(threads) as ex:
+        t0 = time.perf_counter()
+        done = 0
+        for _ in ex.map(lambda w: rs(*w), windows):
+            done += 1
+            if time.perf_counter() - t0 > max_s:
+                break
+        el = time.perf_counter() - t0
+    sites = sum(w[1] for w in windows[:done]) * rs.F
+    return {"value": sites / el, "unit": UNIT, "threads": threads, "kind": rs.source,
+            "label": "upper bound: all host threads on disjoint t-windows of one lattice pass; not the reference's "
+                     "configuration (single-threaded)"}
+
+
+def _spawn_ranks(args, argv) -> int:
+    """--gpus N > 1 without a torch.distributed launcher: start the N ranks here (one process per GPU)
+    with torch.distributed.run on 127.0.0.1, and return its exit code.  Rank 0 prints the line."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ, SU3G_BENCH_SPAWNED="1")
+    return subprocess.call(cmd, env=env)
 
 
 def main(argv=None):
+    argv = sys.argv[1:] if argv is None else list(argv)
     args = parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not os.environ.get("SU3G_BENCH_SPAWNED"):
+        raise SystemExit(_spawn_ranks(args, argv))
     rank, world, local = init_dist(args)
     if args.impl == "reference":
         line = run_reference(args, rank, world)

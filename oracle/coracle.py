@@ -58,6 +58,9 @@ def lib():
             f = getattr(_lib, f"su3o_nn_sweep_{sfx}")
             f.argtypes = [vp, vp, vp, i64, i64, i64, i64]
             f.restype = ctypes.c_int
+            f = getattr(_lib, f"su3o_nn_sweep_slab_{sfx}")
+            f.argtypes = [vp, vp, vp, vp, vp, i64, i64, i64, i64]
+            f.restype = ctypes.c_int
             f = getattr(_lib, f"su3o_link_product_{sfx}")
             f.argtypes = [vp, vp, i64, i64, i64, i64, real]
             f.restype = ctypes.c_int
@@ -100,6 +103,16 @@ def nn_sweep(U, v, dims):
     U, v = _c(U), _c(v)
     out = np.empty_like(v)
     rc = getattr(lib(), f"su3o_nn_sweep_{_sfx(U.dtype)}")(U.ctypes.data, v.ctypes.data, out.ctypes.data, *dims)
+    assert rc == 0
+    return out
+
+
+def nn_sweep_slab(U, v, dims_local, v_hi, w_lo):
+    """One rank's t-slab (oracle.sweeps.nn_sweep_slab in C): v_hi, w_lo are AoS (F, 3, 2) faces."""
+    U, v, v_hi, w_lo = _c(U), _c(v), _c(v_hi), _c(w_lo)
+    out = np.empty_like(v)
+    rc = getattr(lib(), f"su3o_nn_sweep_slab_{_sfx(U.dtype)}")(
+        U.ctypes.data, v.ctypes.data, v_hi.ctypes.data, w_lo.ctypes.data, out.ctypes.data, *dims_local)
     assert rc == 0
     return out
 

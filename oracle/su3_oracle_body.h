@@ -144,6 +144,36 @@ int FN(su3o_nn_sweep)(const REAL *U, const REAL *v, REAL *out, int64_t nx, int64
     return 0;
 }
 
+/* One t-slab of the NN sweep: x, y, z periodic in the slab; the +t neighbour of the
+ * last slice is v_hi (the next rank's first slice of v, AoS (F,3,2)); the -t backward term of the first
+ * slice is w_lo = U_t(x)^dag v(x) on the previous rank's last slice (AoS (F,3,2)), formed by that rank
+ * with the same adj_mat_vec -- so the result equals the unsharded sweep's rows bit for bit. */
+int FN(su3o_nn_sweep_slab)(const REAL *U, const REAL *v, const REAL *v_hi, const REAL *w_lo, REAL *out, int64_t nx,
+                           int64_t ny, int64_t nz, int64_t nt) {
+    const int64_t dims[4] = {nx, ny, nz, nt};
+    const int64_t F = nx * ny * nz, V = F * nt;
+#pragma omp parallel for schedule(static)
+    for (int64_t s = 0; s < V; ++s) {
+        REAL fw[4][6], bw[4][6];
+        const int64_t t = s / F, s3 = s % F;
+        for (int mu = 0; mu < 4; ++mu) {
+            int64_t up = FN(nbr)(s, mu, +1, dims), dn = FN(nbr)(s, mu, -1, dims);
+            const REAL *vu = (mu == 3 && t == nt - 1) ? v_hi + s3 * 6 : v + up * 6;
+            FN(mat_vec)(U + (s * 4 + mu) * 18, vu, fw[mu]);
+            if (mu == 3 && t == 0) {
+                for (int k = 0; k < 6; ++k) bw[mu][k] = w_lo[s3 * 6 + k];
+            } else {
+                FN(adj_mat_vec)(U + (dn * 4 + mu) * 18, v + dn * 6, bw[mu]);
+            }
+        }
+        for (int k = 0; k < 6; ++k) {
+            REAL f = ((fw[0][k] + fw[1][k]) + fw[2][k]) + fw[3][k];
+            out[s * 6 + k] = (((f - bw[0][k]) - bw[1][k]) - bw[2][k]) - bw[3][k];
+        }
+    }
+    return 0;
+}
+
 /* link product: acc = smadd(acc, na(nn(U_mu(x), U_nu(x+mu)), U_mu(x+nu)), s) */
 int FN(su3o_link_product)(const REAL *U, REAL *acc, int64_t nx, int64_t ny, int64_t nz, int64_t nt, REAL s) {
     static const int pairs[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};

@@ -174,8 +174,13 @@ class Field:
         if device is None:
             device = t.device if t.is_cuda else torch.device("cuda", torch.cuda.current_device())
         src = t.to(device).contiguous()
-        if out is not None and out.layout != "soa":
-            raise ValueError("from_aos writes the t-sliced SoA layout; convert with .to_eo() afterwards")
+        if src.dtype not in _SFX:
+            raise ValueError(f"unsupported dtype {src.dtype}")
+        if out is not None:
+            if out.layout != "soa":
+                raise ValueError("from_aos writes the t-sliced SoA layout; convert with .to_eo() afterwards")
+            if out.lattice != lattice or out.kind != kind or out.dtype != src.dtype or out.device != src.device:
+                raise ValueError(f"out must be a {kind!r} field on {lattice.dims} with dtype {src.dtype} on {src.device}")
         f = out if out is not None else cls(lattice, kind, src.dtype, device)
         _lib.call(
             f"su3g_aos_to_soa_{_SFX[f.dtype]}", src.data_ptr(), f.data.data_ptr(), lattice.slice_sites, lattice.nt,
@@ -190,6 +195,9 @@ class Field:
         shape = (self.lattice.volume,) + OPERAND_SHAPES[self.kind]
         if out is None:
             out = torch.empty(shape, dtype=self.dtype, device=self.device)
+        elif (tuple(out.shape) != shape or out.dtype != self.dtype or not out.is_contiguous()
+              or out.device != self.device):
+            raise ValueError(f"out must be a contiguous {shape} tensor of dtype {self.dtype} on {self.device}")
         _lib.call(
             f"su3g_soa_to_aos_{_SFX[self.dtype]}", self.data.data_ptr(), out.data_ptr(), self.lattice.slice_sites,
             self.lattice.nt, self.reals, torch.cuda.current_stream(self.device).cuda_stream,

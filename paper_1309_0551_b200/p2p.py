@@ -79,17 +79,34 @@ class P2PSlabSweep:
 
             dist.barrier(group=self.group)
 
+    def _needs_prime(self, v: Field) -> bool:
+        """Whether v is a fresh source -- decided collectively: if any rank must prime, every rank
+        primes (a per-rank pointer test could diverge when the allocator hands one rank a fresh v at
+        the address of its previous out, and the epochs would then drift apart)."""
+        need = self._primed_for != v.data.data_ptr()
+        if self.dist and self.world > 1:
+            import torch.distributed as dist
+
+            flag = torch.tensor([int(need)], dtype=torch.int32, device=self.U.device)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=self.group)
+            need = bool(flag.item())
+        return need
+
     def invalidate(self) -> None:
         """Forget the in-flight halos: call after writing a source field in place."""
         self._primed_for = None
 
-    def apply(self, v: Field, out: Field) -> Field:
+    def apply(self, v: Field, out: Field, chain: bool | None = None) -> Field:
         """out = D v for this rank's slab (collective: every rank calls it in the same order).
 
         Consecutive calls that feed one call's ``out`` back as the next ``v`` need no
         priming: the boundary kernel already pushed those halos.  Any other source is
         primed first (host barrier + su3g_p2p_prime); if ``out`` was modified in place
         before being fed back, call ``invalidate()`` first.
+
+        ``chain`` makes the decision explicit and identical on every rank: True = v is the
+        previous call's out (raises if it is not), False = prime.  None decides collectively
+        (an all-reduce over the ranks, one host round trip per call).
         """
         if v.kind != "vec" or out.kind != "vec" or v.lattice != self.U.lattice or v.dtype != self.U.dtype:
             raise ValueError("v and out must be 'vec' fields on U's slab lattice and dtype")
@@ -98,7 +115,15 @@ class P2PSlabSweep:
         stream = torch.cuda.current_stream(self.U.device).cuda_stream
         me = ctypes.c_void_p(self.window.data_ptr())
         lo, hi = ctypes.c_void_p(self.win_lo), ctypes.c_void_p(self.win_hi)
-        if self._primed_for != v.data.data_ptr():
+        if chain is None:
+            prime = self._needs_prime(v)
+        elif chain:
+            if self._primed_for != v.data.data_ptr():
+                raise ValueError("chain=True, but v is not the previous application's out (or was invalidated)")
+            prime = False
+        else:
+            prime = True
+        if prime:
             # fresh source: all ranks' earlier launches must be done before the windows are rewritten,
             # and the epoch skips ahead so no stale flag can satisfy the next wait
             self._barrier()
@@ -115,10 +140,16 @@ class P2PSlabSweep:
         """v <- D v `applications` times (ping-pong); the initial v is always primed as a fresh source."""
         self.invalidate()
         a, b = v, (scratch if scratch is not None else v.empty_like())
-        for _ in range(applications):
-            self.apply(a, b)
+        for i in range(applications):
+            self.apply(a, b, chain=i > 0)
             a, b = b, a
+        self.check()
         return a
+
+    def check(self) -> None:
+        """Raise if a halo wait timed out (the boundary kernel's bounded spin set the error word)."""
+        if self.error():
+            raise RuntimeError("P2P halo exchange: a flag wait timed out (protocol failure); results are invalid")
 
     def error(self) -> int:
         """The window's error word: 1 if a halo wait timed out (protocol failure), else 0."""

@@ -44,6 +44,25 @@ def _need_soa(what: str, *fields) -> None:
         raise ValueError(f"{what} works on t-sliced SoA fields; convert checkerboarded fields with .to_soa()")
 
 
+def _check_face(what: str, name: str, face, lat: Lattice4D, dtype, device) -> None:
+    """A t-slab halo face must be a contiguous (6, F) tensor of the field dtype on the field's device."""
+    if face is None:
+        return
+    F = lat.slice_sites
+    if (not isinstance(face, torch.Tensor) or tuple(face.shape) != (6, F) or face.dtype != dtype
+            or not face.is_contiguous() or face.device != device):
+        raise ValueError(f"{what}: {name} must be a contiguous (6, {F}) {dtype} tensor on {device}")
+
+
+def _check_vec_out(what: str, v: Field, out: Field | None) -> None:
+    if out is None:
+        return
+    if out.kind != "vec" or out.lattice != v.lattice or out.dtype != v.dtype or out.device != v.device:
+        raise ValueError(f"{what}: out must be a 'vec' field on v's lattice, dtype and device")
+    if out.data.data_ptr() == v.data.data_ptr():
+        raise ValueError(f"{what}: out must not alias v")
+
+
 def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=None, w_lo=None,
              mode: str = "exact") -> Field:
     """One application of D on the slices t in t_range (default: all).
@@ -58,6 +77,9 @@ def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=No
     _need_soa("nn_sweep", U, v, out)
     if U.lattice != v.lattice or U.dtype != v.dtype:
         raise ValueError("U and v must share lattice and dtype")
+    _check_vec_out("nn_sweep", v, out)
+    _check_face("nn_sweep", "v_hi", v_hi, U.lattice, U.dtype, U.device)
+    _check_face("nn_sweep", "w_lo", w_lo, U.lattice, U.dtype, U.device)
     if out is None:
         out = v.empty_like()
     lat = U.lattice
@@ -72,6 +94,11 @@ def nn_sweep(U: Field, v: Field, out: Field | None = None, t_range=None, v_hi=No
 def nn_halo_w(U: Field, v: Field, w_face: torch.Tensor, mode: str = "exact") -> torch.Tensor:
     """w = U_t^dag v on the last local t-slice -> (6, F) SoA face (sent to the +t neighbour)."""
     _need_soa("nn_halo_w", U, v)
+    if U.kind != "mat4" or v.kind != "vec" or U.lattice != v.lattice or U.dtype != v.dtype:
+        raise ValueError("nn_halo_w needs U ('mat4') and v ('vec') on one lattice and dtype")
+    _check_face("nn_halo_w", "w_face", w_face, U.lattice, U.dtype, U.device)
+    if w_face is None:
+        raise ValueError("nn_halo_w: w_face is required")
     lat = U.lattice
     _lib.call(
         f"su3g_nn_halo_w_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), w_face.data_ptr(),
@@ -87,6 +114,11 @@ def nn_edges(U: Field, v: Field, out: Field, v_hi=None, w_lo=None, w_next: torch
     if U.kind != "mat4" or v.kind != "vec" or out.kind != "vec":
         raise ValueError("nn_edges needs U of kind 'mat4' and v, out of kind 'vec'")
     _need_soa("nn_edges", U, v, out)
+    if U.lattice != v.lattice or U.dtype != v.dtype:
+        raise ValueError("U and v must share lattice and dtype")
+    _check_vec_out("nn_edges", v, out)
+    for name, face in (("v_hi", v_hi), ("w_lo", w_lo), ("w_next", w_next)):
+        _check_face("nn_edges", name, face, U.lattice, U.dtype, U.device)
     lat = U.lattice
     _lib.call(
         f"su3g_nn_sweep_edges_{_SFX[U.dtype]}", U.data.data_ptr(), v.data.data_ptr(), out.data.data_ptr(),
