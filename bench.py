@@ -296,28 +296,31 @@ def run_b200(args, rank, world, local):
         U = Field.from_aos(lat, "mat4", U_aos)
         v0 = Field.from_aos(lat, "vec", v_aos)
         va, vb = v0.empty_like(), v0.empty_like()
-        va.data.copy_(v0.data)
         ntl = lat.nt
         apps = cfg["apps"]
+        # one step = `apps` chained applications v <- D v starting from the step's input field v0 (never
+        # overwritten): the first reads v0, the rest ping-pong between va and vb.  Starting every step
+        # from v0 keeps the values finite (|D| ~ 10: 10 applications, not thousands, compound).
+        last = [v0]
         if args.halo == "p2p":
             from paper_1309_0551_b200.p2p import P2PSlabSweep
 
             p2p = P2PSlabSweep(U, mode=args.mode)
             per_launch_sites = lat.volume  # timed unit: one application (boundary + interior launches)
             launches_per_app = 2 if ntl > 2 else 1
+            extra_launches = 1  # the first application of a step primes the halos of the fresh source
 
-            p2p_chained = [False]
-
-            def step(record=False):
-                nonlocal va, vb
-                for _ in range(apps):
+            def run_step(record=False):
+                src = v0
+                for i in range(apps):
+                    dst = va if i % 2 == 0 else vb
                     if record:
                         with _EventTimer(stream, dominant_events):
-                            p2p.apply(va, vb, chain=p2p_chained[0])
+                            p2p.apply(src, dst, chain=i > 0)
                     else:
-                        p2p.apply(va, vb, chain=p2p_chained[0])
-                    p2p_chained[0] = True
-                    va, vb = vb, va
+                        p2p.apply(src, dst, chain=i > 0)
+                    src = dst
+                last[0] = src
         else:
             slab = SlabSweep(U, kernels=CudaSlabKernels(args.mode))
             if world == 1:
@@ -325,42 +328,45 @@ def run_b200(args, rank, world, local):
             else:
                 per_launch_sites = max(ntl - 2, 0) * lat.slice_sites
             launches_per_app = slab.launches_per_apply(chained=True)  # steady state: the halo pack is fused
-            chained = [False]  # va is the previous application's out from the second application on
+            extra_launches = slab.launches_per_apply(chained=False) - launches_per_app  # first application's pack
 
-            def step(record=False):
-                nonlocal va, vb
-                for _ in range(apps):
-                    slab.apply(va, vb, timer=(lambda: _EventTimer(stream, dominant_events)) if record else None,
-                               chain=chained[0])
-                    chained[0] = True
-                    va, vb = vb, va
+            def run_step(record=False):
+                src = v0
+                for i in range(apps):
+                    dst = va if i % 2 == 0 else vb
+                    slab.apply(src, dst, timer=(lambda: _EventTimer(stream, dominant_events)) if record else None,
+                               chain=i > 0)
+                    src = dst
+                last[0] = src
+
+        def step(record=False):
+            run_step(record)
+
         bytes_per_launch = per_launch_sites * NN_BYTES[args.dtype]
 
         def parity_fn():
-            """One more application of the timed path (chained, as in the steady state) from the current
-            field, against the C oracle on every rank's slab (halo faces from the neighbour ranks)."""
+            """One step of the timed path (all `apps` chained applications from v0), against the C oracle
+            iterated as many times on every rank's slab (halo faces from the neighbour ranks)."""
             from oracle import coracle
 
-            out = va.empty_like()
+            run_step()
             if args.halo == "p2p":
-                p2p.apply(va, out, chain=True)
                 p2p.check()
-            else:
-                slab.apply(va, out, chain=True)
             torch.cuda.synchronize(dev)
-            U_h, v_h, got = U.numpy(), va.numpy(), out.numpy()
-            if world == 1:
-                want = coracle.nn_sweep(U_h, v_h, lat.dims)
-            else:
-                F = lat.slice_sites
-                w_last = coracle.routine("mult_adj_su3_mat_vec", U_h[-F:, 3], v_h[-F:])
-                v_hi, w_lo = _exchange_faces(v_h[:F], w_last, rank, world, dev)
-                want = coracle.nn_sweep_slab(U_h, v_h, lat.dims, v_hi, w_lo)
-            return got, want, (f"one application of the timed path (chained) on every rank's full "
-                               f"{'x'.join(map(str, lat.dims))} slab, vs the C oracle "
+            U_h, want, got = U.numpy(), v0.numpy(), last[0].numpy()
+            F = lat.slice_sites
+            for _ in range(apps):
+                if world == 1:
+                    want = coracle.nn_sweep(U_h, want, lat.dims)
+                else:
+                    w_last = coracle.routine("mult_adj_su3_mat_vec", U_h[-F:, 3], want[-F:])
+                    v_hi, w_lo = _exchange_faces(want[:F], w_last, rank, world, dev)
+                    want = coracle.nn_sweep_slab(U_h, want, lat.dims, v_hi, w_lo)
+            return got, want, (f"one timed step ({apps} chained applications from the step's input) on every "
+                               f"rank's full {'x'.join(map(str, lat.dims))} slab, vs the C oracle iterated "
                                f"({'periodic sweep' if world == 1 else 'slab with the neighbours halo faces'})")
 
-        launches_per_step = apps * launches_per_app
+        launches_per_step = apps * launches_per_app + extra_launches
         sites_per_step = lat.volume * apps  # per rank
         del U_aos
     elif cfg["kind"] == "dslash":
@@ -541,7 +547,7 @@ def run_b200(args, rank, world, local):
     if cfg["kind"] == "nn" and args.halo == "p2p":
         dispatched = "k_p2p_boundary + interior " + dispatched + " (timed together, per application)"
     elif cfg["kind"] == "nn" and world > 1:
-        dispatched = "interior: " + _interior_kernel(sweeps, U, va, vb, lat.nt, args.mode)
+        dispatched = "interior: " + _interior_kernel(sweeps, U, v0, vb, lat.nt, args.mode)
     clocks = ClockSampler(local)
     barrier(world, dev)
     torch.cuda.synchronize(dev)

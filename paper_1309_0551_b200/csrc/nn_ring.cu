@@ -1,0 +1,373 @@
+// NN sweep, warp-specialised TMA ring t-walk (the f64 production path on B200).
+//
+// Why a second t-walk kernel: the f32 walk (nn_tma.cu) stages a whole step -- the block's
+// links, v(t+1) and the halo rows -- per ring stage; at f64 two such stages plus the
+// exchange buffer do not fit 227 KB.  This kernel moves the same bytes through a ring of
+// small, equal-sized slots, one per "chunk" of a step, so the ring is as deep as shared
+// memory allows at any precision:
+//
+//   chunk 0  H1  v(x,t+1) of the block [6][N] | v on the +y halo row [6][H] | U_y on the -y row [18][H]
+//   chunk 1  H2  v on the -y row [6][H] | U_z on the -z row [18][H] | v on the -z row [6][H] | v +z [6][H]
+//   chunk 2-5    U_x, U_y, U_z, U_t of the block [18][N] each
+//
+// (block = NX x 2 x 2 sites, N = 4 NX compute threads, halo rows H = 2 NX = N/2 sites, so every
+// chunk is exactly 18 N reals).  One producer warp issues the 4-D TMA boxes into the ring
+// (full/empty mbarrier pairs); each compute warp releases a slot as soon as its lanes have
+// copied what they need into registers.  Links are never shared between sites, so a slot
+// lives only for the few hundred cycles it takes to read it, and the bytes in flight are the
+// whole ring minus one slot.
+//
+// Per step (site x of the block, slice t): the halo rows' backward half-products
+// w = U^dag v go to the exchange (XH, one halo site per thread); w_x, w_y, w_z of every
+// site go to XW; v(x,t+1) goes to the double-buffered XV, from which the next step reads
+// its in-block forward neighbours.  The -t term w_t and v(t+1) stay in registers.  Two
+// named barriers per step (XW / XH are single-buffered).  Work items (block, t-chunk) are
+// ordered chunk-major over one persistent wave, as in nn_tma.cu.
+//
+// The per-site arithmetic and its order are those of nn_site (the composed reference,
+// SURVEY.md 8(c)): bit-identical results in exact mode.
+#include <algorithm>
+#include <string>
+
+#include "nn_site.cuh"
+#include "tma.cuh"
+
+namespace su3g {
+
+namespace {
+
+struct RingParams {
+    int ny, nz, nt;
+    int64_t F;
+    int nby;         // ny / 2
+    int64_t nblocks;
+    int t_begin, t_end;
+    int chunk;       // t-chunk length of one work item
+    int64_t nitems;  // nblocks * ceil((t_end - t_begin) / chunk), chunk-major
+    int has_vhi;
+};
+
+template <int NX>
+struct RingGeo {
+    static constexpr int N = 4 * NX;  // block sites = compute threads
+    static constexpr int H = 2 * NX;  // sites of one halo row (y or z)
+    static constexpr int SLOT = 18 * N;
+    // H1
+    static constexpr int H1_V = 0, H1_VYU = 6 * N, H1_UYD = 6 * N + 6 * H;
+    // H2
+    static constexpr int H2_VYD = 0, H2_UZD = 6 * H, H2_VZD = 24 * H, H2_VZU = 30 * H;
+    // exchange
+    static constexpr int XW = 0;               // [18][N]
+    static constexpr int XH = 18 * N;          // [6][2H]: -y halo sites, then -z halo sites
+    static constexpr int XV = 18 * N + 12 * H; // [2][6][N]
+    static constexpr int XSIZE = XV + 12 * N;
+};
+
+__device__ __forceinline__ void item_of(const RingParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
+    const int64_t ch = item / p.nblocks;
+    blk = item - ch * p.nblocks;
+    t0 = p.t_begin + static_cast<int>(ch) * p.chunk;
+    t1 = min(t0 + p.chunk, p.t_end);
+}
+
+}  // namespace
+
+template <typename T, bool FUSED, int NX, int S>
+__global__ void __launch_bounds__(4 * NX + 32, 1)
+    k_nn_ring(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
+              const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
+              const __grid_constant__ CUtensorMap mapUzH, const __grid_constant__ CUtensorMap mapVyH,
+              const __grid_constant__ CUtensorMap mapVzH, const T* __restrict__ U, const T* __restrict__ v,
+              T* __restrict__ out, const T* __restrict__ w_lo, RingParams p) {
+    using G = RingGeo<NX>;
+    constexpr int N = G::N, H = G::H, NW = N / 32;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* ring = reinterpret_cast<T*>(smem_raw);
+    T* xb = ring + S * G::SLOT;
+    uint64_t* full = reinterpret_cast<uint64_t*>(xb + G::XSIZE);
+    uint64_t* empty = full + S;
+
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int64_t F = p.F;
+    const int G_ = gridDim.x;
+
+    // ------------------------------------------------------------------ producer warp
+    if (tid >= N) {
+        if (tid != N) return;
+        uint64_t pol_first, pol_normal;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_normal));
+        uint32_t q = 0;
+        for (int64_t item = blockIdx.x; item < p.nitems; item += G_) {
+            int64_t blk;
+            int t0, t1;
+            item_of(p, item, blk, t0, t1);
+            const int y0 = static_cast<int>(blk % p.nby) * 2, z0 = static_cast<int>(blk / p.nby) * 2;
+            const int ydn = (y0 + p.ny - 1) % p.ny, yup = (y0 + 2) % p.ny;
+            const int zdn = (z0 + p.nz - 1) % p.nz, zup = (z0 + 2) % p.nz;
+            for (int t = t0; t < t1; ++t) {
+#pragma unroll 1
+                for (int c = 0; c < 6; ++c, ++q) {
+                    const int s = static_cast<int>(q % S);
+                    if (q >= S) mbar_wait(&empty[s], ((q / S) + 1) & 1);
+                    T* dst = ring + s * G::SLOT;
+                    mbar_arrive_expect_tx(&full[s], uint32_t(G::SLOT) * sizeof(T));
+                    if (c == 0) {
+                        if (t + 1 < p.nt) tma_load_4d(dst + G::H1_V, &mapV, 0, y0, z0, (t + 1) * 6, &full[s], pol_normal);
+                        else if (p.has_vhi) tma_load_4d(dst + G::H1_V, &mapVhi, 0, y0, z0, 0, &full[s], pol_normal);
+                        else tma_load_4d(dst + G::H1_V, &mapV, 0, y0, z0, 0, &full[s], pol_normal);
+                        tma_load_4d(dst + G::H1_VYU, &mapVyH, 0, yup, z0, t * 6, &full[s], pol_normal);
+                        tma_load_4d(dst + G::H1_UYD, &mapUyH, 0, ydn, z0, t * 72 + 18, &full[s], pol_normal);
+                    } else if (c == 1) {
+                        tma_load_4d(dst + G::H2_VYD, &mapVyH, 0, ydn, z0, t * 6, &full[s], pol_normal);
+                        tma_load_4d(dst + G::H2_UZD, &mapUzH, 0, y0, zdn, t * 72 + 36, &full[s], pol_normal);
+                        tma_load_4d(dst + G::H2_VZD, &mapVzH, 0, y0, zdn, t * 6, &full[s], pol_normal);
+                        tma_load_4d(dst + G::H2_VZU, &mapVzH, 0, y0, zup, t * 6, &full[s], pol_normal);
+                    } else {
+                        // U_x and U_t are read exactly once; U_y / U_z are re-read as halo rows by
+                        // the neighbouring blocks in flight at the same time
+                        const int mu = c - 2;
+                        tma_load_4d(dst, &mapU, 0, y0, z0, t * 72 + 18 * mu, &full[s],
+                                    (mu == 1 || mu == 2) ? pol_normal : pol_first);
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------------ compute warps
+    const int lane = tid & 31;
+    const int lx = tid % NX, ly = (tid / NX) & 1, lz = tid / (2 * NX);
+    const int ix_up = (lx + 1 == NX) ? tid - lx : tid + 1;
+    const int ix_dn = (lx == 0) ? tid + NX - 1 : tid - 1;
+    const int jy = lx + NX * lz;  // this column's slot in a y halo row (box x, z)
+    const int jz = lx + NX * ly;  // ... in a z halo row (box x, y)
+    T* XW = xb + G::XW;
+    T* XH = xb + G::XH;
+    T* XV = xb + G::XV;
+
+    uint32_t q = 0;
+    uint32_t k = 0;  // steps done by this CTA (XV parity)
+    for (int64_t item = blockIdx.x; item < p.nitems; item += G_) {
+        int64_t blk;
+        int t0, t1;
+        item_of(p, item, blk, t0, t1);
+        const int y = static_cast<int>(blk % p.nby) * 2 + ly;
+        const int z = static_cast<int>(blk / p.nby) * 2 + lz;
+        const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
+        // prologue: v(x,t0) and the -t half-product w_t(x,t0-1)
+        T vc[6], wt[6];
+        ld_soa<T, 6>(v + int64_t(t0) * 6 * F, F, s3, vc);
+        if (t0 == 0 && w_lo != nullptr) {
+            ld_soa<T, 6>(w_lo, F, s3, wt);
+        } else {
+            const int tp = (t0 > 0) ? t0 - 1 : p.nt - 1;
+            T u[18], vp[6];
+            ld_soa<T, 18>(U + (int64_t(tp) * 72 + 54) * F, F, s3, u);
+            ld_soa<T, 6>(v + int64_t(tp) * 6 * F, F, s3, vp);
+            amv<T, FUSED>(u, vp, wt);
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) XV[((k & 1) * 6 + c) * N + tid] = vc[c];
+        named_sync<N>();
+
+        for (int t = t0; t < t1; ++t, ++k) {
+            const T* xv = XV + (k & 1) * 6 * N;
+            T vnext[6], nby_[6], nbz_[6];
+            // ---- H1, H2: v(t+1), the +y / +z halo v this column needs, the halo half-products
+            {
+                const int s1 = static_cast<int>(q % S), s2 = static_cast<int>((q + 1) % S);
+                mbar_wait(&full[s1], (q / S) & 1);
+                mbar_wait(&full[s2], ((q + 1) / S) & 1);
+                const T* h1 = ring + s1 * G::SLOT;
+                const T* h2 = ring + s2 * G::SLOT;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    vnext[c] = h1[G::H1_V + c * N + tid];
+                    nby_[c] = h1[G::H1_VYU + c * H + jy];
+                    nbz_[c] = h2[G::H2_VZU + c * H + jz];
+                }
+                T uh[18], vh[6], wh[6];
+                if (tid < H) {  // -y halo site tid
+#pragma unroll
+                    for (int c = 0; c < 18; ++c) uh[c] = h1[G::H1_UYD + c * H + tid];
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) vh[c] = h2[G::H2_VYD + c * H + tid];
+                } else {        // -z halo site tid - H
+#pragma unroll
+                    for (int c = 0; c < 18; ++c) uh[c] = h2[G::H2_UZD + c * H + (tid - H)];
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) vh[c] = h2[G::H2_VZD + c * H + (tid - H)];
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty[s1]);
+                    mbar_arrive(&empty[s2]);
+                }
+                amv<T, FUSED>(uh, vh, wh);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) XH[c * (2 * H) + tid] = wh[c];
+            }
+            // ---- U_x, U_y, U_z: publish w_mu, forward term U_mu(x) v(x+mu)
+            T acc[6];
+#pragma unroll
+            for (int mu = 0; mu < 3; ++mu) {
+                const uint32_t qq = q + 2 + mu;
+                const int s = static_cast<int>(qq % S);
+                mbar_wait(&full[s], (qq / S) & 1);
+                const T* su = ring + s * G::SLOT;
+                T u[18];
+#pragma unroll
+                for (int c = 0; c < 18; ++c) u[c] = su[c * N + tid];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                T w[6], nb[6], f[6];
+                amv<T, FUSED>(u, vc, w);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) XW[(6 * mu + c) * N + tid] = w[c];
+                const int src = mu == 0 ? ix_up : (mu == 1 ? (ly == 0 ? tid + NX : -1) : (lz == 0 ? tid + 2 * NX : -1));
+                if (src >= 0) {
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) nb[c] = xv[c * N + src];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) nb[c] = mu == 1 ? nby_[c] : nbz_[c];
+                }
+                mv<T, FUSED>(u, nb, f);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) acc[c] = (mu == 0) ? f[c] : xadd(acc[c], f[c]);
+            }
+            // ---- U_t: -t term of the next step, forward +t term (summed last)
+            T wt_next[6];
+            {
+                const uint32_t qq = q + 5;
+                const int s = static_cast<int>(qq % S);
+                mbar_wait(&full[s], (qq / S) & 1);
+                const T* su = ring + s * G::SLOT;
+                T u[18], f[6];
+#pragma unroll
+                for (int c = 0; c < 18; ++c) u[c] = su[c * N + tid];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                amv<T, FUSED>(u, vc, wt_next);
+                mv<T, FUSED>(u, vnext, f);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) acc[c] = xadd(acc[c], f[c]);
+            }
+            q += 6;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) XV[(((k + 1) & 1) * 6 + c) * N + tid] = vnext[c];
+            named_sync<N>();
+
+            // ---- backward terms (sub_four_su3_vecs chain)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) acc[c] = xsub(acc[c], XW[c * N + ix_dn]);
+            {
+                const T* b = ly == 1 ? XW + 6 * N + tid - NX : XH + jy;
+                const int bs = ly == 1 ? N : 2 * H;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) acc[c] = xsub(acc[c], b[c * bs]);
+                b = lz == 1 ? XW + 12 * N + tid - 2 * NX : XH + H + jz;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) acc[c] = xsub(acc[c], b[c * bs]);
+            }
+#pragma unroll
+            for (int c = 0; c < 6; ++c) acc[c] = xsub(acc[c], wt[c]);
+            T* o = out + int64_t(t) * 6 * F + s3;
+#pragma unroll
+            for (int c = 0; c < 6; ++c) __stcs(o + c * F, acc[c]);
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                vc[c] = vnext[c];
+                wt[c] = wt_next[c];
+            }
+            named_sync<N>();  // XW / XH are rewritten by the next step
+        }
+    }
+}
+
+template <typename T, bool FUSED, int NX, int S>
+static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
+                    const T* v_hi, const T* w_lo, cudaStream_t st) {
+    using G = RingGeo<NX>;
+    CUtensorMap mU, mV, mVhi, mUy, mUz, mVy, mVz;
+    if (!make_map<T>(&mU, U, nx, ny, nz, int64_t(nt) * 72, 2, 2, 18)) return 1;
+    if (!make_map<T>(&mV, v, nx, ny, nz, int64_t(nt) * 6, 2, 2, 6)) return 1;
+    if (v_hi != nullptr) {
+        if (!make_map<T>(&mVhi, v_hi, nx, ny, nz, 6, 2, 2, 6)) return 1;
+    } else {
+        mVhi = mV;
+    }
+    if (!make_map<T>(&mUy, U, nx, ny, nz, int64_t(nt) * 72, 1, 2, 18) ||
+        !make_map<T>(&mVy, v, nx, ny, nz, int64_t(nt) * 6, 1, 2, 6) ||
+        !make_map<T>(&mUz, U, nx, ny, nz, int64_t(nt) * 72, 2, 1, 18) ||
+        !make_map<T>(&mVz, v, nx, ny, nz, int64_t(nt) * 6, 2, 1, 6))
+        return 1;
+    const size_t smem = (size_t(S) * G::SLOT + G::XSIZE) * sizeof(T) + 2 * S * sizeof(uint64_t);
+    const DeviceInfo& di = device_info();
+    if (smem > size_t(di.max_smem_optin)) return 1;
+    auto kern = k_nn_ring<T, FUSED, NX, S>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    RingParams p{};
+    p.ny = ny; p.nz = nz; p.nt = nt;
+    p.F = int64_t(nx) * ny * nz;
+    p.nby = ny / 2;
+    p.nblocks = int64_t(ny / 2) * (nz / 2);
+    p.t_begin = t_begin; p.t_end = t_end;
+    p.has_vhi = v_hi != nullptr;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::N + 32, smem);
+    const int per = std::max(per_sm, 1);
+    const int G_full = di.num_sms * per;
+    const int L = t_end - t_begin;
+    p.chunk = pick_chunk(p.nblocks, L, G_full);
+    p.nitems = p.nblocks * ((L + p.chunk - 1) / p.chunk);
+    int Gr = G_full;
+    if (sm_reserve() > 0) {  // as nn_tma.cu: leave SMs for NCCL only where the last round absorbs it
+        const int64_t rounds = (p.nitems + G_full - 1) / G_full;
+        const int64_t g_same = (p.nitems + rounds - 1) / rounds;
+        const int g_res = std::max(per, sweep_sms() * per);
+        if (g_same <= G_full - per) Gr = static_cast<int>(std::max<int64_t>(g_res, g_same));
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(Gr, p.nitems));
+    kern<<<grid, G::N + 32, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
+    note_kernel(std::string("k_nn_ring<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x2x2," +
+                std::to_string(S) + " slots>" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
+    return check_launch("nn_sweep(ring)");
+}
+
+// 1 = not applicable to this lattice (caller falls back)
+template <typename T>
+int launch_nn_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
+                   const T* v_hi, const T* w_lo, int mode, cudaStream_t st) {
+    if (ny % 2 || nz % 2) return 1;
+    if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
+    const bool fma = mode == SU3G_FMA;
+    constexpr int S = sizeof(T) == 8 ? 4 : 8;
+    if (nx == 64)
+        return fma ? run_ring<T, true, 64, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
+                   : run_ring<T, false, 64, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+    if (nx == 32)
+        return fma ? run_ring<T, true, 32, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
+                   : run_ring<T, false, 32, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+    if (nx == 48)
+        return fma ? run_ring<T, true, 48, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
+                   : run_ring<T, false, 48, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+    return 1;
+}
+
+template int launch_nn_ring<float>(const float*, const float*, float*, int, int, int, int, int, int, const float*,
+                                   const float*, int, cudaStream_t);
+template int launch_nn_ring<double>(const double*, const double*, double*, int, int, int, int, int, int,
+                                    const double*, const double*, int, cudaStream_t);
+
+}  // namespace su3g

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk
+static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
 
 // largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
 static int chunk_planes(int nz, int cap) {
@@ -179,6 +179,12 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
         const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
         if (rc != 1) return rc;
         if (variant == 3) return fail_invalid("nn_sweep: TMA kernel not applicable to this lattice");
+    }
+    const bool auto_ring = variant == 0 && sizeof(T) == 8 && !boundary_only;
+    if (auto_ring || variant == 4) {
+        const int rc = launch_nn_ring<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
+        if (rc != 1) return rc;
+        if (variant == 4) return fail_invalid("nn_sweep: TMA ring kernel not applicable to this lattice");
     }
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int64_t n = int64_t(t_end - t_begin) * g.F;
@@ -307,8 +313,8 @@ extern "C" {
 int su3g_set_option(const char* name, int64_t value) {
     if (name == nullptr) return fail_invalid("set_option: null name");
     if (std::strcmp(name, "nn_variant") == 0) {
-        if (value != 0 && value != 1 && value != 3)
-            return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic) or 3 (tma walk)");
+        if (value != 0 && value != 1 && value != 3 && value != 4)
+            return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic), 3 (tma walk) or 4 (tma ring walk)");
         g_nn_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -220,8 +220,8 @@ def test_slab_edges_launch_chained(ranks, dims, precision):
     assert np.array_equal(got, want)
 
 
-NN_VARIANTS = [0, 1, 3]
-NN_VARIANT_IDS = ["auto", "generic", "tma"]
+NN_VARIANTS = [0, 1, 3, 4]
+NN_VARIANT_IDS = ["auto", "generic", "tma", "ring"]
 
 
 @pytest.fixture(params=NN_VARIANTS, ids=NN_VARIANT_IDS)
@@ -246,7 +246,7 @@ def test_nn_kernel_variants_bitwise(dims, precision, nn_variant):
     try:
         got = sweeps.nn_sweep_aos(U, v, dims)
     except ValueError as e:
-        if nn_variant == 3 and "not applicable" in str(e):
+        if nn_variant in (3, 4) and "not applicable" in str(e):
             pytest.skip(f"variant {nn_variant} not applicable to {dims}")
         raise
     assert np.array_equal(got, want)
@@ -262,7 +262,7 @@ def test_nn_kernel_variants_bitwise(dims, precision, nn_variant):
     assert np.array_equal(out.numpy(), want)
 
 
-@pytest.mark.parametrize("variant", [1, 3])
+@pytest.mark.parametrize("variant", [1, 3, 4])
 def test_slab_halo_path_all_variants(variant, precision):
     from paper_1309_0551_b200 import _lib
 
@@ -270,8 +270,9 @@ def test_slab_halo_path_all_variants(variant, precision):
     try:
         if variant == 3 and precision == "double":
             pytest.skip("the f32 TMA walk does not fit shared memory for f64 on these lattices")
-        test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(16, 4, 4, 8))
-        test_slab_halo_path_equals_periodic_sweep(4, precision, dims=(16, 4, 4, 8))
+        if variant != 4:  # the ring walk takes x extents 32, 48, 64
+            test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(16, 4, 4, 8))
+            test_slab_halo_path_equals_periodic_sweep(4, precision, dims=(16, 4, 4, 8))
         test_slab_halo_path_equals_periodic_sweep(8, precision, dims=(64, 4, 2, 8))
         test_slab_halo_path_equals_periodic_sweep(2, precision, dims=(64, 4, 4, 8))
     finally:
@@ -312,7 +313,7 @@ def test_link_product_bitwise(dims, precision):
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
 
 
-@pytest.mark.parametrize("variant", [1, 3], ids=["generic", "tma"])
+@pytest.mark.parametrize("variant", [1, 3, 4], ids=["generic", "tma", "ring"])
 @pytest.mark.parametrize("dims", [(64, 4, 4, 6), (32, 8, 4, 5), (8, 8, 8, 8)])
 def test_nn_fma_mode_within_tolerance(variant, dims, precision):
     """SU3G_FMA arithmetic: within the north-star tolerance of the reference, and every kernel variant
