@@ -1,4 +1,4 @@
-// NN sweep, warp-specialised TMA ring t-walk (the f64 production path on B200).
+// NN sweep, warp-specialised TMA ring t-walk (the production path on B200, f32 and f64).
 //
 // Why a second t-walk kernel: the f32 walk (nn_tma.cu) stages a whole step -- the block's
 // links, v(t+1) and the halo rows -- per ring stage; at f64 two such stages plus the
@@ -56,11 +56,18 @@ struct RingGeo {
     static constexpr int H1_V = 0, H1_VYU = 6 * N, H1_UYD = 6 * N + 6 * H;
     // H2
     static constexpr int H2_VYD = 0, H2_UZD = 6 * H, H2_VZD = 24 * H, H2_VZU = 30 * H;
-    // exchange
-    static constexpr int XW = 0;               // [18][N]
-    static constexpr int XH = 18 * N;          // [6][2H]: -y halo sites, then -z halo sites
-    static constexpr int XV = 18 * N + 12 * H; // [2][6][N]
+};
+
+// exchange buffers; DB = XW / XH double-buffered (one barrier per step instead of two)
+template <int NX, bool DB>
+struct RingX {
+    static constexpr int N = 4 * NX, H = 2 * NX;
+    static constexpr int NB = DB ? 2 : 1;
+    static constexpr int XW = 0;                    // [NB][18][N]
+    static constexpr int XH = NB * 18 * N;          // [NB][6][2H]: -y halo sites, then -z halo sites
+    static constexpr int XV = NB * (18 * N + 12 * H);  // [2][6][N]
     static constexpr int XSIZE = XV + 12 * N;
+    static constexpr int WSTRIDE = 18 * N, HSTRIDE = 12 * H;  // per buffer
 };
 
 __device__ __forceinline__ void item_of(const RingParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
@@ -72,19 +79,20 @@ __device__ __forceinline__ void item_of(const RingParams& p, int64_t item, int64
 
 }  // namespace
 
-template <typename T, bool FUSED, int NX, int S>
-__global__ void __launch_bounds__(4 * NX + 32, 1)
+template <typename T, bool FUSED, int NX, int S, bool DB, int MINB>
+__global__ void __launch_bounds__(4 * NX + 32, MINB)
     k_nn_ring(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
               const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
               const __grid_constant__ CUtensorMap mapUzH, const __grid_constant__ CUtensorMap mapVyH,
               const __grid_constant__ CUtensorMap mapVzH, const T* __restrict__ U, const T* __restrict__ v,
               T* __restrict__ out, const T* __restrict__ w_lo, RingParams p) {
     using G = RingGeo<NX>;
+    using X = RingX<NX, DB>;
     constexpr int N = G::N, H = G::H, NW = N / 32;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* ring = reinterpret_cast<T*>(smem_raw);
     T* xb = ring + S * G::SLOT;
-    uint64_t* full = reinterpret_cast<uint64_t*>(xb + G::XSIZE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(xb + X::XSIZE);
     uint64_t* empty = full + S;
 
     const int tid = threadIdx.x;
@@ -151,9 +159,9 @@ __global__ void __launch_bounds__(4 * NX + 32, 1)
     const int ix_dn = (lx == 0) ? tid + NX - 1 : tid - 1;
     const int jy = lx + NX * lz;  // this column's slot in a y halo row (box x, z)
     const int jz = lx + NX * ly;  // ... in a z halo row (box x, y)
-    T* XW = xb + G::XW;
-    T* XH = xb + G::XH;
-    T* XV = xb + G::XV;
+    T* const XW0 = xb + X::XW;
+    T* const XH0 = xb + X::XH;
+    T* XV = xb + X::XV;
 
     uint32_t q = 0;
     uint32_t k = 0;  // steps done by this CTA (XV parity)
@@ -182,6 +190,8 @@ __global__ void __launch_bounds__(4 * NX + 32, 1)
 
         for (int t = t0; t < t1; ++t, ++k) {
             const T* xv = XV + (k & 1) * 6 * N;
+            T* XW = XW0 + (DB ? (k & 1) * X::WSTRIDE : 0);
+            T* XH = XH0 + (DB ? (k & 1) * X::HSTRIDE : 0);
             T vnext[6], nby_[6], nbz_[6];
             // ---- H1, H2: v(t+1), the +y / +z halo v this column needs, the halo half-products
             {
@@ -290,15 +300,18 @@ __global__ void __launch_bounds__(4 * NX + 32, 1)
                 vc[c] = vnext[c];
                 wt[c] = wt_next[c];
             }
-            named_sync<N>();  // XW / XH are rewritten by the next step
+            // single-buffered XW / XH are rewritten by the next step; double-buffered ones only by the
+            // step after, whose writers have all passed the next step's barrier (after this read)
+            if constexpr (!DB) named_sync<N>();
         }
     }
 }
 
-template <typename T, bool FUSED, int NX, int S>
+template <typename T, bool FUSED, int NX, int S, bool DB, int MINB>
 static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                     const T* v_hi, const T* w_lo, cudaStream_t st) {
     using G = RingGeo<NX>;
+    using X = RingX<NX, DB>;
     CUtensorMap mU, mV, mVhi, mUy, mUz, mVy, mVz;
     if (!make_map<T>(&mU, U, nx, ny, nz, int64_t(nt) * 72, 2, 2, 18)) return 1;
     if (!make_map<T>(&mV, v, nx, ny, nz, int64_t(nt) * 6, 2, 2, 6)) return 1;
@@ -312,10 +325,10 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
         !make_map<T>(&mUz, U, nx, ny, nz, int64_t(nt) * 72, 2, 1, 18) ||
         !make_map<T>(&mVz, v, nx, ny, nz, int64_t(nt) * 6, 2, 1, 6))
         return 1;
-    const size_t smem = (size_t(S) * G::SLOT + G::XSIZE) * sizeof(T) + 2 * S * sizeof(uint64_t);
+    const size_t smem = (size_t(S) * G::SLOT + X::XSIZE) * sizeof(T) + 2 * S * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    auto kern = k_nn_ring<T, FUSED, NX, S>;
+    auto kern = k_nn_ring<T, FUSED, NX, S, DB, MINB>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     RingParams p{};
     p.ny = ny; p.nz = nz; p.nt = nt;
@@ -341,8 +354,29 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const int grid = static_cast<int>(std::min<int64_t>(Gr, p.nitems));
     kern<<<grid, G::N + 32, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     note_kernel(std::string("k_nn_ring<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x2x2," +
-                std::to_string(S) + " slots>" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
+                std::to_string(S) + " slots" + (DB ? ",1 barrier" : "") + (per > 1 ? "," + std::to_string(per) + " CTAs/SM" : "") +
+                ">" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
     return check_launch("nn_sweep(ring)");
+}
+
+int g_ring_cfg = 0;  // su3g_set_option("nn_ring_cfg"): f32 ring configuration (A/B), 0 = default
+
+template <typename T, bool FUSED, int NX>
+static int ring_dispatch(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
+                         const T* v_hi, const T* w_lo, cudaStream_t st) {
+    if constexpr (sizeof(T) == 8) {  // f64: four 36-KB slots next to the single-buffered exchange
+        return run_ring<T, FUSED, NX, 4, false, 1>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+    } else {
+        // f32: two CTAs per SM, four 18-KB slots each (same-box A/B at 64^3x16, fraction of HBM:
+        // 0.905 vs 0.840 for one CTA with eight slots, 0.812 one CTA with six slots and a double-
+        // buffered exchange, 0.716 two CTAs with two slots each; the f32 TMA walk 0.835)
+        switch (g_ring_cfg) {
+            case 1: return run_ring<T, FUSED, NX, 8, false, 1>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+            case 2: return run_ring<T, FUSED, NX, 6, true, 1>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+            case 3: return run_ring<T, FUSED, NX, 2, true, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+            default: return run_ring<T, FUSED, NX, 4, false, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+        }
+    }
 }
 
 // 1 = not applicable to this lattice (caller falls back)
@@ -352,16 +386,15 @@ int launch_nn_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     if (ny % 2 || nz % 2) return 1;
     if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
     const bool fma = mode == SU3G_FMA;
-    constexpr int S = sizeof(T) == 8 ? 4 : 8;
     if (nx == 64)
-        return fma ? run_ring<T, true, 64, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
-                   : run_ring<T, false, 64, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+        return fma ? ring_dispatch<T, true, 64>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
+                   : ring_dispatch<T, false, 64>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
     if (nx == 32)
-        return fma ? run_ring<T, true, 32, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
-                   : run_ring<T, false, 32, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+        return fma ? ring_dispatch<T, true, 32>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
+                   : ring_dispatch<T, false, 32>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
     if (nx == 48)
-        return fma ? run_ring<T, true, 48, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
-                   : run_ring<T, false, 48, S>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+        return fma ? ring_dispatch<T, true, 48>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st)
+                   : ring_dispatch<T, false, 48>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
     return 1;
 }
 

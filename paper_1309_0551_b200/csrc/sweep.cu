@@ -24,6 +24,7 @@ int g_sweep_zc = 0;  // su3g_set_option("sweep_zc"): z-planes per chunk of the g
 // f64 64^3x16 0.686 -> 0.736 of HBM, 32^4 0.711 -> 0.777, dslash f64 0.569 -> 0.642 (same box A/B)
 int g_sweep_hints = 1;
 extern int g_tma_hints;
+extern int g_ring_cfg;
 extern int g_tma_chunk;
 extern int g_eo_zc;
 extern int g_eo_hints;
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(256)
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk
 
 // largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
 static int chunk_planes(int nz, int cap) {
@@ -169,22 +171,22 @@ static int nn_sweep(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     if (!U || !v || !out) return fail_invalid("nn_sweep: null pointer");
     if (t_begin == t_end) return SU3G_OK;
     const int variant = g_nn_variant.load();
-    // auto policy (measured on B200, profiles/r01): f32 with x rows of 32+ sites -> TMA walk;
-    // f64 and the rest -> generic (fewest registers, best occupancy).  One or two boundary
-    // slices of a t-slab (the halo-dependent launches) go to the generic kernel: a walk
-    // kernel would pay a work-item prologue for every single-slice item
+    // auto policy (measured on B200, profiles/r02): lattices with x extent 32, 48 or 64 and even y, z
+    // -> the TMA ring walk (64^3x16: f32 0.905, f64 0.951 of HBM); other f32 lattices with x rows of
+    // 32+ sites -> the f32 TMA walk; the rest -> generic.  One or two boundary slices of a t-slab (the
+    // halo-dependent launches) go to the generic kernel: a walk kernel would pay a work-item prologue
+    // for every single-slice item
     const bool boundary_only = (t_end - t_begin) <= 2 && nt > 2;
+    if ((variant == 0 && !boundary_only) || variant == 4) {
+        const int rc = launch_nn_ring<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
+        if (rc != 1) return rc;
+        if (variant == 4) return fail_invalid("nn_sweep: TMA ring kernel not applicable to this lattice");
+    }
     const bool auto_tma = variant == 0 && sizeof(T) == 4 && nx >= 32 && !boundary_only;
     if (auto_tma || variant == 3) {
         const int rc = launch_nn_tma<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
         if (rc != 1) return rc;
         if (variant == 3) return fail_invalid("nn_sweep: TMA kernel not applicable to this lattice");
-    }
-    const bool auto_ring = variant == 0 && sizeof(T) == 8 && !boundary_only;
-    if (auto_ring || variant == 4) {
-        const int rc = launch_nn_ring<T>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, mode, st);
-        if (rc != 1) return rc;
-        if (variant == 4) return fail_invalid("nn_sweep: TMA ring kernel not applicable to this lattice");
     }
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int64_t n = int64_t(t_end - t_begin) * g.F;
@@ -294,6 +296,16 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     if (!U || !acc) return fail_invalid("link_product: null pointer");
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("link_product: mode must be SU3G_EXACT or SU3G_FMA");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
+    const int lv = g_link_variant.load();
+    // auto: the ring walk for the f64 FMA product (48^4: 0.534 vs 0.519 of HBM for the rows gather);
+    // exact f64 (FP64-issue bound: 0.457 rows vs 0.295 ring) and f32 (0.305 vs 0.224) stay on rows
+    const bool auto_ring = lv == 0 && sizeof(T) == 8 && mode == SU3G_FMA;
+    if (auto_ring || lv == 2) {
+        const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
+                                        : launch_link_ring<T, false>(U, acc, nx, ny, nz, nt, s, st);
+        if (rc != 1) return rc;
+        if (lv == 2) return fail_invalid("link_product: TMA ring kernel not applicable to this lattice");
+    }
     // z-planes per chunk: 16 measured best for the rows kernel at 48^4 f64 (exact 0.427 -> 0.455,
     // FMA 0.475 -> 0.506 against the unchunked order; 2, 4, 12 also swept).  Chunk once a t-slice of
     // links is more than 1/8 of L2 (48^3 f64 = 64 MB, about half of L2, was left unchunked before).
@@ -316,6 +328,17 @@ int su3g_set_option(const char* name, int64_t value) {
         if (value != 0 && value != 1 && value != 3 && value != 4)
             return fail_invalid("set_option: nn_variant must be 0 (auto), 1 (generic), 3 (tma walk) or 4 (tma ring walk)");
         g_nn_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "link_variant") == 0) {
+        if (value < 0 || value > 2)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather) or 2 (tma ring walk)");
+        g_link_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "nn_ring_cfg") == 0) {
+        if (value < 0 || value > 3) return fail_invalid("set_option: nn_ring_cfg must be in [0, 3]");
+        g_ring_cfg = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "dslash_eo_zc") == 0) {

@@ -45,7 +45,7 @@ def test_config5_weak_ten_chained_applications_bitwise(dtype):
     got = slab.apply_n(v, v.empty_like(), 10)
     kernel = _lib.last_kernel()
     # the bench's dominant kernels
-    assert kernel.startswith("k_nn_tma<f32,64x2x2" if dtype == torch.float32 else "k_nn_ring<f64,64x2x2"), kernel
+    assert kernel.startswith("k_nn_ring<f32,64x2x2" if dtype == torch.float32 else "k_nn_ring<f64,64x2x2"), kernel
     got = got.numpy()
     want = coracle.nn_sweep_iterated(U_h, v_h, WEAK, 10)
     bad = np.argwhere(np.any(got != want, axis=(1, 2))).ravel()

@@ -82,17 +82,27 @@ def test_link_product_vs_c_oracle(dims, precision):
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
 
 
-def test_link_product_config3_full_size():
+@pytest.mark.parametrize("variant", [0, 1], ids=["auto", "rows"])
+def test_link_product_config3_full_size(variant):
     """BASELINE configs[3]: 48^4 link product, complex128 -- exact bitwise, FMA within 1e-12."""
+    from paper_1309_0551_b200 import _lib
+
     dims = (48, 48, 48, 48)
     V = 48**4
     rng = inputs.config_rng(3)
     U = inputs.random_links(rng, V, 4, dtype=np.float64)
     want = coracle.link_product(U, dims, 1 / 6)
-    got = sweeps.link_product_aos(U, dims, 1 / 6)
-    assert np.array_equal(got, want)
-    del got
-    assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
+    _lib.set_option("link_variant", variant)
+    try:
+        got = sweeps.link_product_aos(U, dims, 1 / 6)
+        assert np.array_equal(got, want), _lib.last_kernel()
+        assert _lib.last_kernel().startswith("k_link_rows<f64"), _lib.last_kernel()  # exact: the rows gather
+        del got
+        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
+        if variant == 0:
+            assert _lib.last_kernel().startswith("k_link_ring<f64,48x2x2"), _lib.last_kernel()
+    finally:
+        _lib.set_option("link_variant", 0)
 
 
 def test_link_product_config3_f32_full_size():
@@ -300,17 +310,31 @@ def test_tma_variant_required_fails_loudly_when_inapplicable():
 @pytest.mark.parametrize(
     "dims",
     [(8, 8, 8, 8), (6, 5, 4, 3), (48, 2, 2, 5), (16, 4, 4, 4), (5, 3, 2, 97), (16, 8, 4, 6), (8, 4, 2, 3),
-     (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33), (8, 4, 4, 3), (16, 8, 12, 5), (24, 4, 8, 1)],
+     (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33), (8, 4, 4, 3), (16, 8, 12, 5), (24, 4, 8, 1),
+     (32, 4, 4, 6), (64, 4, 2, 3), (48, 48, 8, 4)],
 )
-def test_link_product_bitwise(dims, precision):
+@pytest.mark.parametrize("variant", [0, 1, 2], ids=["auto", "rows", "ring"])
+def test_link_product_bitwise(dims, precision, variant):
+    from paper_1309_0551_b200 import _lib
+
     dt = _dt(precision)
     V = int(np.prod(dims))
     rng = inputs.config_rng(4000 + V)
     U = inputs.random_links(rng, V, 4, dtype=dt)
     want = coracle.link_product(U, dims, 1 / 6)
-    assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
-    tol = 1e-5 if dt == np.float32 else 1e-12
-    assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
+    _lib.set_option("link_variant", variant)
+    try:
+        try:
+            got = sweeps.link_product_aos(U, dims, 1 / 6)
+        except ValueError as e:
+            if variant == 2 and "not applicable" in str(e):
+                pytest.skip(f"ring walk not applicable to {dims}")
+            raise
+        assert np.array_equal(got, want), _lib.last_kernel()
+        tol = 1e-5 if dt == np.float32 else 1e-12
+        assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= tol
+    finally:
+        _lib.set_option("link_variant", 0)
 
 
 @pytest.mark.parametrize("variant", [1, 3, 4], ids=["generic", "tma", "ring"])
@@ -605,7 +629,7 @@ def test_generic_kernel_knobs_keep_results_bitwise(option, value, default, preci
 
 @pytest.mark.parametrize("dims", [(48, 4, 4, 6), (48, 2, 6, 3), (24, 8, 4, 5), (40, 4, 2, 3), (96, 2, 2, 4), (12, 16, 4, 3)])
 def test_sweeps_for_x_extents_not_dividing_256(dims):
-    """nx = 48 takes the specialised 48x2x2 TMA geometry (when ny, nz > 2); others the generic kernel;
+    """nx = 48 takes the 48x2x2 ring walk (ny, nz even); others the f32 TMA walk or the generic kernel;
     all bitwise vs the oracle."""
     from paper_1309_0551_b200 import _lib
 
@@ -618,8 +642,36 @@ def test_sweeps_for_x_extents_not_dividing_256(dims):
     lat = Lattice4D(*dims)
     Uf, vf = Field.from_aos(lat, "mat4", U), Field.from_aos(lat, "vec", v)
     sweeps.nn_sweep(Uf, vf)
-    if dims[0] == 48 and dims[1] > 2 and dims[2] > 2:
-        assert "k_nn_tma<f32,48x2x2" in _lib.last_kernel(), _lib.last_kernel()
+    if dims[0] == 48 and dims[1] % 2 == 0 and dims[2] % 2 == 0:
+        assert "k_nn_ring<f32,48x2x2" in _lib.last_kernel(), _lib.last_kernel()
     # 3 applications through the same kernel, and FMA within tolerance
     assert np.array_equal(sweeps.nn_sweep_aos(U, v, dims, applications=3), coracle.nn_sweep_iterated(U, v, dims, 3))
     assert floored_rel_err(sweeps.nn_sweep_aos(U, v, dims, mode="fma"), coracle.nn_sweep(U, v, dims)) <= 1e-5
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+@pytest.mark.parametrize("dims", [(64, 8, 4, 6), (32, 8, 8, 12), (48, 4, 6, 5), (64, 64, 16, 3)])
+def test_nn_ring_configurations_bitwise(cfg, dims):
+    """Every f32 ring configuration (slot count, one- or two-barrier exchange, CTAs per SM) and the f64
+    ring: bitwise vs the C oracle over multi-item schedules, FMA within tolerance."""
+    from paper_1309_0551_b200 import _lib
+
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(9700 + V)
+    _lib.set_option("nn_variant", 4)
+    _lib.set_option("nn_ring_cfg", cfg)
+    try:
+        for dt, tol in ((np.float32, 1e-5), (np.float64, 1e-12)):
+            if dt == np.float64 and cfg:
+                continue
+            U = inputs.random_links(rng, V, 4, dtype=dt)
+            v = inputs.random_vectors(rng, V, None, dtype=dt)
+            want = coracle.nn_sweep(U, v, dims)
+            got = sweeps.nn_sweep_aos(U, v, dims)
+            bad = np.argwhere(np.any(got != want, axis=(1, 2))).ravel()
+            assert bad.size == 0, f"{_lib.last_kernel()}: {bad.size} wrong sites, first {bad[:6]}"
+            assert np.array_equal(sweeps.nn_sweep_aos(U, v, dims, applications=3), coracle.nn_sweep_iterated(U, v, dims, 3))
+            assert floored_rel_err(sweeps.nn_sweep_aos(U, v, dims, mode="fma"), want) <= tol
+    finally:
+        _lib.set_option("nn_ring_cfg", 0)
+        _lib.set_option("nn_variant", 0)
