@@ -269,6 +269,13 @@ SU3G_API int su3g_comm_unique_id(void *id_out);
 SU3G_API int su3g_comm_init(int32_t nranks, int32_t rank, const void *id, su3g_comm_t *comm);
 SU3G_API int su3g_comm_destroy(su3g_comm_t comm);
 SU3G_API int su3g_comm_rank(su3g_comm_t comm, int32_t *rank, int32_t *nranks);
+/* Failure detection: waits (host side) for the last enqueued halo exchange, polling NCCL's
+ * asynchronous error state (ncclCommGetAsyncError).  On an NCCL error, or when the exchange is
+ * still pending after timeout_ms (< 0: no deadline) -- a dead or stalled peer -- the communicator
+ * is aborted (ncclCommAbort, so no kernel is left spinning) and SU3G_ENCCL is returned; the
+ * handle must then only be destroyed.  su3g_slab_nn_sweep_* also refuses a communicator that is
+ * already in an asynchronous error state. */
+SU3G_API int su3g_comm_check(su3g_comm_t comm, int64_t timeout_ms);
 SU3G_API int su3g_slab_nn_sweep_f32(su3g_comm_t comm, const float *U, const float *v, float *out, int32_t nx,
                                     int32_t ny, int32_t nz, int32_t nt_local, int32_t mode, su3g_stream_t stream);
 SU3G_API int su3g_slab_nn_sweep_f64(su3g_comm_t comm, const double *U, const double *v, double *out, int32_t nx,

@@ -58,6 +58,7 @@ def _signatures():
         "su3g_comm_init": ([_i32, _i32, _vp, _vp], ctypes.c_int),
         "su3g_comm_destroy": ([_vp], ctypes.c_int),
         "su3g_comm_rank": ([_vp, _vp, _vp], ctypes.c_int),
+        "su3g_comm_check": ([_vp, _i64], ctypes.c_int),
         "su3g_p2p_window_bytes": ([_i32, _i32, _i32, _i32], ctypes.c_int64),
         "su3g_p2p_ctrl_offset": ([_i32, _i32, _i32, _i32], ctypes.c_int64),
         "su3g_ipc_get_handle": ([_vp, _vp], ctypes.c_int),
@@ -122,6 +123,8 @@ def check(rc: int, what: str) -> None:
     if rc == SU3G_OK:
         return
     msg = load().su3g_last_error().decode(errors="replace")
+    if rc == SU3G_ENCCL:
+        raise Su3gError(f"{what}: {msg}")
     if rc < 0:
         raise ValueError(f"{what}: {msg}")
     raise Su3gError(f"{what}: CUDA error {rc}: {msg}")

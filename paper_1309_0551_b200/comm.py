@@ -61,6 +61,12 @@ class NativeComm:
             raise ValueError("communicator is closed")
         return self._h
 
+    def check(self, timeout_s: float | None = 60.0) -> None:
+        """Wait for the last halo exchange, watching NCCL's asynchronous error state (su3g_comm_check).
+        A failed or stalled exchange (dead peer) aborts the communicator and raises RuntimeError."""
+        ms = -1 if timeout_s is None else int(timeout_s * 1000)
+        _lib.call("su3g_comm_check", self.handle, ms)  # the handle stays valid for close()
+
     def close(self) -> None:
         if self._h is not None and self._h.value:
             h, self._h = self._h, None
@@ -103,4 +109,5 @@ def native_slab_apply(comm: NativeComm, U: Field, v: Field, applications: int, s
     for _ in range(applications):
         native_slab_sweep(comm, U, a, b, mode)
         a, b = b, a
+    comm.check()
     return a

@@ -21,10 +21,12 @@
 // communicator exchanges with itself, which runs the whole schedule on one GPU.
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 
 #include <nccl.h>
 
@@ -47,6 +49,8 @@ struct NcclApi {
     decltype(&ncclSend) send = nullptr;
     decltype(&ncclRecv) recv = nullptr;
     decltype(&ncclGetErrorString) errorString = nullptr;
+    decltype(&ncclCommGetAsyncError) getAsyncError = nullptr;
+    decltype(&ncclCommAbort) commAbort = nullptr;
 };
 
 NcclApi g_nccl;
@@ -75,6 +79,8 @@ int load_nccl() {
     SU3G_SYM(send, "ncclSend");
     SU3G_SYM(recv, "ncclRecv");
     SU3G_SYM(errorString, "ncclGetErrorString");
+    SU3G_SYM(getAsyncError, "ncclCommGetAsyncError");
+    SU3G_SYM(commAbort, "ncclCommAbort");
 #undef SU3G_SYM
     if (!ok) return fail_invalid("comm: NCCL library lacks a required symbol");
     g_nccl = a;
@@ -119,6 +125,11 @@ int slab_sweep(su3g_comm_t c, const T* U, const T* v, T* out, int nx, int ny, in
     int dev = -1;
     cudaGetDevice(&dev);
     if (dev != c->device) return fail_invalid("slab_nn_sweep: current device differs from the communicator's");
+    // a communicator that failed asynchronously (peer died, network error) must not be fed more work
+    ncclResult_t async_err = ncclSuccess;
+    if (ncclResult_t r = g_nccl.getAsyncError(c->nccl, &async_err)) return nccl_fail("slab_nn_sweep: async query", r);
+    if (async_err != ncclSuccess && async_err != ncclInProgress)
+        return nccl_fail("slab_nn_sweep: communicator in error state", async_err);
     const int64_t F = int64_t(nx) * ny * nz;
     const size_t face = size_t(6 * F) * sizeof(T);
     if (c->faces_bytes < 3 * face) {
@@ -237,6 +248,36 @@ int su3g_comm_destroy(su3g_comm_t c) {
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     delete c;
     return rc;
+}
+
+int su3g_comm_check(su3g_comm_t c, int64_t timeout_ms) {
+    if (c == nullptr || c->nccl == nullptr) return fail_invalid("comm_check: null or destroyed communicator");
+    // wait for the last enqueued exchange, polling NCCL's asynchronous error state; a peer that never
+    // posts its half leaves the exchange pending forever, so past the deadline the communicator is
+    // aborted (its kernels return) and the call fails instead of hanging the caller
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(c->ev_halo);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) return cuda_fail("comm_check: exchange", q);
+        ncclResult_t async_err = ncclSuccess;
+        if (ncclResult_t r = g_nccl.getAsyncError(c->nccl, &async_err)) return nccl_fail("comm_check: async query", r);
+        if (async_err != ncclSuccess && async_err != ncclInProgress) {
+            g_nccl.commAbort(c->nccl);
+            c->nccl = nullptr;
+            return nccl_fail("comm_check: halo exchange failed (communicator aborted)", async_err);
+        }
+        const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0);
+        if (timeout_ms >= 0 && ms.count() > timeout_ms) {
+            g_nccl.commAbort(c->nccl);
+            c->nccl = nullptr;
+            set_error("comm_check: halo exchange did not complete within " + std::to_string(timeout_ms) +
+                      " ms (communicator aborted)");
+            return SU3G_ENCCL;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    return SU3G_OK;
 }
 
 int su3g_comm_rank(su3g_comm_t c, int32_t* rank, int32_t* nranks) {

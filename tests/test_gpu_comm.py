@@ -46,7 +46,8 @@ def test_one_rank_native_slab_equals_periodic_sweep(comm, dims, dtype):
 def test_one_rank_native_slab_ten_applications(comm, dtype):
     U, v, U_h, v_h = _fields((32, 16, 8, 6), dtype, 71)
     want = coracle.nn_sweep_iterated(U_h, v_h, (32, 16, 8, 6), 10)
-    got = native_slab_apply(comm, U, v, 10).numpy()
+    got = native_slab_apply(comm, U, v, 10).numpy()  # ends with comm.check(): async-error poll, bounded wait
+    comm.check(timeout_s=5.0)
     assert np.array_equal(got, want)
 
 

@@ -281,6 +281,9 @@ def test_comm_abi_without_a_gpu():
     assert lib.su3g_comm_init(2, 2, uid, ctypes.byref(h)) == _lib.SU3G_EINVAL
     assert lib.su3g_comm_init(1, 0, None, ctypes.byref(h)) == _lib.SU3G_EINVAL
     assert lib.su3g_comm_destroy(None) == _lib.SU3G_OK
+    assert lib.su3g_comm_check(None, 1000) == _lib.SU3G_EINVAL
+    with pytest.raises(RuntimeError):  # NCCL failures surface as RuntimeError, argument errors as ValueError
+        _lib.check(_lib.SU3G_ENCCL, "x")
     assert lib.su3g_slab_nn_sweep_f32(None, None, None, None, 4, 4, 4, 4, 0, None) == _lib.SU3G_EINVAL
     with pytest.raises(ValueError, match="128"):
         NativeComm(1, 0, b"short")
