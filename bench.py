@@ -1092,7 +1092,7 @@ def _ref_routine_rate(cfg, dtype: str, budget_s: float):
 def cpu_baseline(args, cfg, budget_s=12.0):
     """The b200 line's cpu_baseline: the reference on one pinned core over a bounded sample (N=1, rank 0)."""
     if cfg["kind"] == "routine":
-        ops, el, kind, desc = _ref_routine_rate(cfg, args.dtype, budget_s)
+        ops, el, kind, desc = _ref_routine_rate(cfg, args.dtype, budget_s / 3)
         return {"value": ops / el, "unit": UNIT, "cores": 1, "kind": kind, "sample": desc, **_host_info()}
     rs = RefSweep(cfg, args.dtype)
     k = _sample_slices(cfg)
