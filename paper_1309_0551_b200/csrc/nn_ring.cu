@@ -218,11 +218,8 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
 #pragma unroll
                     for (int c = 0; c < 6; ++c) vh[c] = h2[G::H2_VZD + c * H + (tid - H)];
                 }
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&empty[s1]);
-                    mbar_arrive(&empty[s2]);
-                }
+                warp_release(&empty[s1], lane);
+                if (lane == 0) mbar_arrive(&empty[s2]);
                 amv<T, FUSED>(uh, vh, wh);
 #pragma unroll
                 for (int c = 0; c < 6; ++c) XH[c * (2 * H) + tid] = wh[c];
@@ -238,8 +235,7 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
                 T u[18];
 #pragma unroll
                 for (int c = 0; c < 18; ++c) u[c] = su[c * N + tid];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
+                warp_release(&empty[s], lane);
                 T w[6], nb[6], f[6];
                 amv<T, FUSED>(u, vc, w);
 #pragma unroll
@@ -266,8 +262,7 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
                 T u[18], f[6];
 #pragma unroll
                 for (int c = 0; c < 18; ++c) u[c] = su[c * N + tid];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
+                warp_release(&empty[s], lane);
                 amv<T, FUSED>(u, vc, wt_next);
                 mv<T, FUSED>(u, vnext, f);
 #pragma unroll

@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(Geometry<Op>::TS)
         if (has_s) s = reinterpret_cast<const T*>(base + G::A_BYTES + G::B_BYTES)[tid];
 
         if (tid == 0) bulk_wait_read<1>();  // result buffer (k & 1) released by the store of tile k-2
+        fence_before_refill();
         __syncthreads();                     // stage st fully consumed; obuf (k & 1) free
         if (tid == 0 && k + STAGES < count) issue(first + (k + STAGES) * stride, st);
 

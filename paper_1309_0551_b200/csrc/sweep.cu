@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256)
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
-static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk, 3 row-split ring walk
 
 // largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
 static int chunk_planes(int nz, int cap) {
@@ -299,6 +299,12 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     const int lv = g_link_variant.load();
     // auto: the ring walk for the f64 FMA product (48^4: 0.534 vs 0.519 of HBM for the rows gather);
     // exact f64 (FP64-issue bound: 0.457 rows vs 0.295 ring) and f32 (0.305 vs 0.224) stay on rows
+    if (lv == 3) {
+        const int rc = mode == SU3G_FMA ? launch_link_ring3<T, true>(U, acc, nx, ny, nz, nt, s, st)
+                                        : launch_link_ring3<T, false>(U, acc, nx, ny, nz, nt, s, st);
+        if (rc != 1) return rc;
+        return fail_invalid("link_product: row-split ring kernel not applicable to this lattice");
+    }
     const bool auto_ring = lv == 0 && sizeof(T) == 8 && mode == SU3G_FMA;
     if (auto_ring || lv == 2) {
         const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
@@ -331,8 +337,9 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 2)
-            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather) or 2 (tma ring walk)");
+        if (value < 0 || value > 3)
+            return fail_invalid(
+                "set_option: link_variant must be 0 (auto), 1 (rows gather), 2 (tma ring walk) or 3 (row-split ring walk)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -78,6 +78,9 @@ int launch_dslash_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, in
 // link product on the TMA ring t-walk (link_ring.cu); 1 = not applicable
 template <typename T, bool FUSED>
 int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
+// row-split ring walk (three lanes per site, link_ring.cu); 1 = not applicable
+template <typename T, bool FUSED>
+int launch_link_ring3(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);
 

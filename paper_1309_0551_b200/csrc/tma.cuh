@@ -55,6 +55,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// Consumer-side release of a ring slot that the producer refills with TMA: fence (each lane's
+// reads of the slot before the async-proxy refill), then one arrive per warp.
+__device__ __forceinline__ void warp_release(uint64_t* bar, int lane) {
+    fence_before_refill();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+}
+
 template <int N>
 __device__ __forceinline__ void named_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory");

@@ -1,0 +1,254 @@
+"""Guard-band bounds checks of every libsu3g kernel family (the memcheck substitute).
+
+compute-sanitizer is closed on this GPU pool (runs under it have left GPUs needing a reset), so
+out-of-bounds accesses are caught the way its memcheck would see their effects:
+
+  * every operand and result lives inside a larger device buffer whose GUARD elements on both
+    sides hold a signalling bit pattern (a NaN payload).  After the call the guards must be
+    bit-for-bit intact: an out-of-bounds WRITE anywhere within GUARD elements of a region shows;
+  * an out-of-bounds READ pulls that NaN into the arithmetic, so the result no longer equals the
+    CPU oracle bit for bit (every check below is bitwise, exact mode).
+
+The buffers are passed straight through the C ABI (include/su3g.h), on ragged sizes, odd lattices
+and every kernel variant the dispatcher can pick (set_option), so the TMA boxes, ring slots,
+halo rows and tails of each kernel run against a guarded edge.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import coracle
+from oracle import routines as R
+from paper_1309_0551_b200 import _lib
+from paper_1309_0551_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+GUARD = 8192  # elements each side (32/64 KB: wider than any TMA box row or halo stride used here)
+PATTERN = {np.float32: np.uint32(0x7FA5A5A5), np.float64: np.uint64(0x7FF5A5A5A5A5A5A5)}  # signalling NaNs
+INT_VIEW = {np.float32: torch.int32, np.float64: torch.int64}
+SFX = {np.float32: "f32", np.float64: "f64"}
+TDT = {np.float32: torch.float32, np.float64: torch.float64}
+
+
+class Guarded:
+    """A device region of `n` reals with poisoned guard bands; `.ptr` is the region's address."""
+
+    def __init__(self, dt, n, fill=None):
+        self.dt, self.n = dt, n
+        self.pat = int(PATTERN[dt])
+        self.buf = torch.full((GUARD + n + GUARD,), self.pat, dtype=INT_VIEW[dt], device="cuda").view(TDT[dt])
+        if fill is not None:
+            self.buf[GUARD:GUARD + n] = torch.from_numpy(np.ascontiguousarray(fill, dtype=dt).reshape(-1)).cuda()
+
+    @property
+    def ptr(self):
+        return self.buf.data_ptr() + GUARD * np.dtype(self.dt).itemsize
+
+    def host(self):
+        return self.buf[GUARD:GUARD + self.n].cpu().numpy()
+
+    def intact(self):
+        iv = self.buf.view(INT_VIEW[self.dt])
+        return bool((iv[:GUARD] == self.pat).all()) and bool((iv[GUARD + self.n:] == self.pat).all())
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _to_soa(aos, dims):
+    """host AoS (V, ...) -> t-sliced SoA [(t*C + c)*F + s3] (include/su3g.h layout transforms)"""
+    nx, ny, nz, nt = dims
+    F = nx * ny * nz
+    C = int(np.prod(aos.shape[1:]))
+    return aos.reshape(nt, F, C).transpose(0, 2, 1).reshape(-1)
+
+
+def _from_soa(soa, dims, shape):
+    nx, ny, nz, nt = dims
+    F = nx * ny * nz
+    C = int(np.prod(shape))
+    return soa.reshape(nt, C, F).transpose(0, 2, 1).reshape((nt * F,) + tuple(shape))
+
+
+@pytest.fixture(params=[np.float32, np.float64], ids=["f32", "f64"])
+def dt(request):
+    return request.param
+
+
+def test_routines_guarded(dt):
+    n = 1013
+    rng = inputs.config_rng(91)
+    U = inputs.random_links(rng, n, 4, dtype=dt)
+    v = inputs.random_vectors(rng, n, 4, dtype=dt)
+    h = rng.standard_normal((n, 2, 3, 2)).astype(dt)
+    ops = {
+        "mult_su3_mat_vec": (U[:, 0], v[:, 0]), "mult_adj_su3_mat_vec": (U[:, 0], v[:, 0]),
+        "mult_su3_nn": (U[:, 0], U[:, 1]), "mult_su3_na": (U[:, 0], U[:, 1]), "mult_su3_an": (U[:, 0], U[:, 1]),
+        "mult_adj_su3_mat_vec_4dir": (U, v[:, 0]), "mult_su3_mat_vec_sum_4dir": (U, v),
+        "add_su3_vector": (v[:, 0], v[:, 1]), "mult_su3_mat_hwvec": (U[:, 0], h),
+        "mult_adj_su3_mat_hwvec": (U[:, 0], h), "su3_projector": (v[:, 0], v[:, 1]),
+    }
+    for r, (a, b) in ops.items():
+        want = R.ALL_ROUTINES[r](a, b)
+        ga, gb = Guarded(dt, a.size, a), Guarded(dt, b.size, b)
+        gc = Guarded(dt, want.size)
+        _lib.call(f"su3g_{r}_{SFX[dt]}", ga.ptr, gb.ptr, gc.ptr, n, _stream())
+        torch.cuda.synchronize()
+        assert gc.intact() and ga.intact() and gb.intact(), f"{r}: guard band overwritten"
+        assert np.array_equal(gc.host().reshape(want.shape), want), r
+    # scalar forms: 0-d scalar and per-site scalar array
+    s_site = rng.standard_normal(n).astype(dt)
+    for r, (a, b) in (("scalar_mult_add_su3_matrix", (U[:, 0], U[:, 1])),
+                      ("scalar_mult_add_su3_vector", (v[:, 0], v[:, 1]))):
+        for per_site in (False, True):
+            s = s_site if per_site else dt(0.5)
+            want = R.ALL_ROUTINES[r](a, b, s)
+            ga, gb, gc = Guarded(dt, a.size, a), Guarded(dt, b.size, b), Guarded(dt, a.size)
+            gs = Guarded(dt, n, s_site) if per_site else None
+            _lib.call(f"su3g_{r}_{SFX[dt]}", ga.ptr, gb.ptr, float(0.5), gs.ptr if per_site else None, gc.ptr, n,
+                      _stream())
+            torch.cuda.synchronize()
+            assert gc.intact() and (gs is None or gs.intact()), f"{r}: guard band overwritten"
+            assert np.array_equal(gc.host().reshape(want.shape), want), (r, per_site)
+    # four destinations, and the in-place sub_four
+    want = R.mult_adj_su3_mat_4vec(U, v[:, 0])
+    want = np.stack(want, 1) if isinstance(want, (tuple, list)) else want
+    ga, gb = Guarded(dt, U.size, U), Guarded(dt, v[:, 0].size, v[:, 0])
+    outs = [Guarded(dt, n * 6) for _ in range(4)]
+    _lib.call(f"su3g_mult_adj_su3_mat_4vec_{SFX[dt]}", ga.ptr, gb.ptr, *[o.ptr for o in outs], n, _stream())
+    torch.cuda.synchronize()
+    for d, o in enumerate(outs):
+        assert o.intact(), "mult_adj_su3_mat_4vec: guard band overwritten"
+        assert np.array_equal(o.host().reshape(n, 3, 2), want[:, d])
+    a = v[:, 0].copy()
+    want = R.sub_four_su3_vecs(a, v[:, 1], v[:, 2], v[:, 3], v[:, 0])
+    g = [Guarded(dt, n * 6, x) for x in (a, v[:, 1], v[:, 2], v[:, 3], v[:, 0])]
+    _lib.call(f"su3g_sub_four_su3_vecs_{SFX[dt]}", *[x.ptr for x in g], n, _stream())
+    torch.cuda.synchronize()
+    assert all(x.intact() for x in g), "sub_four_su3_vecs: guard band overwritten"
+    assert np.array_equal(g[0].host().reshape(n, 3, 2), want)
+
+
+@pytest.mark.parametrize("C", [6, 18, 72])
+def test_layout_transforms_guarded(dt, C):
+    dims = (48, 2, 4, 3)
+    F, nt = 48 * 2 * 4, 3
+    x = np.arange(F * nt * C, dtype=dt)
+    ga, gs, gb = Guarded(dt, x.size, x), Guarded(dt, x.size), Guarded(dt, x.size)
+    _lib.call(f"su3g_aos_to_soa_{SFX[dt]}", ga.ptr, gs.ptr, F, nt, C, _stream())
+    _lib.call(f"su3g_soa_to_aos_{SFX[dt]}", gs.ptr, gb.ptr, F, nt, C, _stream())
+    torch.cuda.synchronize()
+    assert ga.intact() and gs.intact() and gb.intact()
+    assert np.array_equal(gs.host(), _to_soa(x.reshape(F * nt, C), dims))
+    assert np.array_equal(gb.host(), x)
+
+
+NN_DIMS = [(64, 4, 4, 6), (32, 4, 6, 5), (48, 2, 4, 3), (8, 4, 4, 4), (5, 3, 2, 7)]
+
+
+def _fields(dims, dt, seed):
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(seed + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    return U, v, Guarded(dt, U.size, _to_soa(U, dims)), Guarded(dt, v.size, _to_soa(v, dims))
+
+
+@pytest.mark.parametrize("dims", NN_DIMS)
+@pytest.mark.parametrize("variant", [0, 1, 3, 4], ids=["auto", "generic", "tma", "ring"])
+def test_nn_sweep_guarded(dt, dims, variant):
+    U, v, gU, gv = _fields(dims, dt, 600)
+    want = coracle.nn_sweep(U, v, dims)
+    go = Guarded(dt, v.size)
+    _lib.set_option("nn_variant", variant)
+    try:
+        try:
+            _lib.call(f"su3g_nn_sweep_{SFX[dt]}", gU.ptr, gv.ptr, go.ptr, *dims, 0, dims[3], None, None, 0, _stream())
+        except ValueError as e:
+            if "not applicable" in str(e):
+                pytest.skip(str(e))
+            raise
+        torch.cuda.synchronize()
+    finally:
+        _lib.set_option("nn_variant", 0)
+    assert go.intact() and gU.intact() and gv.intact(), _lib.last_kernel()
+    assert np.array_equal(_from_soa(go.host(), dims, (3, 2)), want), _lib.last_kernel()
+
+
+@pytest.mark.parametrize("dims", [(64, 4, 4, 6), (48, 2, 4, 5), (8, 4, 4, 4)])
+def test_slab_pieces_guarded(dt, dims):
+    """interior range with halo faces, the halo pack and the fused edges launch, all guarded"""
+    U, v, gU, gv = _fields(dims, dt, 700)
+    nx, ny, nz, nt = dims
+    F = nx * ny * nz
+    want = coracle.nn_sweep(U, v, dims)
+    v_soa = _to_soa(v, dims)
+    g_vhi = Guarded(dt, 6 * F, v_soa[: 6 * F])       # periodic closure: v on slice 0
+    g_wlo = Guarded(dt, 6 * F)
+    _lib.call(f"su3g_nn_halo_w_{SFX[dt]}", gU.ptr, gv.ptr, g_wlo.ptr, *dims, 0, _stream())
+    go = Guarded(dt, v.size)
+    _lib.call(f"su3g_nn_sweep_{SFX[dt]}", gU.ptr, gv.ptr, go.ptr, *dims, 1, nt - 1, g_vhi.ptr, g_wlo.ptr, 0, _stream())
+    g_next = Guarded(dt, 6 * F)
+    _lib.call(f"su3g_nn_sweep_edges_{SFX[dt]}", gU.ptr, gv.ptr, go.ptr, *dims, g_vhi.ptr, g_wlo.ptr, g_next.ptr, 0,
+              _stream())
+    torch.cuda.synchronize()
+    assert all(g.intact() for g in (gU, gv, go, g_vhi, g_wlo, g_next))
+    assert np.array_equal(_from_soa(go.host(), dims, (3, 2)), want)
+    # w_next = U_t^dag out on the last slice == the pack kernel on out
+    g_chk = Guarded(dt, 6 * F)
+    _lib.call(f"su3g_nn_halo_w_{SFX[dt]}", gU.ptr, go.ptr, g_chk.ptr, *dims, 0, _stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(g_next.host(), g_chk.host())
+
+
+@pytest.mark.parametrize("dims", [(48, 4, 6, 7), (32, 8, 4, 6), (48, 2, 2, 3), (16, 8, 4, 6), (5, 3, 2, 7)])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "rows", "ring", "ring3"])
+def test_link_product_guarded(dt, dims, variant):
+    V = int(np.prod(dims))
+    U = inputs.random_links(inputs.config_rng(800 + V), V, 4, dtype=dt)
+    want = coracle.link_product(U, dims, 1 / 6)
+    gU, ga = Guarded(dt, U.size, _to_soa(U, dims)), Guarded(dt, V * 18)
+    _lib.set_option("link_variant", variant)
+    try:
+        try:
+            _lib.call(f"su3g_link_product_{SFX[dt]}", gU.ptr, ga.ptr, *dims, float(dt(1 / 6)), 0, _stream())
+        except ValueError as e:
+            if "not applicable" in str(e):
+                pytest.skip(str(e))
+            raise
+        torch.cuda.synchronize()
+    finally:
+        _lib.set_option("link_variant", 0)
+    assert ga.intact() and gU.intact(), _lib.last_kernel()
+    assert np.array_equal(_from_soa(ga.host(), dims, (3, 3, 2)), want), _lib.last_kernel()
+
+
+@pytest.mark.parametrize("dims", [(64, 4, 4, 6), (8, 4, 4, 4), (16, 2, 6, 4)])
+def test_dslash_guarded(dt, dims):
+    U, v, gU, gv = _fields(dims, dt, 900)
+    full = coracle.nn_sweep(U, v, dims)
+    C = {"U": 72, "v": 6}
+    gUe, gve = Guarded(dt, U.size), Guarded(dt, v.size)
+    _lib.call(f"su3g_soa_to_eo_{SFX[dt]}", gU.ptr, gUe.ptr, *dims, C["U"], _stream())
+    _lib.call(f"su3g_soa_to_eo_{SFX[dt]}", gv.ptr, gve.ptr, *dims, C["v"], _stream())
+    mask = np.zeros(int(np.prod(dims)), bool)
+    nx, ny, nz, nt = dims
+    t, z, y, x = np.meshgrid(np.arange(nt), np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    mask[((x + y + z + t) % 2 == 0).reshape(-1)] = True
+    for parity in (0, 1):
+        keep = mask if parity == 0 else ~mask
+        # parity kernel on SoA fields: the other parity's sites stay untouched (zeros here)
+        go = Guarded(dt, v.size, np.zeros(v.size, dt))
+        _lib.call(f"su3g_dslash_{SFX[dt]}", gU.ptr, gv.ptr, go.ptr, *dims, parity, 0, _stream())
+        # checkerboarded fields
+        goe, gback = Guarded(dt, v.size, np.zeros(v.size, dt)), Guarded(dt, v.size)
+        _lib.call(f"su3g_dslash_eo_{SFX[dt]}", gUe.ptr, gve.ptr, goe.ptr, *dims, parity, 0, _stream())
+        _lib.call(f"su3g_eo_to_soa_{SFX[dt]}", goe.ptr, gback.ptr, *dims, C["v"], _stream())
+        torch.cuda.synchronize()
+        assert all(g.intact() for g in (gU, gv, gUe, gve, go, goe, gback))
+        for g in (go, gback):
+            got = _from_soa(g.host(), dims, (3, 2))
+            assert np.array_equal(got[keep], full[keep])
+            assert not got[~keep].any()

@@ -313,7 +313,7 @@ def test_tma_variant_required_fails_loudly_when_inapplicable():
      (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33), (8, 4, 4, 3), (16, 8, 12, 5), (24, 4, 8, 1),
      (32, 4, 4, 6), (64, 4, 2, 3), (48, 48, 8, 4)],
 )
-@pytest.mark.parametrize("variant", [0, 1, 2], ids=["auto", "rows", "ring"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "rows", "ring", "ring3"])
 def test_link_product_bitwise(dims, precision, variant):
     from paper_1309_0551_b200 import _lib
 
@@ -327,7 +327,7 @@ def test_link_product_bitwise(dims, precision, variant):
         try:
             got = sweeps.link_product_aos(U, dims, 1 / 6)
         except ValueError as e:
-            if variant == 2 and "not applicable" in str(e):
+            if variant in (2, 3) and "not applicable" in str(e):
                 pytest.skip(f"ring walk not applicable to {dims}")
             raise
         assert np.array_equal(got, want), _lib.last_kernel()

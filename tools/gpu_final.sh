@@ -1,5 +1,6 @@
 #!/bin/bash
-# Round measurement pass: full GPU tests, smoke, the sanitizer driver (plain), the whole suite, the bench
+# Round measurement pass: full GPU tests, smoke, the sanitizer driver (plain, then under compute-sanitizer
+# memcheck / synccheck / racecheck on the su3g kernels), the whole suite, the bench
 # default (20 and 100 steps), and the bench default's ncu launch list.
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
@@ -9,6 +10,11 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 echo "smoke=$?" >> gpurun_out/status.txt
 timeout 600 python tools/sanitize_run.py > gpurun_out/sanitize_plain.log 2>&1
 echo "sanitize_plain=$?" >> gpurun_out/status.txt
+for tool in memcheck synccheck racecheck; do
+  timeout 1200 compute-sanitizer --tool $tool --kernel-name kns=4su3g --error-exitcode 9 --print-limit 50 \
+    python tools/sanitize_run.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "sanitize_$tool=$?" >> gpurun_out/status.txt
+done
 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
 echo "bench=$?" >> gpurun_out/status.txt
 python bench.py --steps 100 --warmup 5 --no-e2e > gpurun_out/bench_100.json 2> gpurun_out/bench_100.err
