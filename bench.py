@@ -73,6 +73,8 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-parity", action="store_true", help="skip the parity check of the timed path against the C oracle")
+    p.add_argument("--no-slab-probe", action="store_true",
+                   help="skip the one-GPU run of the N>1 per-rank t-slab schedule (nn workloads, N=1)")
     p.add_argument("--sites", type=int, default=64**4, help="sites for routine:<name> workloads")
     p.add_argument("--streams", type=int, default=16,
                    help="routine:<name> workloads below 2^20 sites: concurrent graph branches the independent "
@@ -201,14 +203,21 @@ def peak_hbm():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def traffic_for(workload: str, dtype: str):
-    """DRAM bytes per launch of the dominant kernel from a committed ncu capture, if any."""
+def traffic_for(workload: str, dtype: str, mode: str, kernel: str):
+    """DRAM bytes (read + write) per launch of the dominant kernel from a committed ncu --set full
+    capture (profiles/traffic.json), or None when no capture of THIS kernel exists: an entry counts
+    only if the kernel that ran starts with the kernel the capture measured."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(f"{workload}/{dtype}")
+            table = json.load(f)
     except Exception:  # noqa: BLE001
         return None
+    for key in (f"{workload}/{dtype}/{mode}", f"{workload}/{dtype}"):
+        e = table.get(key)
+        if isinstance(e, dict) and kernel and kernel.startswith(e.get("kernel", "\0")):
+            return e.get("bytes")
+    return None
 
 
 # ----------------------------------------------------------------------------
@@ -587,6 +596,11 @@ def run_b200(args, rank, world, local):
     if not args.no_e2e:
         e2e = measure_e2e(args, cfg, rank, world, dev, tdt, stream)
 
+    # ---- the N > 1 per-rank schedule, run on this one GPU ---------------------
+    slab_probe = None
+    if cfg["kind"] == "nn" and world == 1 and args.halo == "nccl" and not args.no_slab_probe:
+        slab_probe = _slab_schedule_probe(U, v0, va, vb, cfg["apps"], args, stream, value, elapsed_ms)
+
     line = {
         "metric": METRIC,
         "value": value,
@@ -622,7 +636,7 @@ def run_b200(args, rank, world, local):
             "frac": (achieved / peak) if achieved else None,
             "peak_datasheet": DATASHEET_HBM_GBS,
             "frac_datasheet": (achieved / DATASHEET_HBM_GBS) if achieved else None,
-            "traffic": traffic_for(args.workload, args.dtype),
+            "traffic": traffic_for(args.workload, args.dtype, args.mode, dispatched),
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kernel_avg_ms": kern_avg_ms,
         },
@@ -634,9 +648,63 @@ def run_b200(args, rank, world, local):
         "clocks": clocks.summary(),
         "e2e": e2e,
     }
+    if slab_probe is not None:
+        line["slab_schedule_1gpu"] = slab_probe
     if rank == 0 and not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args, cfg)
     return line
+
+
+def _slab_schedule_probe(U, v0, va, vb, apps, args, stream, value, elapsed_ms):
+    """The per-rank schedule of an N > 1 t-slab run, timed on this one GPU against itself.
+
+    A one-rank NCCL communicator sends the two halo faces to itself (su3g_slab_nn_sweep: halo pack,
+    grouped send/recv on the communicator's stream, the interior slices with 4 SMs left free for
+    NCCL's kernels, then both boundary slices in one launch) -- every launch and every SM
+    reservation of a multi-GPU rank, minus the NVLink transfer itself, which overlaps the interior.
+    Reported beside `value` as a predictor of the weak-scaling efficiency; it is NOT a multi-GPU
+    measurement (only one GPU is available here)."""
+    import torch
+
+    from paper_1309_0551_b200 import _lib as _l
+    from paper_1309_0551_b200.comm import NativeComm, native_slab_sweep
+
+    if U.lattice.nt < 3:
+        return None
+    saved = 0
+    _l.set_option("sm_reserve", 4)
+    try:
+        with NativeComm(1, 0, NativeComm.unique_id()) as comm:
+            def step():
+                src = v0
+                for i in range(apps):
+                    dst = va if i % 2 == 0 else vb
+                    native_slab_sweep(comm, U, src, dst, args.mode)
+                    src = dst
+
+            for _ in range(max(args.warmup, 3)):
+                step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            comm.check()
+            ms = e0.elapsed_time(e1)
+    finally:
+        _l.set_option("sm_reserve", saved)
+    sites = U.lattice.volume * apps * args.steps
+    probe_value = sites / (ms / 1e3)
+    return {
+        "value": probe_value, "unit": UNIT, "ms_per_step": ms / args.steps,
+        "vs_periodic_value": probe_value / value,
+        "what": "one GPU running the per-rank schedule of an N>1 t-slab run against a one-rank NCCL communicator "
+                "(self send/recv of both halo faces, halo pack, interior with 4 SMs reserved, fused boundary "
+                "launch); predicts the per-GPU rate at N>1 minus the NVLink transfer, which overlaps the interior. "
+                "Not a multi-GPU measurement.",
+    }
 
 
 def _exchange_faces(v_first, w_last, rank, world, dev):

@@ -344,296 +344,6 @@ static int run_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     return check_launch("link_product(ring)");
 }
 
-// ======================================================================================
-// Row-split ring walk (k_link_ring3): three compute lanes per site, lane r owns row r.
-//
-// k_link_ring keeps a whole site (A, T, C and the 18-real accumulator) in one thread: 255
-// registers at f64 with spills, one CTA of six compute warps per SM, too few to cover the
-// FP64 dependency and shared-memory latencies (0.53 of HBM in FMA mode, 0.30 exact).  Row i of
-// every product depends only on row i of its left operand:
-//     T[i][.] = a_i B          P[i][.] = T[i][.] C^dag          acc[i][.] (+)= s P[i][.]
-// so three lanes per site compute rows 0, 1, 2 independently, with exactly the per-element
-// operations (and plane order) of the one-thread form -- bit-identical in exact mode.  The live
-// set per lane is three 6-real rows (a_i, T_i, acc_i), the CTA runs 20 compute warps on the same
-// staged slots, and the three lanes of a site are consecutive (lane = 3 site + row), so every B / C
-// read from shared memory is one address per site: a broadcast, one wavefront for a warp's
-// eleven sites.
-//
-// The C operand of a t-plane, U_mu(x+t), is read straight from global memory.  The producer
-// prefetches those blocks into L2 one step ahead (slice t+2 while step t runs) and the lanes
-// pull their plane's C into L1 (prefetch.global.L1) one plane ahead of its use.
-// ======================================================================================
-
-namespace {
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-
-// T_r = a_r B (mult_su3_nn arithmetic for row r); B element (j, k) at bs[((3j+k)*2+q) * bstr]
-template <typename T, bool FUSED>
-__device__ __forceinline__ void nn_row(const T* a, const T* bs, int bstr, T* tr) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        if constexpr (FUSED)
-            cdot_fma<T, PLAIN, 3>([&](int j, int q) { return a[2 * j + q]; },
-                                  [&](int j, int q) { return bs[((3 * j + k) * 2 + q) * bstr]; }, tr[2 * k],
-                                  tr[2 * k + 1]);
-        else
-            cdot<T, PLAIN, 3>([&](int j, int q) { return a[2 * j + q]; },
-                              [&](int j, int q) { return bs[((3 * j + k) * 2 + q) * bstr]; }, tr[2 * k],
-                              tr[2 * k + 1]);
-    }
-}
-
-// acc_r (+)= s * T_r C^dag (mult_su3_na, then scalar_mult_add, for row r); C element (k, j) at c(k, j, q)
-template <typename T, bool FUSED, bool FIRST, class CF>
-__device__ __forceinline__ void na_row(const T* tr, CF c, T s, T* acc) {
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        T pr, pi;
-        if constexpr (FUSED)
-            cdot_fma<T, CONJ_Q, 3>([&](int j, int q) { return tr[2 * j + q]; },
-                                   [&](int j, int q) { return c(k, j, q); }, pr, pi);
-        else
-            cdot<T, CONJ_Q, 3>([&](int j, int q) { return tr[2 * j + q]; },
-                               [&](int j, int q) { return c(k, j, q); }, pr, pi);
-        if constexpr (FIRST) {
-            acc[2 * k] = FUSED ? fma(s, pr, T(0)) : xadd(T(0), xmul(s, pr));
-            acc[2 * k + 1] = FUSED ? fma(s, pi, T(0)) : xadd(T(0), xmul(s, pi));
-        } else {
-            acc[2 * k] = FUSED ? fma(s, pr, acc[2 * k]) : xadd(acc[2 * k], xmul(s, pr));
-            acc[2 * k + 1] = FUSED ? fma(s, pi, acc[2 * k + 1]) : xadd(acc[2 * k + 1], xmul(s, pi));
-        }
-    }
-}
-
-template <int NX>
-struct Ring3 {
-    static constexpr int N = 4 * NX;
-    static constexpr int NWC = (3 * N + 31) / 32;  // compute warps (48 x 2 x 2: 18, so 19 warps = 96 registers)
-    static constexpr int THREADS = 32 * NWC + 32;
-};
-
-}  // namespace
-
-template <typename T, bool FUSED, int NX>
-__global__ void __launch_bounds__(Ring3<NX>::THREADS, 1)
-    k_link_ring3(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapUy,
-                 const __grid_constant__ CUtensorMap mapUz, const T* __restrict__ U, T* __restrict__ acc_out,
-                 LinkRingParams p, T s) {
-    using G = LinkGeo<NX>;
-    constexpr int N = G::N, H = G::H, NWC = Ring3<NX>::NWC;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T* sm = reinterpret_cast<T*>(smem_raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::TOTAL);
-    uint64_t* empty = full + 4;
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int k = 0; k < 4; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], NWC);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const int64_t F = p.F;
-    const int GR = gridDim.x;
-    T* const E0 = sm + G::OFF0;
-    T* const E1 = sm + G::OFF1;
-    T* const E2 = sm + G::OFF2;
-    T* const E3 = sm + G::OFF3;
-
-    // ------------------------------------------------------------------ producer warp
-    if (tid >= 32 * NWC) {
-        if (tid != 32 * NWC) return;
-        uint64_t pol;
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-        uint32_t n = 0;  // steps issued
-        for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
-            int64_t blk;
-            int t0, t1;
-            link_item(p, item, blk, t0, t1);
-            const int y0 = static_cast<int>(blk % p.nby) * 2, z0 = static_cast<int>(blk / p.nby) * 2;
-            const int yup = (y0 + 2) % p.ny, zup = (z0 + 2) % p.nz;
-            {  // the first step's t-plane C operands (U_0..U_2 of slice t0+1)
-                const int tn = (t0 + 1 == p.nt) ? 0 : t0 + 1;
-                tma_prefetch_4d(&mapU, 0, y0, z0, tn * 72);
-                tma_prefetch_4d(&mapU, 0, y0, z0, tn * 72 + 18);
-                tma_prefetch_4d(&mapU, 0, y0, z0, tn * 72 + 36);
-            }
-            for (int t = t0; t < t1; ++t, ++n) {
-                const int tn = (t + 1 == p.nt) ? 0 : t + 1;
-                const int tn2 = (tn + 1 == p.nt) ? 0 : tn + 1;
-                // L2 warm-up one step ahead: the next step's U_3 block and halo rows, and U_0..U_2 of
-                // slice t+2 (the next step's t-plane C operands; its E0..E2 blocks the step after)
-                tma_prefetch_4d(&mapU, 0, y0, z0, tn * 72 + 54);
-                tma_prefetch_4d(&mapUy, 0, yup, z0, tn * 72);
-                tma_prefetch_4d(&mapUy, 0, yup, z0, tn * 72 + 36);
-                tma_prefetch_4d(&mapUy, 0, yup, z0, tn * 72 + 54);
-                tma_prefetch_4d(&mapUz, 0, y0, zup, tn * 72);
-                tma_prefetch_4d(&mapUz, 0, y0, zup, tn * 72 + 18);
-                tma_prefetch_4d(&mapUz, 0, y0, zup, tn * 72 + 54);
-                if (t + 1 < t1) {
-                    tma_prefetch_4d(&mapU, 0, y0, z0, tn2 * 72);
-                    tma_prefetch_4d(&mapU, 0, y0, z0, tn2 * 72 + 18);
-                    tma_prefetch_4d(&mapU, 0, y0, z0, tn2 * 72 + 36);
-                }
-                const uint32_t par = (n + 1) & 1;
-                const int b = t * 72;
-                if (n) mbar_wait(&empty[0], par);
-                mbar_arrive_expect_tx(&full[0], uint32_t(G::SZ0) * sizeof(T));
-                tma_load_4d(E0, &mapU, 0, y0, z0, b, &full[0], pol);
-                tma_load_4d(E0 + G::ROW1, &mapUy, 0, yup, z0, b, &full[0], pol);
-                tma_load_4d(E0 + G::ROW2, &mapUz, 0, y0, zup, b, &full[0], pol);
-                if (n) mbar_wait(&empty[1], par);
-                mbar_arrive_expect_tx(&full[1], uint32_t(G::SZ1) * sizeof(T));
-                tma_load_4d(E1, &mapU, 0, y0, z0, b + 18, &full[1], pol);
-                tma_load_4d(E1 + G::ROW1, &mapUz, 0, y0, zup, b + 18, &full[1], pol);
-                if (n) mbar_wait(&empty[2], par);
-                mbar_arrive_expect_tx(&full[2], uint32_t(G::SZ2) * sizeof(T));
-                tma_load_4d(E2, &mapU, 0, y0, z0, b + 36, &full[2], pol);
-                tma_load_4d(E2 + G::ROW1, &mapUy, 0, yup, z0, b + 36, &full[2], pol);
-                if (n) mbar_wait(&empty[3], par);
-                mbar_arrive_expect_tx(&full[3], uint32_t(G::SZ3) * sizeof(T));
-                tma_load_4d(E3, &mapU, 0, y0, z0, b + 54, &full[3], pol);
-                tma_load_4d(E3 + G::ROW1, &mapUy, 0, yup, z0, b + 54, &full[3], pol);
-                tma_load_4d(E3 + G::ROW2, &mapUz, 0, y0, zup, b + 54, &full[3], pol);
-            }
-        }
-        return;
-    }
-
-    // ------------------------------------------------------------------ compute warps
-    const int lane = tid & 31;
-    const bool active = tid < 3 * N;
-    const int sl = active ? tid / 3 : 0;  // inactive lanes shadow site 0 and never store
-    const int row = active ? tid - 3 * (tid / 3) : 0;
-    const int lx = sl % NX, ly = (sl / NX) & 1, lz = sl / (2 * NX);
-    const int ix_up = (lx + 1 == NX) ? sl - lx : sl + 1;
-    const int jy = lx + NX * lz, jz = lx + NX * ly;
-    const int y_off = ly == 0 ? sl + NX : G::ROW1 + jy, y_str = ly == 0 ? N : H;
-    const int z_off0 = lz == 0 ? sl + 2 * NX : G::ROW2 + jz;
-    const int z_off1 = lz == 0 ? sl + 2 * NX : G::ROW1 + jz;
-    const int z_str = lz == 0 ? N : H;
-    const int a0 = 6 * row * N + sl;  // row `row` of the site's own link in a slot: a0 + c*N, c < 6
-
-    auto release = [&](int k) { warp_release(&empty[k], lane); };
-    auto smem_c = [](const T* base, int str) {
-        return [=](int k, int j, int q) { return base[((3 * k + j) * 2 + q) * str]; };
-    };
-
-    uint32_t n = 0;
-    for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
-        int64_t blk;
-        int t0, t1;
-        link_item(p, item, blk, t0, t1);
-        const int y = static_cast<int>(blk % p.nby) * 2 + ly;
-        const int z = static_cast<int>(blk / p.nby) * 2 + lz;
-        const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
-        for (int t = t0; t < t1; ++t, ++n) {
-            const uint32_t par = n & 1;
-            const int tn = (t + 1 == p.nt) ? 0 : t + 1;
-            const T* up = U + int64_t(tn) * 72 * F + s3;  // this site's links one slice up
-            auto glob_c = [=](const T* base) {
-                return [=](int k, int j, int q) { return __ldg(base + ((3 * k + j) * 2 + q) * F); };
-            };
-            auto pull_c = [&](int mu) {  // L1 prefetch of row `row` of U_mu(x+t): the site's three lanes cover C
-#pragma unroll
-                for (int c = 0; c < 6; ++c) prefetch_l1(up + (mu * 18 + 6 * row + c) * F);
-            };
-            T a[6], tr[6], acc[6];
-            auto load_a = [&](const T* slot) {
-#pragma unroll
-                for (int c = 0; c < 6; ++c) a[c] = slot[a0 + c * N];
-            };
-            pull_c(0);
-            // ---- (0,1): A = U_0(x), B = U_1(x+0), C = U_0(x+1)
-            mbar_wait(&full[0], par);
-            mbar_wait(&full[1], par);
-            load_a(E0);
-            nn_row<T, FUSED>(a, E1 + ix_up, N, tr);
-            na_row<T, FUSED, true>(tr, smem_c(E0 + y_off, y_str), s, acc);
-            // ---- (0,2): B = U_2(x+0), C = U_0(x+2)
-            mbar_wait(&full[2], par);
-            nn_row<T, FUSED>(a, E2 + ix_up, N, tr);
-            na_row<T, FUSED, false>(tr, smem_c(E0 + z_off0, z_str), s, acc);
-            // ---- (0,3): B = U_3(x+0), C = U_0(x+t) (global, L1-prefetched)
-            mbar_wait(&full[3], par);
-            nn_row<T, FUSED>(a, E3 + ix_up, N, tr);
-            release(0);
-            pull_c(1);
-            na_row<T, FUSED, false>(tr, glob_c(up), s, acc);
-            // ---- (1,2): A = U_1(x), B = U_2(x+1), C = U_1(x+2)
-            load_a(E1);
-            nn_row<T, FUSED>(a, E2 + y_off, y_str, tr);
-            na_row<T, FUSED, false>(tr, smem_c(E1 + z_off1, z_str), s, acc);
-            // ---- (1,3): B = U_3(x+1), C = U_1(x+t)
-            nn_row<T, FUSED>(a, E3 + y_off, y_str, tr);
-            release(1);
-            pull_c(2);
-            na_row<T, FUSED, false>(tr, glob_c(up + 18 * F), s, acc);
-            // ---- (2,3): A = U_2(x), B = U_3(x+2), C = U_2(x+t)
-            load_a(E2);
-            nn_row<T, FUSED>(a, E3 + z_off0, z_str, tr);
-            release(2);
-            release(3);
-            na_row<T, FUSED, false>(tr, glob_c(up + 36 * F), s, acc);
-            if (active) {
-                T* o = acc_out + (int64_t(t) * 18 + 6 * row) * F + s3;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) o[k * F] = acc[k];
-            }
-        }
-    }
-}
-
-template <typename T, bool FUSED, int NX>
-static int run_link_ring3(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
-    using G = LinkGeo<NX>;
-    constexpr int THREADS = Ring3<NX>::THREADS;
-    CUtensorMap mU, mUy, mUz;
-    if (!make_map<T>(&mU, U, nx, ny, nz, int64_t(nt) * 72, 2, 2, 18) ||
-        !make_map<T>(&mUy, U, nx, ny, nz, int64_t(nt) * 72, 1, 2, 18) ||
-        !make_map<T>(&mUz, U, nx, ny, nz, int64_t(nt) * 72, 2, 1, 18))
-        return 1;
-    const size_t smem = size_t(G::TOTAL) * sizeof(T) + 8 * sizeof(uint64_t);
-    const DeviceInfo& di = device_info();
-    if (smem > size_t(di.max_smem_optin)) return 1;
-    auto kern = k_link_ring3<T, FUSED, NX>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    LinkRingParams p{};
-    p.ny = ny; p.nz = nz; p.nt = nt;
-    p.F = int64_t(nx) * ny * nz;
-    p.nby = ny / 2;
-    p.nblocks = int64_t(ny / 2) * (nz / 2);
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
-    const int Gfull = di.num_sms * std::max(per_sm, 1);
-    p.chunk = pick_chunk(p.nblocks, nt, Gfull);
-    p.nitems = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
-    const int grid = static_cast<int>(std::min<int64_t>(Gfull, p.nitems));
-    kern<<<grid, THREADS, smem, st>>>(mU, mUy, mUz, U, acc, p, s);
-    note_kernel(std::string("k_link_ring3<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x2x2" +
-                (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") + ",chunk " + std::to_string(p.chunk) + ">");
-    return check_launch("link_product(ring3)");
-}
-
-// 1 = not applicable to this lattice (caller falls back)
-template <typename T, bool FUSED>
-int launch_link_ring3(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
-    if (ny % 2 || nz % 2 || !aligned16(U)) return 1;
-    if (nx == 48) return run_link_ring3<T, FUSED, 48>(U, acc, nx, ny, nz, nt, s, st);
-    if (nx == 32) return run_link_ring3<T, FUSED, 32>(U, acc, nx, ny, nz, nt, s, st);
-    if (nx == 64 && sizeof(T) == 4) return run_link_ring3<T, FUSED, 64>(U, acc, nx, ny, nz, nt, s, st);
-    return 1;
-}
-
-template int launch_link_ring3<float, false>(const float*, float*, int, int, int, int, float, cudaStream_t);
-template int launch_link_ring3<float, true>(const float*, float*, int, int, int, int, float, cudaStream_t);
-template int launch_link_ring3<double, false>(const double*, double*, int, int, int, int, double, cudaStream_t);
-template int launch_link_ring3<double, true>(const double*, double*, int, int, int, int, double, cudaStream_t);
-
 // 1 = not applicable to this lattice (caller falls back)
 template <typename T, bool FUSED>
 int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {

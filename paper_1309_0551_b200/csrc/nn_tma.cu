@@ -375,11 +375,13 @@ __global__ void __launch_bounds__(NTHR, 1)
                 ut[q] = ut1[q];
                 ut1[q] = ut2[q];
             }
-            fence_before_refill();
             named_sync<NTHR>();  // exchange buffer and stage s free for the next step
             // refill stage s with step k + 2: every thread is past its last read of it, so
             // no empty-barrier wait is needed (and warp 0 never stalls mid-step)
-            if (tid == 0 && c2.valid) issue(s, c2.blk, c2.t);
+            if (tid == 0 && c2.valid) {
+                fence_before_refill();  // the step's reads of stage s (ordered by the barrier) before the TMA refill
+                issue(s, c2.blk, c2.t);
+            }
         }
     }
 }

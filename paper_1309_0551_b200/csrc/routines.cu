@@ -280,9 +280,11 @@ __global__ void __launch_bounds__(Geometry<Op>::TS)
         if (has_s) s = reinterpret_cast<const T*>(base + G::A_BYTES + G::B_BYTES)[tid];
 
         if (tid == 0) bulk_wait_read<1>();  // result buffer (k & 1) released by the store of tile k-2
-        fence_before_refill();
         __syncthreads();                     // stage st fully consumed; obuf (k & 1) free
-        if (tid == 0 && k + STAGES < count) issue(first + (k + STAGES) * stride, st);
+        if (tid == 0 && k + STAGES < count) {
+            fence_before_refill();           // the barrier's reads of stage st before the bulk refill
+            issue(first + (k + STAGES) * stride, st);
+        }
 
         Op::apply(a, b, s, c);
         T* ob = obuf + (k & 1) * TS * Op::NC;

@@ -130,10 +130,11 @@ template <int N> __device__ __forceinline__ void bulk_wait() {
 // make generic-proxy shared-memory writes visible to the async (bulk copy) proxy
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// A thread's shared-memory READS of a staging buffer (generic proxy) must be ordered before the
-// TMA / bulk copy (async proxy) that refills it: every reading thread fences before the barrier or
-// mbarrier arrive that hands the buffer back to the producer.  Without it an LDS still queued at
-// the arrive can observe the refill (seen on B200: k_nn_ring, 2 CTAs/SM, FMA mode).
+// Shared-memory READS of a staging buffer (generic proxy) must be ordered before the TMA / bulk
+// copy (async proxy) that refills it.  Where the hand-back is an mbarrier arrive (warp-specialised
+// rings) every reading lane fences before the arrive: without it an LDS still queued at the arrive
+// can observe the refill (seen on B200: k_nn_ring, 2 CTAs/SM, FMA mode).  Where it is a CTA
+// barrier, the barrier completes the reads and the issuing thread fences before the refill.
 #ifndef SU3G_RELEASE_FENCE
 #define SU3G_RELEASE_FENCE 1
 #endif

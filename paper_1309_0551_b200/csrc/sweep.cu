@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256)
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
-static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk, 3 row-split ring walk
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk, 3 row-split carried t-walk
 
 // largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
 static int chunk_planes(int nz, int cap) {
@@ -297,15 +297,17 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("link_product: mode must be SU3G_EXACT or SU3G_FMA");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int lv = g_link_variant.load();
-    // auto: the ring walk for the f64 FMA product (48^4: 0.534 vs 0.519 of HBM for the rows gather);
-    // exact f64 (FP64-issue bound: 0.457 rows vs 0.295 ring) and f32 (0.305 vs 0.224) stay on rows
-    if (lv == 3) {
-        const int rc = mode == SU3G_FMA ? launch_link_ring3<T, true>(U, acc, nx, ny, nz, nt, s, st)
-                                        : launch_link_ring3<T, false>(U, acc, nx, ny, nz, nt, s, st);
+    // auto (48^4 on B200, fraction of HBM, profiles/r02/ab_link_walk.md): f32 exact -> the row-split
+    // carried t-walk (0.351 vs rows 0.309); f64 FMA -> the ring walk (0.546 vs rows 0.525, walk 0.493);
+    // f64 exact (rows 0.465, walk 0.461) and f32 FMA (ring 0.397, walk 0.394, rows 0.357) -> below
+    const bool auto_walk = lv == 0 && sizeof(T) == 4 && mode == SU3G_EXACT;
+    if (auto_walk || lv == 3) {
+        const int rc = mode == SU3G_FMA ? launch_link_walk<T, true>(U, acc, nx, ny, nz, nt, s, st)
+                                        : launch_link_walk<T, false>(U, acc, nx, ny, nz, nt, s, st);
         if (rc != 1) return rc;
-        return fail_invalid("link_product: row-split ring kernel not applicable to this lattice");
+        if (lv == 3) return fail_invalid("link_product: row-split walk kernel not applicable to this lattice");
     }
-    const bool auto_ring = lv == 0 && sizeof(T) == 8 && mode == SU3G_FMA;
+    const bool auto_ring = lv == 0 && mode == SU3G_FMA;
     if (auto_ring || lv == 2) {
         const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
                                         : launch_link_ring<T, false>(U, acc, nx, ny, nz, nt, s, st);
@@ -339,7 +341,7 @@ int su3g_set_option(const char* name, int64_t value) {
     if (std::strcmp(name, "link_variant") == 0) {
         if (value < 0 || value > 3)
             return fail_invalid(
-                "set_option: link_variant must be 0 (auto), 1 (rows gather), 2 (tma ring walk) or 3 (row-split ring walk)");
+                "set_option: link_variant must be 0 (auto), 1 (rows gather), 2 (tma ring walk) or 3 (row-split walk)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -44,7 +44,8 @@ __device__ __forceinline__ T ld_stream(const T* p, uint64_t pol) {
 // relative cost of a work item's prologue, in steps (su3g_set_option("chunk_prologue_x10"))
 inline double g_prologue_cost = 2.0;
 
-inline int pick_chunk(int64_t nblocks, int nt_range, int G) {
+inline int pick_chunk(int64_t nblocks, int nt_range, int G, double prologue = -1.0) {
+    const double cost = prologue >= 0 ? prologue : g_prologue_cost;
     int best_L = nt_range;
     double best_eff = -1;
     for (int L = nt_range; L >= 1; --L) {
@@ -52,7 +53,7 @@ inline int pick_chunk(int64_t nblocks, int nt_range, int G) {
         const int64_t items = nblocks * nchunks;
         const int64_t per = (items + G - 1) / G;
         const double work = double(nblocks) * nt_range;
-        const double eff = work / (double(per) * G * L) * (L / (L + g_prologue_cost));
+        const double eff = work / (double(per) * G * L) * (L / (L + cost));
         if (eff > best_eff + 1e-9) {
             best_eff = eff;
             best_L = L;
@@ -78,9 +79,9 @@ int launch_dslash_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, in
 // link product on the TMA ring t-walk (link_ring.cu); 1 = not applicable
 template <typename T, bool FUSED>
 int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
-// row-split ring walk (three lanes per site, link_ring.cu); 1 = not applicable
+// row-split t-walk with carried t-planes (link_walk.cu); 1 = not applicable
 template <typename T, bool FUSED>
-int launch_link_ring3(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
+int launch_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);
 

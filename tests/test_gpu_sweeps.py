@@ -111,8 +111,12 @@ def test_link_product_config3_f32_full_size():
     rng = inputs.config_rng(33)
     U = inputs.random_links(rng, 48**4, 4, dtype=np.float32)
     want = coracle.link_product(U, dims, 1 / 6)
+    from paper_1309_0551_b200 import _lib
+
     assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
+    assert _lib.last_kernel().startswith("k_link_walk<f32,48x3x1"), _lib.last_kernel()  # exact f32: the carried walk
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-5
+    assert _lib.last_kernel().startswith("k_link_ring<f32,48x2x2"), _lib.last_kernel()
 
 
 @pytest.mark.parametrize("C", [6, 18, 24, 72])
@@ -313,7 +317,7 @@ def test_tma_variant_required_fails_loudly_when_inapplicable():
      (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33), (8, 4, 4, 3), (16, 8, 12, 5), (24, 4, 8, 1),
      (32, 4, 4, 6), (64, 4, 2, 3), (48, 48, 8, 4)],
 )
-@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "rows", "ring", "ring3"])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "rows", "ring", "walk"])
 def test_link_product_bitwise(dims, precision, variant):
     from paper_1309_0551_b200 import _lib
 
