@@ -203,6 +203,26 @@ def peak_hbm():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def _compute_floor(cfg, args, bytes_per_launch, kern_avg_ms):
+    """Exact-mode FP-pipe time of one launch (every flop one FMUL/FADD or DMUL/DADD, flops.py) beside the
+    HBM time of its algorithmic bytes: which roof binds.  None for FMA mode (fused ops) and routines."""
+    from paper_1309_0551_b200 import flops as _flops
+
+    if cfg["kind"] not in ("nn", "link", "dslash") or args.mode != "exact" or not kern_avg_ms:
+        return None
+    per_site = _flops.intensity(cfg["kind"], args.dtype)["bytes_per_site"]
+    if cfg["kind"] == "dslash":
+        per_site = DSLASH_BYTES[args.dtype]
+    sites = bytes_per_launch / per_site
+    if cfg["kind"] == "dslash":
+        sites /= 2  # one parity launch computes half of the sites
+    fp_ms = _flops.compute_floor_s(cfg["kind"], args.dtype, int(sites)) * 1e3
+    hbm_ms = bytes_per_launch / (peak_hbm()[0] * 1e9) * 1e3
+    return {"fp_pipe_ms": fp_ms, "hbm_ms": hbm_ms, "bound": "fp-pipe" if fp_ms > hbm_ms else "hbm",
+            "max_hbm_frac": min(1.0, hbm_ms / fp_ms), "frac_of_binding_roof": max(fp_ms, hbm_ms) / kern_avg_ms,
+            "pipe": "FP32 128 / FP64 64 lanes per SM per clock x 148 SMs x 1.965 GHz, one instruction per flop"}
+
+
 def traffic_for(workload: str, dtype: str, mode: str, kernel: str):
     """DRAM bytes (read + write) per launch of the dominant kernel from a committed ncu --set full
     capture (profiles/traffic.json), or None when no capture of THIS kernel exists: an entry counts
@@ -639,6 +659,7 @@ def run_b200(args, rank, world, local):
             "traffic": traffic_for(args.workload, args.dtype, args.mode, dispatched),
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kernel_avg_ms": kern_avg_ms,
+            "compute_floor": _compute_floor(cfg, args, bytes_per_launch, kern_avg_ms),
         },
         "flops_per_site": intensity["flops_per_site"],
         "ai_flop_per_byte": intensity["ai_flop_per_byte"],

@@ -341,6 +341,298 @@ static int run_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     return check_launch("link_product(walk)");
 }
 
+// ======================================================================================
+// FMA mode: two lanes per site, three planes each (k_link_pair).
+//
+// With FMA chains the plane order is free (the north-star tolerance, not bit equality), so a site's
+// six planes split over two adjacent lanes that each own whole products: lane 0 takes (0,2) (1,2)
+// (2,3), lane 1 takes (0,1) (1,3) (0,3), one plane per lane per phase, and the two partial
+// accumulators meet through one shuffle at the end.  Unlike the row split, each lane reads a
+// distinct operand, so shared memory delivers every staged link once per use (a third of the
+// walk's wavefronts).  The t-planes read C = U_mu(x+t) from the NEXT slice's E0..E2, which the
+// double-buffered slots hold during the step (no carry): the producer loads slice t+1 while step t
+// starts.  Phase p of the step (lane 0 | lane 1):
+//   p0  (0,2): A U_0, B U_2(x+0), C U_0(x+2) [Z chunk 0]   | (0,1): A U_0, B U_1(x+0), C U_0(x+1)
+//   p1  (1,2): A U_1, B U_2(x+1), C U_1(x+2) [Z chunk 1]   | (1,3): A U_1, B U_3(x+1), C U_1(x+t)
+//   p2  (2,3): A U_2, B U_3(x+2) [Z chunk 2], C U_2(x+t)   | (0,3): A U_0, B U_3(x+0), C U_0(x+t)
+// so one Z chunk is live per phase and a ring of two Z slots suffices.
+// ======================================================================================
+
+template <typename T, int NX, int BY>
+struct PairGeo {
+    static constexpr int N = NX * BY;
+    static_assert(N % 16 == 0, "a warp covers 16 sites x 2 lanes");
+    static constexpr int NWC = N / 16;
+    static constexpr int THREADS = 32 * NWC + 32;
+    static constexpr int BLK = 18 * N;
+    static constexpr int YSZ = 54 * NX;
+    static constexpr int OFF_E = 0;                 // E[k][b] (link k of the block, buffer b) at (2k + b) * BLK
+    static constexpr int OFF_E3 = 6 * BLK;
+    static constexpr int OFF_Y = 7 * BLK;
+    static constexpr int OFF_Z = 7 * BLK + YSZ;     // Z[j] at OFF_Z + j * BLK
+    static constexpr int TOTAL = 9 * BLK + YSZ;
+    static constexpr int NBAR = 10;                 // E[k][b] (6), E3, Y, Z0, Z1
+};
+
+namespace {
+
+// acc (+)= s * (A B) C^dag with FMA chains; A in a[18] registers, B / C element (r, c) at ptr[((3r+c)*2+q) * str]
+template <typename T, bool FIRST>
+__device__ __forceinline__ void plane_fma(const T* a, const T* bs, int bstr, const T* cs, int cstr, T s, T* acc) {
+    T tm[18];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T bc[6];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            bc[2 * j] = bs[((3 * j + k) * 2) * bstr];
+            bc[2 * j + 1] = bs[((3 * j + k) * 2 + 1) * bstr];
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            cdot_fma<T, PLAIN, 3>([&](int j, int q) { return a[(3 * i + j) * 2 + q]; },
+                                  [&](int j, int q) { return bc[2 * j + q]; }, tm[(3 * i + k) * 2],
+                                  tm[(3 * i + k) * 2 + 1]);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T cr[6];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            cr[2 * j] = cs[((3 * k + j) * 2) * cstr];
+            cr[2 * j + 1] = cs[((3 * k + j) * 2 + 1) * cstr];
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            T pr, pi;
+            cdot_fma<T, CONJ_Q, 3>([&](int j, int q) { return tm[(3 * i + j) * 2 + q]; },
+                                   [&](int j, int q) { return cr[2 * j + q]; }, pr, pi);
+            const int e = (3 * i + k) * 2;
+            acc[e] = fma(s, pr, FIRST ? T(0) : acc[e]);
+            acc[e + 1] = fma(s, pi, FIRST ? T(0) : acc[e + 1]);
+        }
+    }
+}
+
+}  // namespace
+
+template <typename T, int NX, int BY>
+__global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
+    k_link_pair(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapY,
+                T* __restrict__ acc_out, WalkParams p, T s) {
+    using G = PairGeo<T, NX, BY>;
+    constexpr int N = G::N, NWC = G::NWC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::TOTAL);
+    uint64_t* empty = full + G::NBAR;
+    constexpr int B_E3 = 6, B_Y = 7, B_Z = 8;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int k = 0; k < G::NBAR; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], NWC);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int GR = gridDim.x;
+
+    if (tid >= 32 * NWC) {  // ------------------------------------------ producer warp
+        if (tid != 32 * NWC) return;
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        uint32_t ne = 0, n3 = 0, ny_ = 0, nz_ = 0;  // ne: slices loaded (buffer ne & 1)
+        auto load_blk = [&](int bar, uint32_t use, T* dst, int y0, int z0, int plane) {
+            if (use) mbar_wait(&empty[bar], (use - 1) & 1);
+            mbar_arrive_expect_tx(&full[bar], G::BLK * sizeof(T));
+            tma_load_4d(dst, &mapB, 0, y0, z0, plane, &full[bar], pol);
+        };
+        auto load_link = [&](int k, uint32_t slice_no, int ts, int y0, int z0) {  // link k of slice load slice_no
+            const int b = slice_no & 1;
+            load_blk(2 * k + b, slice_no >> 1, sm + G::OFF_E + (2 * k + b) * G::BLK, y0, z0, ts * 72 + 18 * k);
+        };
+        auto load_z = [&](int y0, int zup, int plane) {
+            const int j = nz_ & 1;
+            load_blk(B_Z + j, nz_ >> 1, sm + G::OFF_Z + j * G::BLK, y0, zup, plane);
+            ++nz_;
+        };
+        for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
+            int64_t blk;
+            int t0, t1;
+            walk_item(p, item, blk, t0, t1);
+            const int y0 = static_cast<int>(blk % p.nby) * BY, z0 = static_cast<int>(blk / p.nby);
+            const int yup = (y0 + BY) % p.ny, zup = (z0 + 1) % p.nz;
+            for (int k = 0; k < 3; ++k) load_link(k, ne, t0, y0, z0);
+            ++ne;
+            for (int t = t0; t < t1; ++t) {
+                const int tn = (t + 1 == p.nt) ? 0 : t + 1;
+                // issue order = the order the previous step releases the slots (monotone waits):
+                // Y, Z0 and U_1 of slice t-1 free after phase 1, E3 / Z1 / U_0 / U_2 at its end, Z3
+                // after this step's phase 0
+                if (ny_) mbar_wait(&empty[B_Y], (ny_ - 1) & 1);
+                mbar_arrive_expect_tx(&full[B_Y], G::YSZ * sizeof(T));
+                T* yd = sm + G::OFF_Y;
+                tma_load_4d(yd, &mapY, 0, yup, z0, t * 72, &full[B_Y], pol);
+                tma_load_4d(yd + 18 * NX, &mapY, 0, yup, z0, t * 72 + 36, &full[B_Y], pol);
+                tma_load_4d(yd + 36 * NX, &mapY, 0, yup, z0, t * 72 + 54, &full[B_Y], pol);
+                ++ny_;
+                load_z(y0, zup, t * 72);                // U_0 on +z: phase 0
+                load_link(1, ne, tn, y0, z0);           // U_1(x+t): phase 1
+                load_blk(B_E3, n3, sm + G::OFF_E3, y0, z0, t * 72 + 54);
+                ++n3;
+                load_z(y0, zup, t * 72 + 18);           // U_1 on +z: phase 1
+                load_link(0, ne, tn, y0, z0);           // U_0(x+t), U_2(x+t): phase 2
+                load_link(2, ne, tn, y0, z0);
+                ++ne;
+                load_z(y0, zup, t * 72 + 54);           // U_3 on +z: phase 2
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------------ compute warps
+    // a warp covers 16 consecutive sites twice: lanes 0-15 take planes (0,2) (1,2) (2,3), lanes 16-31
+    // (0,1) (1,3) (0,3), so every 64-bit shared load of a half-warp reads one slot, 16 sites, 128 B
+    const int lane = tid & 31;
+    const int sl = (tid >> 5) * 16 + (lane & 15);
+    const int h = lane >> 4;
+    const int lx = sl % NX, ly = sl / NX;
+    const int ix_up = (lx + 1 == NX) ? sl - lx : sl + 1;
+    const bool y_in = ly + 1 < BY;
+    const T* const Y = sm + G::OFF_Y;
+    const T* const E3 = sm + G::OFF_E3;
+    auto release = [&](int bar) { warp_release(&empty[bar], lane); };
+    auto wait_full = [&](int bar, uint32_t use) { mbar_wait(&full[bar], use & 1); };
+    auto E = [&](int k, uint32_t slice_no) { return sm + G::OFF_E + (2 * k + (slice_no & 1)) * G::BLK; };
+
+    uint32_t ne = 0, n3 = 0, ny_ = 0, nz_ = 0;
+    for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
+        int64_t blk;
+        int t0, t1;
+        walk_item(p, item, blk, t0, t1);
+        const int y = static_cast<int>(blk % p.nby) * BY + ly;
+        const int z = static_cast<int>(blk / p.nby);
+        const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
+        for (int t = t0; t < t1; ++t) {
+            const uint32_t c = ne, n = ne + 1;  // slice loads of t and t+1
+            const T *E0c = E(0, c), *E1c = E(1, c), *E2c = E(2, c);
+            for (int k = 0; k < 3; ++k) wait_full(2 * k + (c & 1), c >> 1);
+            T acc[18], a[18];
+            // ---- phase 0: (0,2) C = U_0(x+2) on Z chunk 0 | (0,1) C = U_0(x+1)
+            {
+                const int zb = B_Z + (nz_ & 1);
+                const T* Z = sm + G::OFF_Z + (nz_ & 1) * G::BLK;
+                wait_full(zb, nz_ >> 1);
+                wait_full(B_Y, ny_);
+#pragma unroll
+                for (int q = 0; q < 18; ++q) a[q] = E0c[q * N + sl];  // U_0(x)
+                const T* bs = (h ? E1c : E2c) + ix_up;                  // U_1(x+0) | U_2(x+0)
+                const T* cs = h ? (y_in ? E0c + sl + NX : Y + lx) : Z + sl;
+                const int cstr = (h && !y_in) ? NX : N;
+                plane_fma<T, true>(a, bs, N, cs, cstr, s, acc);
+                release(zb);
+                ++nz_;
+            }
+            // ---- phase 1: (1,2) B = U_2(x+1), C = U_1(x+2) on Z chunk 1 | (1,3) B = U_3(x+1), C = U_1(x+t)
+            wait_full(B_E3, n3);
+            wait_full(2 + (n & 1), n >> 1);
+            {
+                const int zb = B_Z + (nz_ & 1);
+                const T* Z = sm + G::OFF_Z + (nz_ & 1) * G::BLK;
+                wait_full(zb, nz_ >> 1);
+#pragma unroll
+                for (int q = 0; q < 18; ++q) a[q] = E1c[q * N + sl];  // U_1(x)
+                const T* bs = y_in ? (h ? E3 : E2c) + sl + NX : Y + (h ? 36 : 18) * NX + lx;
+                const int bstr = y_in ? N : NX;
+                const T* cs = h ? E(1, n) + sl : Z + sl;
+                plane_fma<T, false>(a, bs, bstr, cs, N, s, acc);
+                release(zb);
+                ++nz_;
+            }
+            release(B_Y);
+            ++ny_;
+            release(2 + (c & 1));  // U_1 of slice t: its buffer takes U_1 of slice t+2
+            // ---- phase 2: (2,3) A = U_2, B = U_3(x+2) on Z chunk 2, C = U_2(x+t) | (0,3) A = U_0, B = U_3(x+0), C = U_0(x+t)
+            wait_full(0 + (n & 1), n >> 1);
+            wait_full(4 + (n & 1), n >> 1);
+            {
+                const int zb = B_Z + (nz_ & 1);
+                const T* Z = sm + G::OFF_Z + (nz_ & 1) * G::BLK;
+                wait_full(zb, nz_ >> 1);
+                const T* as = h ? E0c : E2c;
+#pragma unroll
+                for (int q = 0; q < 18; ++q) a[q] = as[q * N + sl];
+                const T* bs = h ? E3 + ix_up : Z + sl;
+                const T* cs = (h ? E(0, n) : E(2, n)) + sl;
+                plane_fma<T, false>(a, bs, N, cs, N, s, acc);
+                release(zb);
+                ++nz_;
+            }
+            release(0 + (c & 1));
+            release(4 + (c & 1));
+            release(B_E3);
+            ++n3;
+            ++ne;
+            // ---- the two half-sums meet: lanes 0-15 store elements 0..8, lanes 16-31 elements 9..17
+            T* o = acc_out + int64_t(t) * 18 * p.F + s3;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const T mine = h ? acc[9 + k] : acc[k];
+                const T give = h ? acc[k] : acc[9 + k];
+                const T got = __shfl_xor_sync(0xffffffffu, give, 16);
+                __stcs(o + (9 * h + k) * p.F, mine + got);
+            }
+        }
+        // slice t1 (only the last step's t-planes read it)
+        for (int k = 0; k < 3; ++k) release(2 * k + (ne & 1));
+        ++ne;
+    }
+}
+
+template <typename T, int NX, int BY>
+static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
+    using G = PairGeo<T, NX, BY>;
+    CUtensorMap mB, mY;
+    if (!make_map<T>(&mB, U, nx, ny, nz, int64_t(nt) * 72, BY, 1, 18) ||
+        !make_map<T>(&mY, U, nx, ny, nz, int64_t(nt) * 72, 1, 1, 18))
+        return 1;
+    const size_t smem = size_t(G::TOTAL) * sizeof(T) + 2 * G::NBAR * sizeof(uint64_t);
+    const DeviceInfo& di = device_info();
+    if (smem > size_t(di.max_smem_optin)) return 1;
+    auto kern = k_link_pair<T, NX, BY>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    WalkParams p{};
+    p.ny = ny; p.nz = nz; p.nt = nt;
+    p.F = int64_t(nx) * ny * nz;
+    p.nby = ny / BY;
+    p.nblocks = int64_t(ny / BY) * nz;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, smem);
+    const int Gfull = di.num_sms * std::max(per_sm, 1);
+    p.chunk = pick_chunk(p.nblocks, nt, Gfull, 0.5);  // an item of L slices loads L+1 E slices
+    p.nitems = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
+    const int grid = static_cast<int>(std::min<int64_t>(Gfull, p.nitems));
+    kern<<<grid, G::THREADS, smem, st>>>(mB, mY, acc, p, s);
+    note_kernel(std::string("k_link_pair<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
+                std::to_string(BY) + "x1" + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
+                ",chunk " + std::to_string(p.chunk) + ">");
+    return check_launch("link_product(pair)");
+}
+
+// FMA mode only; 1 = not applicable to this lattice
+template <typename T>
+int launch_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
+    if (!aligned16(U)) return 1;
+    if (nx == 48 && ny % 3 == 0) return run_link_pair<T, 48, 3>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 32 && ny % 4 == 0) return run_link_pair<T, 32, 4>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 64 && ny % 2 == 0) return run_link_pair<T, 64, 2>(U, acc, nx, ny, nz, nt, s, st);
+    return 1;
+}
+
+template int launch_link_pair<float>(const float*, float*, int, int, int, int, float, cudaStream_t);
+template int launch_link_pair<double>(const double*, double*, int, int, int, int, double, cudaStream_t);
+
 // 1 = not applicable to this lattice (caller falls back)
 template <typename T, bool FUSED>
 int launch_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {

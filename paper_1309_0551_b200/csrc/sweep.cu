@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256)
 }
 
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
-static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk, 3 row-split carried t-walk
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk, 3 row-split carried t-walk, 4 two-lane pair walk (FMA)
 
 // largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
 static int chunk_planes(int nz, int cap) {
@@ -307,6 +307,12 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
         if (rc != 1) return rc;
         if (lv == 3) return fail_invalid("link_product: row-split walk kernel not applicable to this lattice");
     }
+    if (lv == 4) {
+        if (mode != SU3G_FMA) return fail_invalid("link_product: the pair kernel (link_variant 4) is FMA mode only");
+        const int rc = launch_link_pair<T>(U, acc, nx, ny, nz, nt, s, st);
+        if (rc != 1) return rc;
+        return fail_invalid("link_product: pair kernel not applicable to this lattice");
+    }
     const bool auto_ring = lv == 0 && mode == SU3G_FMA;
     if (auto_ring || lv == 2) {
         const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
@@ -339,9 +345,9 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 3)
-            return fail_invalid(
-                "set_option: link_variant must be 0 (auto), 1 (rows gather), 2 (tma ring walk) or 3 (row-split walk)");
+        if (value < 0 || value > 4)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 2 (tma ring walk), "
+                                "3 (row-split walk) or 4 (two-lane pair walk, FMA)");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -82,6 +82,9 @@ int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cu
 // row-split t-walk with carried t-planes (link_walk.cu); 1 = not applicable
 template <typename T, bool FUSED>
 int launch_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
+// two lanes per site, three planes each, FMA mode only (link_walk.cu); 1 = not applicable
+template <typename T>
+int launch_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);
 

@@ -8,9 +8,12 @@ scalar kernel on an instrumented number; here they are a table, pinned by
 oracle and against the reference's hand table (``pkg/tests/test_flops.py:8-24``).
 
 Arithmetic intensity = flops per site / algorithmic HBM bytes per site (read each
-input object once, write each output object once).  Every entry
-is far below the B200 ridge (~11 flop/B f32, ~5.7 flop/B f64), so every kernel
-on this path is HBM-bound.
+input object once, write each output object once).  In the exact
+(reference) association every flop is its own FMUL/FADD (DMUL/DADD) instruction, so
+the ridge is the scalar pipe rate over HBM: 148 SMs x 128 (f32) / 64 (f64) ops/clk x
+1.965 GHz over 6.45 TB/s = 5.8 (f32) / 2.9 (f64) flop/B.  The routines, the NN sweep
+and the dslash sit far below it (HBM-bound); the link product (7.2 / 3.6 flop/B) sits
+above it: in exact mode it is FP-pipe-bound, at most ~0.78 of HBM (``compute_floor``).
 """
 from __future__ import annotations
 
@@ -85,6 +88,14 @@ def routine_reals(routine: str) -> int:
     """Algorithmic reals moved per site: every array operand read once + the result written once."""
     spec = routine_spec(routine)
     return sum(REALS[k] for k in spec.operands if k != "scalar") + REALS[spec.result]
+
+
+def compute_floor_s(name: str, dtype: str, sites: int, sms: int = 148, clock_hz: float = 1.965e9) -> float:
+    """Seconds the FP pipe needs for `sites` sites in exact mode (one instruction per flop):
+    FP32 128 and FP64 64 lanes per SM per clock (B200)."""
+    lanes = 128 if dtype == "f32" else 64
+    fc = sweep_flop_count(name) if name in _SWEEP_FLOPS else flop_count(name)
+    return fc.total * sites / (sms * lanes * clock_hz)
 
 
 def intensity(name: str, dtype: str) -> dict:

@@ -225,6 +225,25 @@ def test_link_product_guarded(dt, dims, variant):
     assert np.array_equal(_from_soa(ga.host(), dims, (3, 3, 2)), want), _lib.last_kernel()
 
 
+@pytest.mark.parametrize("dims", [(48, 6, 5, 7), (32, 8, 4, 6), (48, 3, 2, 3)])
+def test_link_pair_fma_guarded(dt, dims):
+    """the FMA-only pair kernel: guards intact, result within tolerance (a NaN read would not be)"""
+    from oracle.compare import floored_rel_err
+
+    V = int(np.prod(dims))
+    U = inputs.random_links(inputs.config_rng(850 + V), V, 4, dtype=dt)
+    want = coracle.link_product(U, dims, 1 / 6)
+    gU, ga = Guarded(dt, U.size, _to_soa(U, dims)), Guarded(dt, V * 18)
+    _lib.set_option("link_variant", 4)
+    try:
+        _lib.call(f"su3g_link_product_{SFX[dt]}", gU.ptr, ga.ptr, *dims, float(dt(1 / 6)), 1, _stream())
+        torch.cuda.synchronize()
+    finally:
+        _lib.set_option("link_variant", 0)
+    assert ga.intact() and gU.intact(), _lib.last_kernel()
+    assert floored_rel_err(_from_soa(ga.host(), dims, (3, 3, 2)), want) <= (1e-5 if dt == np.float32 else 1e-12)
+
+
 @pytest.mark.parametrize("dims", [(64, 4, 4, 6), (8, 4, 4, 4), (16, 2, 6, 4)])
 def test_dslash_guarded(dt, dims):
     U, v, gU, gv = _fields(dims, dt, 900)

@@ -341,6 +341,30 @@ def test_link_product_bitwise(dims, precision, variant):
         _lib.set_option("link_variant", 0)
 
 
+@pytest.mark.parametrize(
+    "dims", [(48, 3, 2, 3), (48, 6, 5, 7), (32, 8, 4, 6), (64, 4, 3, 5), (32, 4, 1, 2), (48, 48, 3, 4)]
+)
+def test_link_pair_fma_within_tolerance(dims, precision):
+    """link_variant 4 (two lanes per site, three planes each; FMA mode only): within the north-star
+    tolerance of the composed reference, on lattices covering every block geometry and the periodic
+    wrap of the t-chunks; exact mode is refused."""
+    from paper_1309_0551_b200 import _lib
+
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    U = inputs.random_links(inputs.config_rng(4500 + V), V, 4, dtype=dt)
+    want = coracle.link_product(U, dims, 1 / 6)
+    _lib.set_option("link_variant", 4)
+    try:
+        got = sweeps.link_product_aos(U, dims, 1 / 6, mode="fma")
+        assert _lib.last_kernel().startswith("k_link_pair<"), _lib.last_kernel()
+        assert floored_rel_err(got, want) <= (1e-5 if dt == np.float32 else 1e-12)
+        with pytest.raises(ValueError, match="FMA mode only"):
+            sweeps.link_product_aos(U, dims, 1 / 6)
+    finally:
+        _lib.set_option("link_variant", 0)
+
+
 @pytest.mark.parametrize("variant", [1, 3, 4], ids=["generic", "tma", "ring"])
 @pytest.mark.parametrize("dims", [(64, 4, 4, 6), (32, 8, 4, 5), (8, 8, 8, 8)])
 def test_nn_fma_mode_within_tolerance(variant, dims, precision):
