@@ -6,7 +6,7 @@
 // Why this shape.  Per site the sweep reads 15 link matrices for 4 compulsory ones, so the links
 // must come from shared memory, and at f64 a site's links are 576 B: only ~150 sites of one slice
 // fit an SM next to their halos.  One thread per site then holds A, T, C and the accumulator
-// (255 registers, 7 warps/SM, k_link_ring) and cannot cover the FP64 and shared-memory latencies.
+// (255 registers, 7 warps/SM, the r02 ring walk since removed) and cannot cover the FP64 and shared-memory latencies.
 // Here:
 //   * three lanes per site, lane r owns row r of every product: row r of T = A B needs row r of A,
 //     row r of P = T C^dag needs row r of T, so the rows are independent and each lane performs
@@ -40,6 +40,8 @@
 
 namespace su3g {
 
+int g_pair_prefetch = -1;  // su3g_set_option("link_pair_prefetch"): L2 prefetch one step ahead in k_link_pair (-1 auto)
+
 namespace {
 
 struct WalkParams {
@@ -67,6 +69,13 @@ struct WalkGeo {
     // barriers: full/empty for E[k][b] (6), E3, Y, Z0, Z1
     static constexpr int NBAR = 10;
 };
+
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+                 : "memory");
+}
 
 __device__ __forceinline__ void walk_item(const WalkParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
     const int64_t ch = item / p.nblocks;
@@ -345,17 +354,18 @@ static int run_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
 // FMA mode: two lanes per site, three planes each (k_link_pair).
 //
 // With FMA chains the plane order is free (the north-star tolerance, not bit equality), so a site's
-// six planes split over two adjacent lanes that each own whole products: lane 0 takes (0,2) (1,2)
-// (2,3), lane 1 takes (0,1) (1,3) (0,3), one plane per lane per phase, and the two partial
-// accumulators meet through one shuffle at the end.  Unlike the row split, each lane reads a
-// distinct operand, so shared memory delivers every staged link once per use (a third of the
-// walk's wavefronts).  The t-planes read C = U_mu(x+t) from the NEXT slice's E0..E2, which the
-// double-buffered slots hold during the step (no carry): the producer loads slice t+1 while step t
-// starts.  Phase p of the step (lane 0 | lane 1):
-//   p0  (0,2): A U_0, B U_2(x+0), C U_0(x+2) [Z chunk 0]   | (0,1): A U_0, B U_1(x+0), C U_0(x+1)
-//   p1  (1,2): A U_1, B U_2(x+1), C U_1(x+2) [Z chunk 1]   | (1,3): A U_1, B U_3(x+1), C U_1(x+t)
-//   p2  (2,3): A U_2, B U_3(x+2) [Z chunk 2], C U_2(x+t)   | (0,3): A U_0, B U_3(x+0), C U_0(x+t)
-// so one Z chunk is live per phase and a ring of two Z slots suffices.
+// six planes split over two lanes that each own whole products, one plane per lane per phase, and
+// the two partial accumulators meet through one shuffle at the end.  Unlike the row split, each
+// lane reads a distinct operand, so shared memory delivers every staged link once per use, and a
+// warp covers 16 sites twice (lanes 0-15 | 16-31): each half-warp's 64-bit load is one slot, 128 B.
+// The t-planes read C = U_mu(x+t) from the NEXT slice's U_0..U_2, double-buffered per link, so the
+// block walk needs no carried state.  Phase p of a step (lanes 0-15 | lanes 16-31):
+//   p0  (0,2): A U_0, B U_2(x+0), C U_0(x+2) [Z0]       | (0,1): A U_0, B U_1(x+0), C U_0(x+1) [Y0]
+//   p1  (1,2): A U_1, B U_2(x+1) [Y2], C U_1(x+2) [Z1]  | (2,3): A U_2, B U_3(x+2) [Z3], C U_2(x+t)
+//   p2  (0,3): A U_0, B U_3(x+0), C U_0(x+t)            | (1,3): A U_1, B U_3(x+1) [Y3], C U_1(x+t)
+// Every halo chunk has its own slot and barrier, and the producer issues the loads in the order the
+// previous step frees their slots, so each load is in flight for at least two thirds of a step
+// before its phase: phase 0 frees Z0 / Y0, phase 1 Z1 / Z3 / Y2 / U_2, the end E3 / Y3 / U_0 / U_1.
 // ======================================================================================
 
 template <typename T, int NX, int BY>
@@ -365,13 +375,14 @@ struct PairGeo {
     static constexpr int NWC = N / 16;
     static constexpr int THREADS = 32 * NWC + 32;
     static constexpr int BLK = 18 * N;
-    static constexpr int YSZ = 54 * NX;
+    static constexpr int YSUB = 18 * NX;            // one link on the +y row
     static constexpr int OFF_E = 0;                 // E[k][b] (link k of the block, buffer b) at (2k + b) * BLK
     static constexpr int OFF_E3 = 6 * BLK;
-    static constexpr int OFF_Y = 7 * BLK;
-    static constexpr int OFF_Z = 7 * BLK + YSZ;     // Z[j] at OFF_Z + j * BLK
-    static constexpr int TOTAL = 9 * BLK + YSZ;
-    static constexpr int NBAR = 10;                 // E[k][b] (6), E3, Y, Z0, Z1
+    static constexpr int OFF_Z = 7 * BLK;           // Z0, Z1, Z3 (U_0, U_1, U_3 on the +z plane)
+    static constexpr int OFF_Y = 10 * BLK;          // Y0, Y2, Y3 (U_0, U_2, U_3 on the +y row), YSUB each
+    static constexpr int TOTAL = 10 * BLK + 3 * YSUB;
+    // barriers: E[k][b] 0..5, E3 6, Z 7..9, Y 10..12
+    static constexpr int NBAR = 13;
 };
 
 namespace {
@@ -416,7 +427,7 @@ __device__ __forceinline__ void plane_fma(const T* a, const T* bs, int bstr, con
 
 }  // namespace
 
-template <typename T, int NX, int BY>
+template <typename T, int NX, int BY, bool PF>
 __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
     k_link_pair(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapY,
                 T* __restrict__ acc_out, WalkParams p, T s) {
@@ -426,7 +437,7 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
     T* sm = reinterpret_cast<T*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::TOTAL);
     uint64_t* empty = full + G::NBAR;
-    constexpr int B_E3 = 6, B_Y = 7, B_Z = 8;
+    constexpr int B_E3 = 6, B_Z = 7, B_Y = 10;  // Z: +0 U_0, +1 U_1, +2 U_3; Y: +0 U_0, +1 U_2, +2 U_3
     const int tid = threadIdx.x;
     if (tid == 0) {
         for (int k = 0; k < G::NBAR; ++k) {
@@ -442,20 +453,16 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
         if (tid != 32 * NWC) return;
         uint64_t pol;
         asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-        uint32_t ne = 0, n3 = 0, ny_ = 0, nz_ = 0;  // ne: slices loaded (buffer ne & 1)
-        auto load_blk = [&](int bar, uint32_t use, T* dst, int y0, int z0, int plane) {
+        uint32_t ne = 0, ns = 0;  // slices loaded (buffer ne & 1); steps issued (E3 / Z / Y uses)
+        auto load = [&](int bar, uint32_t use, T* dst, const CUtensorMap* map, int y, int z, int plane, int reals) {
             if (use) mbar_wait(&empty[bar], (use - 1) & 1);
-            mbar_arrive_expect_tx(&full[bar], G::BLK * sizeof(T));
-            tma_load_4d(dst, &mapB, 0, y0, z0, plane, &full[bar], pol);
+            mbar_arrive_expect_tx(&full[bar], reals * sizeof(T));
+            tma_load_4d(dst, map, 0, y, z, plane, &full[bar], pol);
         };
-        auto load_link = [&](int k, uint32_t slice_no, int ts, int y0, int z0) {  // link k of slice load slice_no
+        auto load_link = [&](int k, uint32_t slice_no, int ts, int y0, int z0) {
             const int b = slice_no & 1;
-            load_blk(2 * k + b, slice_no >> 1, sm + G::OFF_E + (2 * k + b) * G::BLK, y0, z0, ts * 72 + 18 * k);
-        };
-        auto load_z = [&](int y0, int zup, int plane) {
-            const int j = nz_ & 1;
-            load_blk(B_Z + j, nz_ >> 1, sm + G::OFF_Z + j * G::BLK, y0, zup, plane);
-            ++nz_;
+            load(2 * k + b, slice_no >> 1, sm + G::OFF_E + (2 * k + b) * G::BLK, &mapB, y0, z0, ts * 72 + 18 * k,
+                 G::BLK);
         };
         for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
             int64_t blk;
@@ -465,48 +472,57 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
             const int yup = (y0 + BY) % p.ny, zup = (z0 + 1) % p.nz;
             for (int k = 0; k < 3; ++k) load_link(k, ne, t0, y0, z0);
             ++ne;
-            for (int t = t0; t < t1; ++t) {
+            for (int t = t0; t < t1; ++t, ++ns) {
                 const int tn = (t + 1 == p.nt) ? 0 : t + 1;
-                // issue order = the order the previous step releases the slots (monotone waits):
-                // Y, Z0 and U_1 of slice t-1 free after phase 1, E3 / Z1 / U_0 / U_2 at its end, Z3
-                // after this step's phase 0
-                if (ny_) mbar_wait(&empty[B_Y], (ny_ - 1) & 1);
-                mbar_arrive_expect_tx(&full[B_Y], G::YSZ * sizeof(T));
-                T* yd = sm + G::OFF_Y;
-                tma_load_4d(yd, &mapY, 0, yup, z0, t * 72, &full[B_Y], pol);
-                tma_load_4d(yd + 18 * NX, &mapY, 0, yup, z0, t * 72 + 36, &full[B_Y], pol);
-                tma_load_4d(yd + 36 * NX, &mapY, 0, yup, z0, t * 72 + 54, &full[B_Y], pol);
-                ++ny_;
-                load_z(y0, zup, t * 72);                // U_0 on +z: phase 0
-                load_link(1, ne, tn, y0, z0);           // U_1(x+t): phase 1
-                load_blk(B_E3, n3, sm + G::OFF_E3, y0, z0, t * 72 + 54);
-                ++n3;
-                load_z(y0, zup, t * 72 + 18);           // U_1 on +z: phase 1
-                load_link(0, ne, tn, y0, z0);           // U_0(x+t), U_2(x+t): phase 2
+                if constexpr (PF) {  // L2 warm-up one step ahead: the next step's halos and U_3, slice t+2
+                    const int tn2 = (tn + 1 == p.nt) ? 0 : tn + 1;
+                    if (t + 1 < t1) {
+                        for (int k : {0, 36, 54}) tma_prefetch(&mapY, 0, yup, z0, tn * 72 + k);
+                        for (int k : {0, 18, 54}) tma_prefetch(&mapB, 0, y0, zup, tn * 72 + k);
+                        tma_prefetch(&mapB, 0, y0, z0, tn * 72 + 54);
+                        for (int k = 0; k < 3; ++k) tma_prefetch(&mapB, 0, y0, z0, tn2 * 72 + 18 * k);
+                    }
+                }
+                // issue order = the order the previous step releases the slots, so every wait is
+                // monotone: phase 0 frees Z0 / Y0, phase 1 Z1 / Z3 / Y2 / U_2, the end E3 / Y3 / U_0 / U_1
+                load(B_Z + 0, ns, sm + G::OFF_Z, &mapB, y0, zup, t * 72, G::BLK);
+                load(B_Y + 0, ns, sm + G::OFF_Y, &mapY, yup, z0, t * 72, G::YSUB);
+                load(B_Z + 1, ns, sm + G::OFF_Z + G::BLK, &mapB, y0, zup, t * 72 + 18, G::BLK);
+                load(B_Z + 2, ns, sm + G::OFF_Z + 2 * G::BLK, &mapB, y0, zup, t * 72 + 54, G::BLK);
+                load(B_Y + 1, ns, sm + G::OFF_Y + G::YSUB, &mapY, yup, z0, t * 72 + 36, G::YSUB);
                 load_link(2, ne, tn, y0, z0);
+                load(B_E3, ns, sm + G::OFF_E3, &mapB, y0, z0, t * 72 + 54, G::BLK);
+                load(B_Y + 2, ns, sm + G::OFF_Y + 2 * G::YSUB, &mapY, yup, z0, t * 72 + 54, G::YSUB);
+                load_link(0, ne, tn, y0, z0);
+                load_link(1, ne, tn, y0, z0);
                 ++ne;
-                load_z(y0, zup, t * 72 + 54);           // U_3 on +z: phase 2
             }
         }
         return;
     }
 
     // ------------------------------------------------------------------ compute warps
-    // a warp covers 16 consecutive sites twice: lanes 0-15 take planes (0,2) (1,2) (2,3), lanes 16-31
-    // (0,1) (1,3) (0,3), so every 64-bit shared load of a half-warp reads one slot, 16 sites, 128 B
+    // a warp covers 16 consecutive sites twice: lanes 0-15 take planes (0,2) (1,2) (0,3), lanes 16-31
+    // (0,1) (2,3) (1,3), so every 64-bit shared load of a half-warp reads one slot, 16 sites, 128 B
     const int lane = tid & 31;
     const int sl = (tid >> 5) * 16 + (lane & 15);
     const int h = lane >> 4;
     const int lx = sl % NX, ly = sl / NX;
     const int ix_up = (lx + 1 == NX) ? sl - lx : sl + 1;
     const bool y_in = ly + 1 < BY;
-    const T* const Y = sm + G::OFF_Y;
+    const int ystr = y_in ? N : NX;
     const T* const E3 = sm + G::OFF_E3;
+    const T* const Z0 = sm + G::OFF_Z;
+    const T* const Z1 = Z0 + G::BLK;
+    const T* const Z3 = Z1 + G::BLK;
+    const T* const Y0 = sm + G::OFF_Y;
+    const T* const Y2 = Y0 + G::YSUB;
+    const T* const Y3 = Y2 + G::YSUB;
     auto release = [&](int bar) { warp_release(&empty[bar], lane); };
     auto wait_full = [&](int bar, uint32_t use) { mbar_wait(&full[bar], use & 1); };
     auto E = [&](int k, uint32_t slice_no) { return sm + G::OFF_E + (2 * k + (slice_no & 1)) * G::BLK; };
 
-    uint32_t ne = 0, n3 = 0, ny_ = 0, nz_ = 0;
+    uint32_t ne = 0, ns = 0;
     for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
         int64_t blk;
         int t0, t1;
@@ -514,65 +530,54 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
         const int y = static_cast<int>(blk % p.nby) * BY + ly;
         const int z = static_cast<int>(blk / p.nby);
         const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
-        for (int t = t0; t < t1; ++t) {
+        for (int t = t0; t < t1; ++t, ++ns) {
             const uint32_t c = ne, n = ne + 1;  // slice loads of t and t+1
             const T *E0c = E(0, c), *E1c = E(1, c), *E2c = E(2, c);
             for (int k = 0; k < 3; ++k) wait_full(2 * k + (c & 1), c >> 1);
             T acc[18], a[18];
-            // ---- phase 0: (0,2) C = U_0(x+2) on Z chunk 0 | (0,1) C = U_0(x+1)
-            {
-                const int zb = B_Z + (nz_ & 1);
-                const T* Z = sm + G::OFF_Z + (nz_ & 1) * G::BLK;
-                wait_full(zb, nz_ >> 1);
-                wait_full(B_Y, ny_);
+            // ---- phase 0: (0,2) B = U_2(x+0), C = U_0(x+2) [Z0] | (0,1) B = U_1(x+0), C = U_0(x+1)
+            wait_full(B_Z + 0, ns);
+            wait_full(B_Y + 0, ns);
 #pragma unroll
-                for (int q = 0; q < 18; ++q) a[q] = E0c[q * N + sl];  // U_0(x)
-                const T* bs = (h ? E1c : E2c) + ix_up;                  // U_1(x+0) | U_2(x+0)
-                const T* cs = h ? (y_in ? E0c + sl + NX : Y + lx) : Z + sl;
-                const int cstr = (h && !y_in) ? NX : N;
-                plane_fma<T, true>(a, bs, N, cs, cstr, s, acc);
-                release(zb);
-                ++nz_;
-            }
-            // ---- phase 1: (1,2) B = U_2(x+1), C = U_1(x+2) on Z chunk 1 | (1,3) B = U_3(x+1), C = U_1(x+t)
-            wait_full(B_E3, n3);
-            wait_full(2 + (n & 1), n >> 1);
-            {
-                const int zb = B_Z + (nz_ & 1);
-                const T* Z = sm + G::OFF_Z + (nz_ & 1) * G::BLK;
-                wait_full(zb, nz_ >> 1);
-#pragma unroll
-                for (int q = 0; q < 18; ++q) a[q] = E1c[q * N + sl];  // U_1(x)
-                const T* bs = y_in ? (h ? E3 : E2c) + sl + NX : Y + (h ? 36 : 18) * NX + lx;
-                const int bstr = y_in ? N : NX;
-                const T* cs = h ? E(1, n) + sl : Z + sl;
-                plane_fma<T, false>(a, bs, bstr, cs, N, s, acc);
-                release(zb);
-                ++nz_;
-            }
-            release(B_Y);
-            ++ny_;
-            release(2 + (c & 1));  // U_1 of slice t: its buffer takes U_1 of slice t+2
-            // ---- phase 2: (2,3) A = U_2, B = U_3(x+2) on Z chunk 2, C = U_2(x+t) | (0,3) A = U_0, B = U_3(x+0), C = U_0(x+t)
-            wait_full(0 + (n & 1), n >> 1);
+            for (int q = 0; q < 18; ++q) a[q] = E0c[q * N + sl];  // U_0(x)
+            plane_fma<T, true>(a, (h ? E1c : E2c) + ix_up, N, h ? (y_in ? E0c + sl + NX : Y0 + lx) : Z0 + sl,
+                               h ? ystr : N, s, acc);
+            release(B_Z + 0);
+            release(B_Y + 0);
+            // ---- phase 1: (1,2) A = U_1, B = U_2(x+1), C = U_1(x+2) [Z1] | (2,3) A = U_2, B = U_3(x+2) [Z3], C = U_2(x+t)
+            wait_full(B_Z + 1, ns);
+            wait_full(B_Z + 2, ns);
+            wait_full(B_Y + 1, ns);
             wait_full(4 + (n & 1), n >> 1);
             {
-                const int zb = B_Z + (nz_ & 1);
-                const T* Z = sm + G::OFF_Z + (nz_ & 1) * G::BLK;
-                wait_full(zb, nz_ >> 1);
-                const T* as = h ? E0c : E2c;
+                const T* as = h ? E2c : E1c;
 #pragma unroll
                 for (int q = 0; q < 18; ++q) a[q] = as[q * N + sl];
-                const T* bs = h ? E3 + ix_up : Z + sl;
-                const T* cs = (h ? E(0, n) : E(2, n)) + sl;
-                plane_fma<T, false>(a, bs, N, cs, N, s, acc);
-                release(zb);
-                ++nz_;
+                const T* bs = h ? Z3 + sl : (y_in ? E2c + sl + NX : Y2 + lx);
+                const T* cs = h ? E(2, n) + sl : Z1 + sl;
+                plane_fma<T, false>(a, bs, h ? N : ystr, cs, N, s, acc);
             }
-            release(0 + (c & 1));
-            release(4 + (c & 1));
+            release(B_Z + 1);
+            release(B_Z + 2);
+            release(B_Y + 1);
+            release(4 + (c & 1));  // U_2 of slice t: its buffer takes U_2 of slice t+2
+            // ---- phase 2: (0,3) A = U_0, B = U_3(x+0), C = U_0(x+t) | (1,3) A = U_1, B = U_3(x+1), C = U_1(x+t)
+            wait_full(B_E3, ns);
+            wait_full(B_Y + 2, ns);
+            wait_full(0 + (n & 1), n >> 1);
+            wait_full(2 + (n & 1), n >> 1);
+            {
+                const T* as = h ? E1c : E0c;
+#pragma unroll
+                for (int q = 0; q < 18; ++q) a[q] = as[q * N + sl];
+                const T* bs = h ? (y_in ? E3 + sl + NX : Y3 + lx) : E3 + ix_up;
+                const T* cs = (h ? E(1, n) : E(0, n)) + sl;
+                plane_fma<T, false>(a, bs, h ? ystr : N, cs, N, s, acc);
+            }
             release(B_E3);
-            ++n3;
+            release(B_Y + 2);
+            release(0 + (c & 1));
+            release(2 + (c & 1));
             ++ne;
             // ---- the two half-sums meet: lanes 0-15 store elements 0..8, lanes 16-31 elements 9..17
             T* o = acc_out + int64_t(t) * 18 * p.F + s3;
@@ -600,7 +605,8 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     const size_t smem = size_t(G::TOTAL) * sizeof(T) + 2 * G::NBAR * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    auto kern = k_link_pair<T, NX, BY>;
+    const bool pf = g_pair_prefetch < 0 ? sizeof(T) == 4 : g_pair_prefetch != 0;  // auto: f32 only (A/B)
+    auto kern = pf ? k_link_pair<T, NX, BY, true> : k_link_pair<T, NX, BY, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     WalkParams p{};
     p.ny = ny; p.nz = nz; p.nt = nt;
@@ -615,7 +621,7 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     const int grid = static_cast<int>(std::min<int64_t>(Gfull, p.nitems));
     kern<<<grid, G::THREADS, smem, st>>>(mB, mY, acc, p, s);
     note_kernel(std::string("k_link_pair<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
-                std::to_string(BY) + "x1" + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
+                std::to_string(BY) + "x1" + (pf ? ",L2 prefetch" : "") + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
                 ",chunk " + std::to_string(p.chunk) + ">");
     return check_launch("link_product(pair)");
 }

@@ -147,8 +147,9 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+extern int g_pair_prefetch;
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
-static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 2 TMA ring walk, 3 row-split carried t-walk, 4 two-lane pair walk (FMA)
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 3 row-split carried t-walk, 4 two-lane pair walk (FMA)
 
 // largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
 static int chunk_planes(int nz, int cap) {
@@ -297,28 +298,21 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("link_product: mode must be SU3G_EXACT or SU3G_FMA");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int lv = g_link_variant.load();
-    // auto (48^4 on B200, fraction of HBM, profiles/r02/ab_link_walk.md): f32 exact -> the row-split
-    // carried t-walk (0.351 vs rows 0.309); f64 FMA -> the ring walk (0.546 vs rows 0.525, walk 0.493);
-    // f64 exact (rows 0.465, walk 0.461) and f32 FMA (ring 0.397, walk 0.394, rows 0.357) -> below
-    const bool auto_walk = lv == 0 && sizeof(T) == 4 && mode == SU3G_EXACT;
-    if (auto_walk || lv == 3) {
+    // auto (48^4 on B200, fraction of HBM; profiles/r02/ab_link_walk.md, ab_link_pair.txt): FMA mode -> the
+    // two-lane pair walk (f64 0.620, f32 0.435; the removed ring walk 0.546 / 0.397, rows 0.525 / 0.357);
+    // exact f32 -> the row-split carried walk (0.351 vs rows 0.309); exact f64 -> rows (0.465; walk 0.461,
+    // an exact pair walk 0.413)
+    if (lv == 4 || (lv == 0 && mode == SU3G_FMA)) {
+        if (mode != SU3G_FMA) return fail_invalid("link_product: the pair walk (link_variant 4) is FMA mode only");
+        const int rc = launch_link_pair<T>(U, acc, nx, ny, nz, nt, s, st);
+        if (rc != 1) return rc;
+        if (lv == 4) return fail_invalid("link_product: pair kernel not applicable to this lattice");
+    }
+    if (lv == 3 || (lv == 0 && sizeof(T) == 4 && mode == SU3G_EXACT)) {
         const int rc = mode == SU3G_FMA ? launch_link_walk<T, true>(U, acc, nx, ny, nz, nt, s, st)
                                         : launch_link_walk<T, false>(U, acc, nx, ny, nz, nt, s, st);
         if (rc != 1) return rc;
         if (lv == 3) return fail_invalid("link_product: row-split walk kernel not applicable to this lattice");
-    }
-    if (lv == 4) {
-        if (mode != SU3G_FMA) return fail_invalid("link_product: the pair kernel (link_variant 4) is FMA mode only");
-        const int rc = launch_link_pair<T>(U, acc, nx, ny, nz, nt, s, st);
-        if (rc != 1) return rc;
-        return fail_invalid("link_product: pair kernel not applicable to this lattice");
-    }
-    const bool auto_ring = lv == 0 && mode == SU3G_FMA;
-    if (auto_ring || lv == 2) {
-        const int rc = mode == SU3G_FMA ? launch_link_ring<T, true>(U, acc, nx, ny, nz, nt, s, st)
-                                        : launch_link_ring<T, false>(U, acc, nx, ny, nz, nt, s, st);
-        if (rc != 1) return rc;
-        if (lv == 2) return fail_invalid("link_product: TMA ring kernel not applicable to this lattice");
     }
     // z-planes per chunk: 16 measured best for the rows kernel at 48^4 f64 (exact 0.427 -> 0.455,
     // FMA 0.475 -> 0.506 against the unchunked order; 2, 4, 12 also swept).  Chunk once a t-slice of
@@ -345,10 +339,15 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 4)
-            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 2 (tma ring walk), "
-                                "3 (row-split walk) or 4 (two-lane pair walk, FMA)");
+        if (value < 0 || value > 4 || value == 2)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 3 (row-split walk) or "
+                                "4 (two-lane pair walk, FMA); 2 (the ring walk) was removed, measured slower");
         g_link_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "link_pair_prefetch") == 0) {
+        if (value < -1 || value > 1) return fail_invalid("set_option: link_pair_prefetch must be -1 (auto), 0 or 1");
+        g_pair_prefetch = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "nn_ring_cfg") == 0) {

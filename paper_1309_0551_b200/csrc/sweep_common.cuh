@@ -76,13 +76,10 @@ int launch_nn_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
 template <typename T>
 int launch_dslash_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int parity, int mode,
                       cudaStream_t st);
-// link product on the TMA ring t-walk (link_ring.cu); 1 = not applicable
-template <typename T, bool FUSED>
-int launch_link_ring(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 // row-split t-walk with carried t-planes (link_walk.cu); 1 = not applicable
 template <typename T, bool FUSED>
 int launch_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
-// two lanes per site, three planes each, FMA mode only (link_walk.cu); 1 = not applicable
+// two lanes per site, three planes each, FMA mode (link_walk.cu); 1 = not applicable
 template <typename T>
 int launch_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 template <typename T, bool FUSED>

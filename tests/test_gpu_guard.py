@@ -204,7 +204,7 @@ def test_slab_pieces_guarded(dt, dims):
 
 
 @pytest.mark.parametrize("dims", [(48, 4, 6, 7), (32, 8, 4, 6), (48, 2, 2, 3), (16, 8, 4, 6), (5, 3, 2, 7)])
-@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "rows", "ring", "walk"])
+@pytest.mark.parametrize("variant", [0, 1, 3], ids=["auto", "rows", "walk"])
 def test_link_product_guarded(dt, dims, variant):
     V = int(np.prod(dims))
     U = inputs.random_links(inputs.config_rng(800 + V), V, 4, dtype=dt)

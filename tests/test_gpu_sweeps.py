@@ -100,7 +100,7 @@ def test_link_product_config3_full_size(variant):
         del got
         assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
         if variant == 0:
-            assert _lib.last_kernel().startswith("k_link_ring<f64,48x2x2"), _lib.last_kernel()
+            assert _lib.last_kernel().startswith("k_link_pair<f64,48x3x1"), _lib.last_kernel()
     finally:
         _lib.set_option("link_variant", 0)
 
@@ -116,7 +116,7 @@ def test_link_product_config3_f32_full_size():
     assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
     assert _lib.last_kernel().startswith("k_link_walk<f32,48x3x1"), _lib.last_kernel()  # exact f32: the carried walk
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-5
-    assert _lib.last_kernel().startswith("k_link_ring<f32,48x2x2"), _lib.last_kernel()
+    assert _lib.last_kernel().startswith("k_link_pair<f32,48x3x1"), _lib.last_kernel()
 
 
 @pytest.mark.parametrize("C", [6, 18, 24, 72])
@@ -317,7 +317,7 @@ def test_tma_variant_required_fails_loudly_when_inapplicable():
      (48, 4, 6, 7), (48, 6, 2, 1), (48, 2, 4, 33), (8, 4, 4, 3), (16, 8, 12, 5), (24, 4, 8, 1),
      (32, 4, 4, 6), (64, 4, 2, 3), (48, 48, 8, 4)],
 )
-@pytest.mark.parametrize("variant", [0, 1, 2, 3], ids=["auto", "rows", "ring", "walk"])
+@pytest.mark.parametrize("variant", [0, 1, 3], ids=["auto", "rows", "walk"])
 def test_link_product_bitwise(dims, precision, variant):
     from paper_1309_0551_b200 import _lib
 
@@ -331,7 +331,7 @@ def test_link_product_bitwise(dims, precision, variant):
         try:
             got = sweeps.link_product_aos(U, dims, 1 / 6)
         except ValueError as e:
-            if variant in (2, 3) and "not applicable" in str(e):
+            if variant == 3 and "not applicable" in str(e):
                 pytest.skip(f"ring walk not applicable to {dims}")
             raise
         assert np.array_equal(got, want), _lib.last_kernel()
@@ -344,10 +344,10 @@ def test_link_product_bitwise(dims, precision, variant):
 @pytest.mark.parametrize(
     "dims", [(48, 3, 2, 3), (48, 6, 5, 7), (32, 8, 4, 6), (64, 4, 3, 5), (32, 4, 1, 2), (48, 48, 3, 4)]
 )
-def test_link_pair_fma_within_tolerance(dims, precision):
-    """link_variant 4 (two lanes per site, three planes each; FMA mode only): within the north-star
-    tolerance of the composed reference, on lattices covering every block geometry and the periodic
-    wrap of the t-chunks; exact mode is refused."""
+def test_link_pair_walk(dims, precision):
+    """link_variant 4 (two lanes per site, three planes each; the FMA-mode default): within the
+    north-star tolerance of the composed reference, on lattices covering every block geometry and the
+    periodic wrap of the t-chunks; exact mode is refused."""
     from paper_1309_0551_b200 import _lib
 
     dt = _dt(precision)

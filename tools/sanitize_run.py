@@ -4,7 +4,7 @@
 
 Covers the per-site stream kernels (all fifteen routines, both precisions), the layout transforms, the
 seeded fill, the NN sweep kernels (ring walk, f32 TMA walk, generic, t-slab edges / halo pack), the
-dslash (SoA parity kernels, checkerboarded fields), the link product (rows gather, ring walk), the
+dslash (SoA parity kernels, checkerboarded fields), the link product (rows gather, row-split walk, pair walk), the
 one-rank P2P boundary protocol and the one-rank NCCL slab driver.  Every result is compared with the
 CPU oracle, so a kernel that misbehaves under the tool is visible in the exit code too.
 """
@@ -84,10 +84,10 @@ def main():
                         _lib.set_option("nn_ring_cfg", 0)
                         _lib.set_option("nn_variant", 0)
             wl = coracle.link_product(U, dims, 1 / 6)
-            for lv in (1, 2):
+            for lv in (1, 3, 4):
                 _lib.set_option("link_variant", lv)
                 try:
-                    for mode in ("exact", "fma"):
+                    for mode in ("exact", "fma") if lv != 4 else ("fma",):
                         got = sweeps.link_product_aos(U, dims, 1 / 6, mode=mode)
                         check(mode == "fma" or np.array_equal(got, wl), f"link {dims} {dt} {lv}")
                 except ValueError:
