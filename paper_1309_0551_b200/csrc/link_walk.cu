@@ -70,13 +70,6 @@ struct WalkGeo {
     static constexpr int NBAR = 10;
 };
 
-__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
-    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-                 : "memory");
-}
-
 __device__ __forceinline__ void walk_item(const WalkParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
     const int64_t ch = item / p.nblocks;
     blk = item - ch * p.nblocks;

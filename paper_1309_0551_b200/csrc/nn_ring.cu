@@ -43,8 +43,9 @@ struct RingParams {
     int64_t nblocks;
     int t_begin, t_end;
     int chunk;       // t-chunk length of one work item
-    int64_t nitems;  // nblocks * ceil((t_end - t_begin) / chunk), chunk-major
+    int64_t nitems;  // nblocks * ceil((t_end - t_begin) / chunk), chunk-major; EDGES: nblocks * (boundary slices)
     int has_vhi;
+    void* w_next;    // EDGES: w = U_t^dag out on slice nt-1 (the next application's halo), or null
 };
 
 template <int NX>
@@ -70,16 +71,22 @@ struct RingX {
     static constexpr int WSTRIDE = 18 * N, HSTRIDE = 12 * H;  // per buffer
 };
 
+template <bool EDGES = false>
 __device__ __forceinline__ void item_of(const RingParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
     const int64_t ch = item / p.nblocks;
     blk = item - ch * p.nblocks;
-    t0 = p.t_begin + static_cast<int>(ch) * p.chunk;
-    t1 = min(t0 + p.chunk, p.t_end);
+    if constexpr (EDGES) {  // the boundary slices of a t-slab: t = 0 for every block, then t = nt - 1
+        t0 = ch == 0 ? 0 : p.nt - 1;
+        t1 = t0 + 1;
+    } else {
+        t0 = p.t_begin + static_cast<int>(ch) * p.chunk;
+        t1 = min(t0 + p.chunk, p.t_end);
+    }
 }
 
 }  // namespace
 
-template <typename T, bool FUSED, int NX, int S, bool DB, int MINB>
+template <typename T, bool FUSED, int NX, int S, bool DB, int MINB, bool EDGES>
 __global__ void __launch_bounds__(4 * NX + 32, MINB)
     k_nn_ring(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapV,
               const __grid_constant__ CUtensorMap mapVhi, const __grid_constant__ CUtensorMap mapUyH,
@@ -117,10 +124,23 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
         for (int64_t item = blockIdx.x; item < p.nitems; item += G_) {
             int64_t blk;
             int t0, t1;
-            item_of(p, item, blk, t0, t1);
+            item_of<EDGES>(p, item, blk, t0, t1);
             const int y0 = static_cast<int>(blk % p.nby) * 2, z0 = static_cast<int>(blk / p.nby) * 2;
             const int ydn = (y0 + p.ny - 1) % p.ny, yup = (y0 + 2) % p.ny;
             const int zdn = (z0 + p.nz - 1) % p.nz, zup = (z0 + 2) % p.nz;
+            if constexpr (EDGES) {  // one-step items: warm L2 with the NEXT item's prologue operands
+                if (item + G_ < p.nitems) {
+                    int64_t nb;
+                    int n0, n1;
+                    item_of<EDGES>(p, item + G_, nb, n0, n1);
+                    const int ny0 = static_cast<int>(nb % p.nby) * 2, nz0 = static_cast<int>(nb / p.nby) * 2;
+                    tma_prefetch(&mapV, 0, ny0, nz0, n0 * 6);  // v(t0)
+                    if (n0 > 0) {                              // w_t(t0-1) = U_t(t0-1)^dag v(t0-1)
+                        tma_prefetch(&mapV, 0, ny0, nz0, (n0 - 1) * 6);
+                        tma_prefetch(&mapU, 0, ny0, nz0, (n0 - 1) * 72 + 54);
+                    }
+                }
+            }
             for (int t = t0; t < t1; ++t) {
 #pragma unroll 1
                 for (int c = 0; c < 6; ++c, ++q) {
@@ -168,7 +188,7 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
     for (int64_t item = blockIdx.x; item < p.nitems; item += G_) {
         int64_t blk;
         int t0, t1;
-        item_of(p, item, blk, t0, t1);
+        item_of<EDGES>(p, item, blk, t0, t1);
         const int y = static_cast<int>(blk % p.nby) * 2 + ly;
         const int z = static_cast<int>(blk / p.nby) * 2 + lz;
         const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
@@ -254,6 +274,7 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
             }
             // ---- U_t: -t term of the next step, forward +t term (summed last)
             T wt_next[6];
+            T ut_keep[EDGES ? 18 : 1];
             {
                 const uint32_t qq = q + 5;
                 const int s = static_cast<int>(qq % S);
@@ -267,6 +288,10 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
                 mv<T, FUSED>(u, vnext, f);
 #pragma unroll
                 for (int c = 0; c < 6; ++c) acc[c] = xadd(acc[c], f[c]);
+                if constexpr (EDGES) {
+#pragma unroll
+                    for (int c = 0; c < 18; ++c) ut_keep[c] = u[c];
+                }
             }
             q += 6;
 #pragma unroll
@@ -290,6 +315,15 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
             T* o = out + int64_t(t) * 6 * F + s3;
 #pragma unroll
             for (int c = 0; c < 6; ++c) __stcs(o + c * F, acc[c]);
+            if constexpr (EDGES) {  // the next application's +t halo: U_t^dag out, nn_halo_w's arithmetic
+                if (p.w_next != nullptr && t == p.nt - 1) {
+                    T w[6];
+                    amv<T, FUSED>(ut_keep, acc, w);
+                    T* wn = static_cast<T*>(p.w_next) + s3;
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) wn[c * F] = w[c];
+                }
+            }
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
                 vc[c] = vnext[c];
@@ -302,9 +336,9 @@ __global__ void __launch_bounds__(4 * NX + 32, MINB)
     }
 }
 
-template <typename T, bool FUSED, int NX, int S, bool DB, int MINB>
+template <typename T, bool FUSED, int NX, int S, bool DB, int MINB, bool EDGES = false>
 static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
-                    const T* v_hi, const T* w_lo, cudaStream_t st) {
+                    const T* v_hi, const T* w_lo, cudaStream_t st, T* w_next = nullptr) {
     using G = RingGeo<NX>;
     using X = RingX<NX, DB>;
     CUtensorMap mU, mV, mVhi, mUy, mUz, mVy, mVz;
@@ -323,7 +357,7 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const size_t smem = (size_t(S) * G::SLOT + X::XSIZE) * sizeof(T) + 2 * S * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    auto kern = k_nn_ring<T, FUSED, NX, S, DB, MINB>;
+    auto kern = k_nn_ring<T, FUSED, NX, S, DB, MINB, EDGES>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     RingParams p{};
     p.ny = ny; p.nz = nz; p.nt = nt;
@@ -339,6 +373,8 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const int L = t_end - t_begin;
     p.chunk = pick_chunk(p.nblocks, L, G_full);
     p.nitems = p.nblocks * ((L + p.chunk - 1) / p.chunk);
+    p.w_next = w_next;
+    if constexpr (EDGES) p.nitems = p.nblocks * (nt > 1 ? 2 : 1);
     int Gr = G_full;
     if (sm_reserve() > 0) {  // as nn_tma.cu: leave SMs for NCCL only where the last round absorbs it
         const int64_t rounds = (p.nitems + G_full - 1) / G_full;
@@ -350,7 +386,7 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     kern<<<grid, G::N + 32, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     note_kernel(std::string("k_nn_ring<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x2x2," +
                 std::to_string(S) + " slots" + (DB ? ",1 barrier" : "") + (per > 1 ? "," + std::to_string(per) + " CTAs/SM" : "") +
-                ">" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
+                (EDGES ? ",edges" : "") + ">" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
     return check_launch("nn_sweep(ring)");
 }
 
@@ -393,6 +429,29 @@ int launch_nn_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int n
     return 1;
 }
 
+// Both boundary slices of a t-slab (t = 0 with w_lo, t = nt-1 with v_hi) as one-step work items of the
+// ring walk, and w_next = U_t^dag out on slice nt-1 (the next application's halo).  1 = not applicable.
+template <typename T>
+int launch_nn_ring_edges(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, const T* v_hi, const T* w_lo,
+                         T* w_next, int mode, cudaStream_t st) {
+    if (ny % 2 || nz % 2 || nt < 3) return 1;
+    if (!aligned16(U) || !aligned16(v) || (v_hi && !aligned16(v_hi))) return 1;
+    const bool fma = mode == SU3G_FMA;
+    constexpr int MB = sizeof(T) == 4 ? 2 : 1;
+#define SU3G_EDGES(NXV)                                                                                           \
+    return fma ? run_ring<T, true, NXV, 4, false, MB, true>(U, v, out, nx, ny, nz, nt, 0, nt, v_hi, w_lo, st, w_next) \
+               : run_ring<T, false, NXV, 4, false, MB, true>(U, v, out, nx, ny, nz, nt, 0, nt, v_hi, w_lo, st, w_next)
+    if (nx == 64) SU3G_EDGES(64);
+    if (nx == 32) SU3G_EDGES(32);
+    if (nx == 48) SU3G_EDGES(48);
+#undef SU3G_EDGES
+    return 1;
+}
+
+template int launch_nn_ring_edges<float>(const float*, const float*, float*, int, int, int, int, const float*,
+                                         const float*, float*, int, cudaStream_t);
+template int launch_nn_ring_edges<double>(const double*, const double*, double*, int, int, int, int, const double*,
+                                          const double*, double*, int, cudaStream_t);
 template int launch_nn_ring<float>(const float*, const float*, float*, int, int, int, int, int, int, const float*,
                                    const float*, int, cudaStream_t);
 template int launch_nn_ring<double>(const double*, const double*, double*, int, int, int, int, int, int,

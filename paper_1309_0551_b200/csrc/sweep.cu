@@ -231,6 +231,11 @@ static int nn_edges(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("nn_edges: mode must be SU3G_EXACT or SU3G_FMA");
     if (!U || !v || !out) return fail_invalid("nn_edges: null pointer");
     if (out == v) return fail_invalid("nn_edges: out must not alias v");
+    // the ring walk on one-step items (both boundary slices, same values bit for bit) where it applies
+    if (g_nn_variant.load() == 0 || g_nn_variant.load() == 4) {
+        const int rc = launch_nn_ring_edges<T>(U, v, out, nx, ny, nz, nt, v_hi, w_lo, w_next, mode, st);
+        if (rc != 1) return rc;
+    }
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int nedge = nt > 1 ? 2 : 1;
     const unsigned gs = static_cast<unsigned>((nedge * g.F + 255) / 256);
