@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+extern int g_eo_variant;
 int g_eo_zc = 0;      // su3g_set_option("dslash_eo_zc"): z-planes per visiting chunk (0 = auto)
 // su3g_set_option("dslash_eo_hints"): U loads evict-first, streaming stores.  Off by default: every U
 // sector is read once per launch anyway, and the plain form measured 1-1.5% faster (64^3x16: f64
@@ -186,6 +187,11 @@ static int dslash_eo(const T* U, const T* v, T* out, int nx, int ny, int nz, int
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("dslash_eo: mode must be SU3G_EXACT or SU3G_FMA");
     if (!U || !v || !out) return fail_invalid("dslash_eo: null pointer");
     if (out == v) return fail_invalid("dslash_eo: out must not alias v");
+    if (g_eo_variant != 1) {  // the ring walk on the half-lattice (dslash_ring.cu) where it applies
+        const int rc = launch_dslash_ring<T>(U, v, out, nx, ny, nz, nt, parity, mode, st);
+        if (rc != 1) return rc;
+        if (g_eo_variant == 2) return fail_invalid("dslash_eo: ring kernel not applicable to this lattice");
+    }
     EoGeom g{nx, ny, nz, nt, nx / 2, int64_t(nx) * ny * nz, int64_t(nx) * ny * nz / 2};
     // z-chunked order keeps the v planes a chunk re-reads in L2 (same rule as the generic sweep)
     int ZC = nz;

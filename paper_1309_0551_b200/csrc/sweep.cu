@@ -27,6 +27,8 @@ extern int g_tma_hints;
 extern int g_ring_cfg;
 extern int g_tma_chunk;
 extern int g_eo_zc;
+extern int g_eo_variant;
+extern int g_eo_ring_cfg;
 extern int g_eo_hints;
 
 // ---------------------------------------------------------------------------
@@ -348,6 +350,17 @@ int su3g_set_option(const char* name, int64_t value) {
             return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 3 (row-split walk) or "
                                 "4 (two-lane pair walk, FMA); 2 (the ring walk) was removed, measured slower");
         g_link_variant.store(static_cast<int>(value));
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "dslash_eo_variant") == 0) {
+        if (value < 0 || value > 2)
+            return fail_invalid("set_option: dslash_eo_variant must be 0 (auto), 1 (gather) or 2 (ring walk)");
+        g_eo_variant = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "dslash_eo_ring_cfg") == 0) {
+        if (value < 0 || value > 1) return fail_invalid("set_option: dslash_eo_ring_cfg must be 0 or 1");
+        g_eo_ring_cfg = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_pair_prefetch") == 0) {

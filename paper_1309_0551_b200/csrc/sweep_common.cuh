@@ -70,6 +70,10 @@ int launch_nn_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt
                   const T* v_hi, const T* w_lo, int mode, cudaStream_t st);
 
 // warp-specialised TMA ring t-walk (nn_ring.cu; the f64 path); 1 = not applicable
+// even/odd dslash on checkerboarded fields, ring walk on the half-lattice (dslash_ring.cu); 1 = not applicable
+template <typename T>
+int launch_dslash_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int parity, int mode,
+                       cudaStream_t st);
 template <typename T>
 int launch_nn_ring_edges(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, const T* v_hi, const T* w_lo,
                          T* w_next, int mode, cudaStream_t st);

@@ -244,7 +244,7 @@ def test_link_pair_fma_guarded(dt, dims):
     assert floored_rel_err(_from_soa(ga.host(), dims, (3, 3, 2)), want) <= (1e-5 if dt == np.float32 else 1e-12)
 
 
-@pytest.mark.parametrize("dims", [(64, 4, 4, 6), (8, 4, 4, 4), (16, 2, 6, 4)])
+@pytest.mark.parametrize("dims", [(64, 4, 4, 6), (8, 4, 4, 4), (16, 2, 6, 4), (32, 4, 2, 4)])
 def test_dslash_guarded(dt, dims):
     U, v, gU, gv = _fields(dims, dt, 900)
     full = coracle.nn_sweep(U, v, dims)

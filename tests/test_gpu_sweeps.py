@@ -591,6 +591,37 @@ def test_dslash_eo_vs_c_oracle(dims, hints, zc, precision):
         _lib.set_option("dslash_eo_zc", 0)
 
 
+@pytest.mark.parametrize("cfg", [0, 1])
+@pytest.mark.parametrize("dims", [(64, 4, 4, 6), (32, 8, 4, 6), (64, 2, 6, 2), (32, 4, 2, 8), (64, 64, 16, 4)])
+def test_dslash_eo_ring_vs_c_oracle(dims, cfg, precision):
+    """the half-lattice ring walk (dslash_eo_variant 2, both slot configurations) equals the full sweep on
+    its parity bit for bit, writes nothing on the other parity, and matches the gather kernel in FMA mode"""
+    from oracle import sweeps as OS
+    from paper_1309_0551_b200 import _lib
+
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(6300 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    full = coracle.nn_sweep(U, v, dims)
+    even = OS.parity_mask(dims)
+    _lib.set_option("dslash_eo_ring_cfg", cfg)
+    try:
+        for parity, keep in ((0, even), (1, ~even)):
+            _lib.set_option("dslash_eo_variant", 2)
+            got = sweeps.dslash_aos(U, v, dims, parity, layout="eo")
+            assert _lib.last_kernel().startswith("k_dslash_ring<"), _lib.last_kernel()
+            assert np.array_equal(got[keep], full[keep])
+            assert not np.any(got[~keep])
+            fm = sweeps.dslash_aos(U, v, dims, parity, mode="fma", layout="eo")
+            _lib.set_option("dslash_eo_variant", 1)
+            assert np.array_equal(fm, sweeps.dslash_aos(U, v, dims, parity, mode="fma", layout="eo"))
+    finally:
+        _lib.set_option("dslash_eo_variant", 0)
+        _lib.set_option("dslash_eo_ring_cfg", 0)
+
+
 def test_dslash_eo_composes_and_checks_layouts(precision):
     """D_eo D_oe on eo fields; out keeps its other parity; mixed layouts and eo inputs elsewhere raise."""
     from oracle import sweeps as OS
