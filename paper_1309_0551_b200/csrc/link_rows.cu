@@ -25,20 +25,27 @@ namespace {
 __constant__ int c_plane_mu[6] = {0, 0, 0, 1, 1, 2};
 __constant__ int c_plane_nu[6] = {1, 2, 3, 2, 3, 3};
 
-__device__ __forceinline__ int64_t shifted(const Geom& g, int x, int y, int z, int t, int mu) {
+// The links of the site one step along +mu: base pointer of its t-slice's 72 planes and its in-slice
+// offset (no 64-bit division: the r01 kernel derived (t, s3) from a flat site index with one per load)
+struct LinkSite {
+    const void* slice;  // U + t*72*F
+    int64_t s3;
+};
+
+template <typename T>
+__device__ __forceinline__ LinkSite link_site_at(const T* __restrict__ U, const Geom& g, int x, int y, int z, int t,
+                                                 int mu) {
     if (mu == 0) x = (x + 1 == g.nx) ? 0 : x + 1;
     else if (mu == 1) y = (y + 1 == g.ny) ? 0 : y + 1;
     else if (mu == 2) z = (z + 1 == g.nz) ? 0 : z + 1;
-    else t = (t + 1 == g.nt) ? 0 : t + 1;
-    return int64_t(t) * g.F + x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
+    else if (mu == 3) t = (t + 1 == g.nt) ? 0 : t + 1;  // mu == 4: the site itself
+    return {U + int64_t(t) * 72 * g.F, x + int64_t(g.nx) * (y + int64_t(g.ny) * z)};
 }
 
-// N consecutive components of link mu at a site: U[(t*72 + mu*18 + c0 + k) * F + s3]
+// N consecutive components of link mu at a site: slice[(mu*18 + c0 + k) * F + s3]
 template <typename T, int N>
-__device__ __forceinline__ void ld_link_part(const T* __restrict__ U, const Geom& g, int64_t site, int mu, int c0,
-                                             T* r) {
-    const int64_t t = site / g.F, s3 = site - t * g.F;
-    ld_soa<T, N>(U + (t * 72 + mu * 18 + c0) * g.F, g.F, s3, r);
+__device__ __forceinline__ void ld_link_part(const LinkSite& st, int64_t F, int mu, int c0, T* r) {
+    ld_soa<T, N>(static_cast<const T*>(st.slice) + (mu * 18 + c0) * F, F, st.s3, r);
 }
 
 template <typename T, bool FUSED, int MODE, class PF, class QF>
@@ -67,7 +74,7 @@ __global__ void __launch_bounds__(128, MINB)
     const int t = static_cast<int>(r % g.nt);
     const int z = static_cast<int>(r / g.nt) * ZC + zl;
     const int64_t s3 = x + int64_t(g.nx) * (y + int64_t(g.ny) * z);
-    const int64_t site = int64_t(t) * g.F + s3;
+    const LinkSite own = link_site_at(U, g, x, y, z, t, 4);
     T* acc = sacc + tid;  // element k at acc[k * 128]
 
 #pragma unroll 1
@@ -75,14 +82,14 @@ __global__ void __launch_bounds__(128, MINB)
         const int mu = c_plane_mu[pl], nu = c_plane_nu[pl];
         T tm[18], c[18];
         // EARLY_C: gather C with B (both in flight together, +18 live reals); else after T is built
-        if constexpr (EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);
+        if constexpr (EARLY_C) ld_link_part<T, 18>(link_site_at(U, g, x, y, z, t, nu), g.F, mu, 0, c);
         {
             T b[18];
-            ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, mu), nu, 0, b);  // B = U_nu(x + mu)
+            ld_link_part<T, 18>(link_site_at(U, g, x, y, z, t, mu), g.F, nu, 0, b);  // B = U_nu(x + mu)
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 T a[6];
-                ld_link_part<T, 6>(U, g, site, mu, 6 * i, a);  // row i of A = U_mu(x)
+                ld_link_part<T, 6>(own, g.F, mu, 6 * i, a);  // row i of A = U_mu(x)
 #pragma unroll
                 for (int k = 0; k < 3; ++k)  // t[i][k] = sum_j a[i][j] b[j][k]   (mat_nn)
                     dot3<T, FUSED, PLAIN>([&](int j, int q) { return a[2 * j + q]; },
@@ -90,7 +97,7 @@ __global__ void __launch_bounds__(128, MINB)
                                           tm[(3 * i + k) * 2 + 1]);
             }
         }
-        if constexpr (!EARLY_C) ld_link_part<T, 18>(U, g, shifted(g, x, y, z, t, nu), mu, 0, c);  // C = U_mu(x + nu)
+        if constexpr (!EARLY_C) ld_link_part<T, 18>(link_site_at(U, g, x, y, z, t, nu), g.F, mu, 0, c);  // C = U_mu(x + nu)
 #pragma unroll
         for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -117,7 +124,9 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     const int64_t n = g.F * g.nt;
     const unsigned grid = static_cast<unsigned>((n + 127) / 128);
     // register budget and gather order from the 48^4 sweep on B200 (fraction of HBM): f64 exact
-    // 4 CTAs/SM (0.427), f64 FMA 3 (0.474 vs 0.467 at 4), f32 6 with C gathered early (0.310 vs 0.299)
+    // 4 CTAs/SM (0.427), f64 FMA 3 (0.474 vs 0.467 at 4), f32 6 with C gathered early (0.310 vs 0.299).
+    // r02: dropping the per-load 64-bit site division took f64 exact 0.450 -> 0.497 (same box); a fully
+    // unrolled plane loop (compile-time mu, nu) measured 0.362 (loads hoisted across planes)
     if constexpr (sizeof(T) == 4) k_link_rows<T, FUSED, 6, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     else k_link_rows<T, FUSED, FUSED ? 3 : 4, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     return check_launch("link_product(rows)");
