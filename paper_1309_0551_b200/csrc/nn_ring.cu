@@ -371,7 +371,10 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     const int per = std::max(per_sm, 1);
     const int G_full = di.num_sms * per;
     const int L = t_end - t_begin;
-    p.chunk = pick_chunk(p.nblocks, L, G_full);
+    // a ring work item's prologue (v(t0) and w_t(t0-1) from global) costs about half a step: same-box
+    // A/B of the chunk picker's cost (profiles/r02/ab_nn_ring_prologue.txt): 32^4 f32 0.799 / f64 0.754
+    // at 0.5 against 0.785 / 0.724 at the walk kernels' 2.0; 64^3x16 and 64^3x128 unchanged
+    p.chunk = pick_chunk(p.nblocks, L, G_full, 0.5);
     p.nitems = p.nblocks * ((L + p.chunk - 1) / p.chunk);
     p.w_next = w_next;
     if constexpr (EDGES) p.nitems = p.nblocks * (nt > 1 ? 2 : 1);
