@@ -64,6 +64,32 @@ def test_invalid_arguments_rejected_without_touching_the_device():
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_tuning_knobs_validate_names_and_ranges_without_a_device():
+    """su3g_set_option (include/su3g.h): every documented knob accepts its range, rejects the rest
+    (the removed ring link walk included), and restores its default."""
+    lib = _lib.load()
+    ok = {"nn_variant": (0, 1, 3, 4), "link_variant": (0, 1, 3, 4), "dslash_eo_variant": (0, 1, 2),
+          "dslash_eo_ring_cfg": (0, 1), "link_pair_prefetch": (-1, 0, 1), "nn_ring_cfg": (0, 1, 2, 3),
+          "sm_reserve": (0, 4)}
+    bad = {"nn_variant": (2, 5), "link_variant": (2, 5, -1), "dslash_eo_variant": (3, -1),
+           "dslash_eo_ring_cfg": (2,), "link_pair_prefetch": (2, -2), "nn_ring_cfg": (4,), "sm_reserve": (-1, 65)}
+    try:
+        for name, vals in ok.items():
+            for v in vals:
+                assert lib.su3g_set_option(name.encode(), v) == _lib.SU3G_OK, (name, v)
+        for name, vals in bad.items():
+            for v in vals:
+                assert lib.su3g_set_option(name.encode(), v) == _lib.SU3G_EINVAL, (name, v)
+        lib.su3g_set_option(b"link_variant", 2)
+        assert b"removed" in lib.su3g_last_error()
+        assert lib.su3g_set_option(b"no_such_knob", 0) == _lib.SU3G_EINVAL
+    finally:
+        for name, default in (("nn_variant", 0), ("link_variant", 0), ("dslash_eo_variant", 0),
+                              ("dslash_eo_ring_cfg", 0), ("link_pair_prefetch", -1), ("nn_ring_cfg", 0),
+                              ("sm_reserve", 0)):
+            lib.su3g_set_option(name.encode(), default)
+
+
 def test_no_cpu_fallback():
     from paper_1309_0551_b200 import kernels
 
