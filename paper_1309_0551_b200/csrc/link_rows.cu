@@ -126,7 +126,8 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     // register budget and gather order from the 48^4 sweep on B200 (fraction of HBM): f64 exact
     // 4 CTAs/SM (0.427), f64 FMA 3 (0.474 vs 0.467 at 4), f32 6 with C gathered early (0.310 vs 0.299).
     // r02: dropping the per-load 64-bit site division took f64 exact 0.450 -> 0.497 (same box); a fully
-    // unrolled plane loop (compile-time mu, nu) measured 0.362 (loads hoisted across planes)
+    // unrolled plane loop (compile-time mu, nu) measured 0.362 (loads hoisted across planes), 5 / 6 CTAs
+    // per SM (96 / 80 registers, spills) 0.430 / 0.379 against 0.480 at 4 (profiles/r02/ab_link_rows_unroll.txt)
     if constexpr (sizeof(T) == 4) k_link_rows<T, FUSED, 6, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     else k_link_rows<T, FUSED, FUSED ? 3 : 4, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     return check_launch("link_product(rows)");

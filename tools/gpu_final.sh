@@ -25,6 +25,6 @@ $CMD > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "ncu_launch=$?" >> gpurun_out/status.txt
 python tools/prof_targets.py > gpurun_out/prof_targets_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:'k_nn_ring|k_link|k_dslash_eo' -c 8 \
+  ncu --set full --clock-control none --import-source on -k regex:'k_nn_ring|k_link|k_dslash' -c 8 \
       -o gpurun_out/prof_final python tools/prof_targets.py > gpurun_out/ncu_prof_final.log 2>&1
 echo "ncu_full=$?" >> gpurun_out/status.txt

@@ -1,11 +1,11 @@
 """Launch each bench workload's dominant kernel ONCE in one process, for a single ncu --set full capture:
 
-    ncu --set full -k regex:'k_nn_ring|k_link|k_dslash_eo' -c 8 -o prof python tools/prof_targets.py
+    ncu --set full -k regex:'k_nn_ring|k_link|k_dslash' -c 8 -o prof python tools/prof_targets.py
 
 Targets, in launch order (the default dispatch of each bench workload):
   nn-weak f32 / f64  64^3x16 NN sweep (k_nn_ring)               -- the headline kernel
   link f64           48^4 link product, exact and FMA
-  dslash f32 / f64   64^3x16 even/odd dslash on checkerboarded fields (k_dslash_eo)
+  dslash f32 / f64   64^3x16 even/odd dslash on checkerboarded fields (k_dslash_ring)
 The kernel names print to stdout, so the capture order can be matched to traffic.json keys.
 """
 import os
