@@ -370,6 +370,7 @@ static int dring_dispatch(const T* U, const T* v, T* out, int nx, int ny, int nz
         return run_dslash_ring<T, FUSED, NXH, 4, 2>(U, v, out, nx, ny, nz, nt, parity, st);
     } else {  // 64^3x16, fraction of HBM: 8 slots x 2 CTAs/SM 0.976-0.979, 6 slots x 3 CTAs 0.970-0.972
         if (g_eo_ring_cfg == 1) return run_dslash_ring<T, FUSED, NXH, 6, 3>(U, v, out, nx, ny, nz, nt, parity, st);
+        if (g_eo_ring_cfg == 2) return run_dslash_ring<T, FUSED, NXH, 4, 4>(U, v, out, nx, ny, nz, nt, parity, st);
         return run_dslash_ring<T, FUSED, NXH, 8, 2>(U, v, out, nx, ny, nz, nt, parity, st);
     }
 }

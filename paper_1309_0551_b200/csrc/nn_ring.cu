@@ -393,14 +393,19 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     return check_launch("nn_sweep(ring)");
 }
 
-int g_ring_cfg = 0;  // su3g_set_option("nn_ring_cfg"): f32 ring configuration (A/B), 0 = default
+int g_ring_cfg = 0;  // su3g_set_option("nn_ring_cfg"): ring slot / CTA configuration (A/B), 0 = default
 
 template <typename T, bool FUSED, int NX>
 static int ring_dispatch(const T* U, const T* v, T* out, int nx, int ny, int nz, int nt, int t_begin, int t_end,
                          const T* v_hi, const T* w_lo, cudaStream_t st) {
-    if constexpr (sizeof(T) == 8) {  // f64: four 36-KB slots next to the single-buffered exchange
+    if constexpr (sizeof(T) == 8) {  // f64: four slots next to the single-buffered exchange
+        if (g_ring_cfg == 1 || (g_ring_cfg == 0 && NX == 32))  // 32-wide blocks: two CTAs per SM
+            return run_ring<T, FUSED, NX, 4, false, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
         return run_ring<T, FUSED, NX, 4, false, 1>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
     } else {
+        // 32-wide blocks (N = 128): four CTAs per SM at <= 96 registers (32^4: 0.843 vs 0.791 with three)
+        if (NX == 32 && g_ring_cfg == 0)
+            return run_ring<T, FUSED, NX, 4, false, 4>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
         // f32: two CTAs per SM, four 18-KB slots each (same-box A/B at 64^3x16, fraction of HBM:
         // 0.905 vs 0.840 for one CTA with eight slots, 0.812 one CTA with six slots and a double-
         // buffered exchange, 0.716 two CTAs with two slots each; the f32 TMA walk 0.835)
@@ -408,6 +413,7 @@ static int ring_dispatch(const T* U, const T* v, T* out, int nx, int ny, int nz,
             case 1: return run_ring<T, FUSED, NX, 8, false, 1>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
             case 2: return run_ring<T, FUSED, NX, 6, true, 1>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
             case 3: return run_ring<T, FUSED, NX, 2, true, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
+            case 4: return run_ring<T, FUSED, NX, 4, false, 4>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
             default: return run_ring<T, FUSED, NX, 4, false, 2>(U, v, out, nx, ny, nz, nt, t_begin, t_end, v_hi, w_lo, st);
         }
     }

@@ -359,7 +359,7 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "dslash_eo_ring_cfg") == 0) {
-        if (value < 0 || value > 1) return fail_invalid("set_option: dslash_eo_ring_cfg must be 0 or 1");
+        if (value < 0 || value > 2) return fail_invalid("set_option: dslash_eo_ring_cfg must be in [0, 2]");
         g_eo_ring_cfg = static_cast<int>(value);
         return SU3G_OK;
     }
@@ -369,7 +369,7 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "nn_ring_cfg") == 0) {
-        if (value < 0 || value > 3) return fail_invalid("set_option: nn_ring_cfg must be in [0, 3]");
+        if (value < 0 || value > 4) return fail_invalid("set_option: nn_ring_cfg must be in [0, 4]");
         g_ring_cfg = static_cast<int>(value);
         return SU3G_OK;
     }
