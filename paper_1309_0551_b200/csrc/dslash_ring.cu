@@ -368,10 +368,10 @@ static int dring_dispatch(const T* U, const T* v, T* out, int nx, int ny, int nz
     if constexpr (sizeof(T) == 8) {  // 64^3x16: 4 slots x 2 CTAs/SM 1.009, 6 slots x 1 CTA 1.003-1.004
         if (g_eo_ring_cfg == 1) return run_dslash_ring<T, FUSED, NXH, 6, 1>(U, v, out, nx, ny, nz, nt, parity, st);
         return run_dslash_ring<T, FUSED, NXH, 4, 2>(U, v, out, nx, ny, nz, nt, parity, st);
-    } else {  // 64^3x16, fraction of HBM: 8 slots x 2 CTAs/SM 0.976-0.979, 6 slots x 3 CTAs 0.970-0.972
+    } else {  // 64^3x16, fraction of HBM: 4 slots x 4 CTAs/SM 0.992, 8 x 2: 0.971-0.979, 6 x 3: 0.970
         if (g_eo_ring_cfg == 1) return run_dslash_ring<T, FUSED, NXH, 6, 3>(U, v, out, nx, ny, nz, nt, parity, st);
-        if (g_eo_ring_cfg == 2) return run_dslash_ring<T, FUSED, NXH, 4, 4>(U, v, out, nx, ny, nz, nt, parity, st);
-        return run_dslash_ring<T, FUSED, NXH, 8, 2>(U, v, out, nx, ny, nz, nt, parity, st);
+        if (g_eo_ring_cfg == 2) return run_dslash_ring<T, FUSED, NXH, 8, 2>(U, v, out, nx, ny, nz, nt, parity, st);
+        return run_dslash_ring<T, FUSED, NXH, 4, 4>(U, v, out, nx, ny, nz, nt, parity, st);
     }
 }
 

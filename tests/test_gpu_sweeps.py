@@ -591,7 +591,7 @@ def test_dslash_eo_vs_c_oracle(dims, hints, zc, precision):
         _lib.set_option("dslash_eo_zc", 0)
 
 
-@pytest.mark.parametrize("cfg", [0, 1])
+@pytest.mark.parametrize("cfg", [0, 1, 2])
 @pytest.mark.parametrize("dims", [(64, 4, 4, 6), (32, 8, 4, 6), (64, 2, 6, 2), (32, 4, 2, 8), (64, 64, 16, 4)])
 def test_dslash_eo_ring_vs_c_oracle(dims, cfg, precision):
     """the half-lattice ring walk (dslash_eo_variant 2, both slot configurations) equals the full sweep on
