@@ -61,7 +61,8 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "nn_variant":   0 auto, 1 generic one-thread-per-site (z-chunked order), 3 TMA t-walk,
  *                   4 TMA ring walk (the default where it applies: nx in {32, 48, 64}, even ny, nz)
  *   "nn_ring_cfg":  f32 ring-walk slot / CTA configuration for A/B (0 = default)
- *   "link_variant": 0 auto, 1 rows gather, 3 row-split carried t-walk, 4 two-lane pair walk (FMA mode)
+ *   "link_variant": 0 auto, 1 rows gather, 3 row-split carried t-walk, 4 two-lane pair walk (FMA mode),
+ *                   5 factored two-lane pair walk (FMA mode, nine products per site)
  *   "link_pair_prefetch": -1 auto (f32), 0 / 1: L2 prefetch one step ahead in the pair walk
  *   "dslash_eo_variant": 0 auto, 1 gather kernel, 2 half-lattice ring walk (nx in {32, 64}, even ny, nz)
  *   "dslash_eo_ring_cfg": slot / CTA configuration of that ring walk for A/B (0 = default)

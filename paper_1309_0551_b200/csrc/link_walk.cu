@@ -588,7 +588,256 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
     }
 }
 
-template <typename T, int NX, int BY>
+// ======================================================================================
+// FMA mode, factored: two lanes per site, nine matrix products instead of twelve (k_link_fact).
+//
+// With FMA chains the association is free as well (the north-star tolerance, not bit equality):
+//   acc(x) = s * sum_mu U_mu(x) M_mu(x),   M_mu(x) = sum_{nu > mu} U_nu(x+mu) U_mu(x+nu)^dag,
+// three B C^dag products for mu = 0, two for mu = 1, one for mu = 2, then one A M product per mu:
+// 9 x 108 FMAs + 18 multiplies = 990 per site instead of 1404, and 15 staged matrices read per site
+// instead of 18.  Lanes 0-15 of a warp take mu = 0 (four products), lanes 16-31 mu = 1 and 2 (five);
+// every step has the same product type in both halves, so the warp runs five product steps with one
+// instruction stream (lanes 0-15 sit out the fifth):
+//   S1  M = B C^dag : B U_1(x+0), C U_0(x+1) [Y0]      | B U_2(x+1) [Y2], C U_1(x+2) [Z1]
+//   S2  M += B C^dag: B U_2(x+0), C U_0(x+2) [Z0]      | B U_3(x+1) [Y3], C U_1(x+t)
+//   S3  M += B C^dag: B U_3(x+0), C U_0(x+t)           | (M_1 set aside, M = 0) B U_3(x+2) [Z3], C U_2(x+t)
+//   S4  acc = A M   : A U_0(x), M_0                    | A U_1(x), M_1
+//   S5  acc += A M  :                                  | A U_2(x), M_2
+// Same slots, barriers and block walk as k_link_pair; the producer issues a step's loads in the order
+// the previous step frees their slots (S1 frees Y0 / Y2 / Z1, S2 Z0 / Y3, S3 E3 / Z3, S4 U_0 / U_1,
+// S5 U_2).
+// ======================================================================================
+
+namespace {
+
+// m (+)= B C^dag: m[i][k] += sum_j B[i][j] conj(C[k][j]); element (r, c) of B / C at ptr[((3r+c)*2+q) * str]
+template <typename T, bool FIRST>
+__device__ __forceinline__ void bcdag_fma(const T* bs, int bstr, const T* cs, int cstr, T* m) {
+    T b[18];
+#pragma unroll
+    for (int q = 0; q < 18; ++q) b[q] = bs[q * bstr];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T c[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) c[q] = cs[(6 * k + q) * cstr];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            T re = FIRST ? T(0) : m[(3 * i + k) * 2], im = FIRST ? T(0) : m[(3 * i + k) * 2 + 1];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const T br = b[(3 * i + j) * 2], bi = b[(3 * i + j) * 2 + 1], cr = c[2 * j], ci = c[2 * j + 1];
+                if (FIRST && j == 0) {
+                    re = br * cr;
+                    im = bi * cr;
+                } else {
+                    re = fma(br, cr, re);
+                    im = fma(bi, cr, im);
+                }
+                re = fma(bi, ci, re);
+                im = fma(-br, ci, im);
+            }
+            m[(3 * i + k) * 2] = re;
+            m[(3 * i + k) * 2 + 1] = im;
+        }
+    }
+}
+
+// acc (+)= A M: acc[i][k] += sum_j A[i][j] M[j][k]; A element (i, j) at as[((3i+j)*2+q) * astr], M in registers
+template <typename T, bool FIRST>
+__device__ __forceinline__ void am_fma(const T* as, int astr, const T* m, T* acc) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        T a[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) a[q] = as[(6 * i + q) * astr];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            T re = FIRST ? T(0) : acc[(3 * i + k) * 2], im = FIRST ? T(0) : acc[(3 * i + k) * 2 + 1];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const T ar = a[2 * j], ai = a[2 * j + 1], mr = m[(3 * j + k) * 2], mi = m[(3 * j + k) * 2 + 1];
+                if (FIRST && j == 0) {
+                    re = ar * mr;
+                    im = ar * mi;
+                } else {
+                    re = fma(ar, mr, re);
+                    im = fma(ar, mi, im);
+                }
+                re = fma(-ai, mi, re);
+                im = fma(ai, mr, im);
+            }
+            acc[(3 * i + k) * 2] = re;
+            acc[(3 * i + k) * 2 + 1] = im;
+        }
+    }
+}
+
+}  // namespace
+
+template <typename T, int NX, int BY, bool PF>
+__global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
+    k_link_fact(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapY,
+                T* __restrict__ acc_out, WalkParams p, T s) {
+    using G = PairGeo<T, NX, BY>;
+    constexpr int N = G::N, NWC = G::NWC;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::TOTAL);
+    uint64_t* empty = full + G::NBAR;
+    constexpr int B_E3 = 6, B_Z = 7, B_Y = 10;  // Z: +0 U_0, +1 U_1, +2 U_3; Y: +0 U_0, +1 U_2, +2 U_3
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int k = 0; k < G::NBAR; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], NWC);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int GR = gridDim.x;
+
+    if (tid >= 32 * NWC) {  // ------------------------------------------ producer warp
+        if (tid != 32 * NWC) return;
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+        uint32_t ne = 0, ns = 0;  // slices loaded (buffer ne & 1); steps issued (E3 / Z / Y uses)
+        auto load = [&](int bar, uint32_t use, T* dst, const CUtensorMap* map, int y, int z, int plane, int reals) {
+            if (use) mbar_wait(&empty[bar], (use - 1) & 1);
+            mbar_arrive_expect_tx(&full[bar], reals * sizeof(T));
+            tma_load_4d(dst, map, 0, y, z, plane, &full[bar], pol);
+        };
+        auto load_link = [&](int k, uint32_t slice_no, int ts, int y0, int z0) {
+            const int b = slice_no & 1;
+            load(2 * k + b, slice_no >> 1, sm + G::OFF_E + (2 * k + b) * G::BLK, &mapB, y0, z0, ts * 72 + 18 * k,
+                 G::BLK);
+        };
+        for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
+            int64_t blk;
+            int t0, t1;
+            walk_item(p, item, blk, t0, t1);
+            const int y0 = static_cast<int>(blk % p.nby) * BY, z0 = static_cast<int>(blk / p.nby);
+            const int yup = (y0 + BY) % p.ny, zup = (z0 + 1) % p.nz;
+            for (int k = 0; k < 3; ++k) load_link(k, ne, t0, y0, z0);
+            ++ne;
+            for (int t = t0; t < t1; ++t, ++ns) {
+                const int tn = (t + 1 == p.nt) ? 0 : t + 1;
+                if constexpr (PF) {  // L2 warm-up one step ahead: the next step's halos and U_3, slice t+2
+                    const int tn2 = (tn + 1 == p.nt) ? 0 : tn + 1;
+                    if (t + 1 < t1) {
+                        for (int k : {0, 36, 54}) tma_prefetch(&mapY, 0, yup, z0, tn * 72 + k);
+                        for (int k : {0, 18, 54}) tma_prefetch(&mapB, 0, y0, zup, tn * 72 + k);
+                        tma_prefetch(&mapB, 0, y0, z0, tn * 72 + 54);
+                        for (int k = 0; k < 3; ++k) tma_prefetch(&mapB, 0, y0, z0, tn2 * 72 + 18 * k);
+                    }
+                }
+                // issue order = the order the previous step releases the slots (every wait monotone)
+                load(B_Y + 0, ns, sm + G::OFF_Y, &mapY, yup, z0, t * 72, G::YSUB);
+                load(B_Y + 1, ns, sm + G::OFF_Y + G::YSUB, &mapY, yup, z0, t * 72 + 36, G::YSUB);
+                load(B_Z + 1, ns, sm + G::OFF_Z + G::BLK, &mapB, y0, zup, t * 72 + 18, G::BLK);
+                load(B_Z + 0, ns, sm + G::OFF_Z, &mapB, y0, zup, t * 72, G::BLK);
+                load(B_Y + 2, ns, sm + G::OFF_Y + 2 * G::YSUB, &mapY, yup, z0, t * 72 + 54, G::YSUB);
+                load(B_E3, ns, sm + G::OFF_E3, &mapB, y0, z0, t * 72 + 54, G::BLK);
+                load(B_Z + 2, ns, sm + G::OFF_Z + 2 * G::BLK, &mapB, y0, zup, t * 72 + 54, G::BLK);
+                load_link(1, ne, tn, y0, z0);
+                load_link(0, ne, tn, y0, z0);
+                load_link(2, ne, tn, y0, z0);
+                ++ne;
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------------------ compute warps
+    const int lane = tid & 31;
+    const int sl = (tid >> 5) * 16 + (lane & 15);
+    const int h = lane >> 4;
+    const int lx = sl % NX, ly = sl / NX;
+    const int ix_up = (lx + 1 == NX) ? sl - lx : sl + 1;
+    const bool y_in = ly + 1 < BY;
+    const int ystr = y_in ? N : NX;
+    const T* const E3 = sm + G::OFF_E3;
+    const T* const Z0 = sm + G::OFF_Z;
+    const T* const Z1 = Z0 + G::BLK;
+    const T* const Z3 = Z1 + G::BLK;
+    const T* const Y0 = sm + G::OFF_Y;
+    const T* const Y2 = Y0 + G::YSUB;
+    const T* const Y3 = Y2 + G::YSUB;
+    auto release = [&](int bar) { warp_release(&empty[bar], lane); };
+    auto wait_full = [&](int bar, uint32_t use) { mbar_wait(&full[bar], use & 1); };
+    auto E = [&](int k, uint32_t slice_no) { return sm + G::OFF_E + (2 * k + (slice_no & 1)) * G::BLK; };
+
+    uint32_t ne = 0, ns = 0;
+    for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
+        int64_t blk;
+        int t0, t1;
+        walk_item(p, item, blk, t0, t1);
+        const int y = static_cast<int>(blk % p.nby) * BY + ly;
+        const int z = static_cast<int>(blk / p.nby);
+        const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
+        for (int t = t0; t < t1; ++t, ++ns) {
+            const uint32_t c = ne, n = ne + 1;  // slice loads of t and t+1
+            const T *E0c = E(0, c), *E1c = E(1, c), *E2c = E(2, c);
+            for (int k = 0; k < 3; ++k) wait_full(2 * k + (c & 1), c >> 1);
+            T m[18], m1[18], acc[18];
+            // ---- S1: B U_1(x+0), C U_0(x+1) | B U_2(x+1), C U_1(x+2)
+            wait_full(B_Y + 0, ns);
+            wait_full(B_Y + 1, ns);
+            wait_full(B_Z + 1, ns);
+            bcdag_fma<T, true>(h ? (y_in ? E2c + sl + NX : Y2 + lx) : E1c + ix_up, h ? ystr : N,
+                               h ? Z1 + sl : (y_in ? E0c + sl + NX : Y0 + lx), h ? N : ystr, m);
+            release(B_Y + 0);
+            release(B_Y + 1);
+            release(B_Z + 1);
+            // ---- S2: B U_2(x+0), C U_0(x+2) | B U_3(x+1), C U_1(x+t)
+            wait_full(B_Z + 0, ns);
+            wait_full(B_Y + 2, ns);
+            wait_full(B_E3, ns);
+            wait_full(2 + (n & 1), n >> 1);
+            bcdag_fma<T, false>(h ? (y_in ? E3 + sl + NX : Y3 + lx) : E2c + ix_up, h ? ystr : N,
+                                h ? E(1, n) + sl : Z0 + sl, N, m);
+            release(B_Z + 0);
+            release(B_Y + 2);
+            // lanes 16-31: M_1 is complete, M_2 starts from zero
+#pragma unroll
+            for (int q = 0; q < 18; ++q) {
+                m1[q] = m[q];
+                m[q] = h ? T(0) : m[q];
+            }
+            // ---- S3: B U_3(x+0), C U_0(x+t) | B U_3(x+2), C U_2(x+t)
+            wait_full(B_Z + 2, ns);
+            wait_full(0 + (n & 1), n >> 1);
+            wait_full(4 + (n & 1), n >> 1);
+            bcdag_fma<T, false>(h ? Z3 + sl : E3 + ix_up, N, (h ? E(2, n) : E(0, n)) + sl, N, m);
+            release(B_E3);
+            release(B_Z + 2);
+            // ---- S4: acc = U_0(x) M_0 | acc = U_1(x) M_1
+#pragma unroll
+            for (int q = 0; q < 18; ++q) m1[q] = h ? m1[q] : m[q];
+            am_fma<T, true>((h ? E1c : E0c) + sl, N, m1, acc);
+            release(0 + (c & 1));
+            release(2 + (c & 1));
+            // ---- S5: lanes 16-31 acc += U_2(x) M_2
+            if (h) am_fma<T, false>(E2c + sl, N, m, acc);
+            release(4 + (c & 1));
+            ++ne;
+            // ---- the two half-sums meet: lanes 0-15 store elements 0..8, lanes 16-31 elements 9..17
+            T* o = acc_out + int64_t(t) * 18 * p.F + s3;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const T mine = h ? acc[9 + k] : acc[k];
+                const T give = h ? acc[k] : acc[9 + k];
+                const T got = __shfl_xor_sync(0xffffffffu, give, 16);
+                __stcs(o + (9 * h + k) * p.F, s * (mine + got));
+            }
+        }
+        // slice t1 (only the last step's t-planes read it)
+        for (int k = 0; k < 3; ++k) release(2 * k + (ne & 1));
+        ++ne;
+    }
+}
+
+template <typename T, int NX, int BY, bool FACT>
 static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
     using G = PairGeo<T, NX, BY>;
     CUtensorMap mB, mY;
@@ -599,7 +848,8 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
     const bool pf = g_pair_prefetch < 0 ? sizeof(T) == 4 : g_pair_prefetch != 0;  // auto: f32 only (A/B)
-    auto kern = pf ? k_link_pair<T, NX, BY, true> : k_link_pair<T, NX, BY, false>;
+    auto kern = FACT ? (pf ? k_link_fact<T, NX, BY, true> : k_link_fact<T, NX, BY, false>)
+                     : (pf ? k_link_pair<T, NX, BY, true> : k_link_pair<T, NX, BY, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     WalkParams p{};
     p.ny = ny; p.nz = nz; p.nt = nt;
@@ -613,24 +863,26 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     p.nitems = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
     const int grid = static_cast<int>(std::min<int64_t>(Gfull, p.nitems));
     kern<<<grid, G::THREADS, smem, st>>>(mB, mY, acc, p, s);
-    note_kernel(std::string("k_link_pair<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
+    note_kernel(std::string(FACT ? "k_link_fact<" : "k_link_pair<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
                 std::to_string(BY) + "x1" + (pf ? ",L2 prefetch" : "") + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
                 ",chunk " + std::to_string(p.chunk) + ">");
-    return check_launch("link_product(pair)");
+    return check_launch(FACT ? "link_product(fact)" : "link_product(pair)");
 }
 
 // FMA mode only; 1 = not applicable to this lattice
-template <typename T>
+template <typename T, bool FACT>
 int launch_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
     if (!aligned16(U)) return 1;
-    if (nx == 48 && ny % 3 == 0) return run_link_pair<T, 48, 3>(U, acc, nx, ny, nz, nt, s, st);
-    if (nx == 32 && ny % 4 == 0) return run_link_pair<T, 32, 4>(U, acc, nx, ny, nz, nt, s, st);
-    if (nx == 64 && ny % 2 == 0) return run_link_pair<T, 64, 2>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 48 && ny % 3 == 0) return run_link_pair<T, 48, 3, FACT>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 32 && ny % 4 == 0) return run_link_pair<T, 32, 4, FACT>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 64 && ny % 2 == 0) return run_link_pair<T, 64, 2, FACT>(U, acc, nx, ny, nz, nt, s, st);
     return 1;
 }
 
-template int launch_link_pair<float>(const float*, float*, int, int, int, int, float, cudaStream_t);
-template int launch_link_pair<double>(const double*, double*, int, int, int, int, double, cudaStream_t);
+template int launch_link_pair<float, false>(const float*, float*, int, int, int, int, float, cudaStream_t);
+template int launch_link_pair<double, false>(const double*, double*, int, int, int, int, double, cudaStream_t);
+template int launch_link_pair<float, true>(const float*, float*, int, int, int, int, float, cudaStream_t);
+template int launch_link_pair<double, true>(const double*, double*, int, int, int, int, double, cudaStream_t);
 
 // 1 = not applicable to this lattice (caller falls back)
 template <typename T, bool FUSED>

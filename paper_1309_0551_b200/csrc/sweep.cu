@@ -305,15 +305,22 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     if (mode != SU3G_EXACT && mode != SU3G_FMA) return fail_invalid("link_product: mode must be SU3G_EXACT or SU3G_FMA");
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int lv = g_link_variant.load();
-    // auto (48^4 on B200, fraction of HBM; profiles/r02/ab_link_walk.md, ab_link_pair.txt): FMA mode -> the
-    // two-lane pair walk (f64 0.620, f32 0.435; the removed ring walk 0.546 / 0.397, rows 0.525 / 0.357);
+    // auto (48^4 on B200, fraction of HBM; profiles/r02/ab_link_walk.md, ab_link_pair.txt, ab_link_fact.txt):
+    // FMA mode -> the factored two-lane pair walk (f64 0.677, f32 0.565; the plane-by-plane pair walk
+    // 0.611 / 0.429, the removed ring walk 0.546 / 0.397, rows 0.525 / 0.357);
     // exact f32 -> the row-split carried walk (0.351 vs rows 0.309); exact f64 -> rows (0.465; walk 0.461,
     // an exact pair walk 0.413)
-    if (lv == 4 || (lv == 0 && mode == SU3G_FMA)) {
-        if (mode != SU3G_FMA) return fail_invalid("link_product: the pair walk (link_variant 4) is FMA mode only");
-        const int rc = launch_link_pair<T>(U, acc, nx, ny, nz, nt, s, st);
+    if (lv == 5 || (lv == 0 && mode == SU3G_FMA)) {
+        if (mode != SU3G_FMA) return fail_invalid("link_product: the factored pair walk (link_variant 5) is FMA mode only");
+        const int rc = launch_link_pair<T, true>(U, acc, nx, ny, nz, nt, s, st);
         if (rc != 1) return rc;
-        if (lv == 4) return fail_invalid("link_product: pair kernel not applicable to this lattice");
+        if (lv == 5) return fail_invalid("link_product: factored pair kernel not applicable to this lattice");
+    }
+    if (lv == 4) {
+        if (mode != SU3G_FMA) return fail_invalid("link_product: the pair walk (link_variant 4) is FMA mode only");
+        const int rc = launch_link_pair<T, false>(U, acc, nx, ny, nz, nt, s, st);
+        if (rc != 1) return rc;
+        return fail_invalid("link_product: pair kernel not applicable to this lattice");
     }
     if (lv == 3 || (lv == 0 && sizeof(T) == 4 && mode == SU3G_EXACT)) {
         const int rc = mode == SU3G_FMA ? launch_link_walk<T, true>(U, acc, nx, ny, nz, nt, s, st)
@@ -346,9 +353,10 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 4 || value == 2)
-            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 3 (row-split walk) or "
-                                "4 (two-lane pair walk, FMA); 2 (the ring walk) was removed, measured slower");
+        if (value < 0 || value > 5 || value == 2)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 3 (row-split walk), "
+                                "4 (two-lane pair walk, FMA) or 5 (factored pair walk, FMA); 2 (the ring walk) was "
+                                "removed, measured slower");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }

@@ -225,16 +225,17 @@ def test_link_product_guarded(dt, dims, variant):
     assert np.array_equal(_from_soa(ga.host(), dims, (3, 3, 2)), want), _lib.last_kernel()
 
 
+@pytest.mark.parametrize("variant", [4, 5], ids=["pair", "factored"])
 @pytest.mark.parametrize("dims", [(48, 6, 5, 7), (32, 8, 4, 6), (48, 3, 2, 3)])
-def test_link_pair_fma_guarded(dt, dims):
-    """the FMA-only pair kernel: guards intact, result within tolerance (a NaN read would not be)"""
+def test_link_pair_fma_guarded(dt, dims, variant):
+    """the FMA-only pair kernels: guards intact, result within tolerance (a NaN read would not be)"""
     from oracle.compare import floored_rel_err
 
     V = int(np.prod(dims))
     U = inputs.random_links(inputs.config_rng(850 + V), V, 4, dtype=dt)
     want = coracle.link_product(U, dims, 1 / 6)
     gU, ga = Guarded(dt, U.size, _to_soa(U, dims)), Guarded(dt, V * 18)
-    _lib.set_option("link_variant", 4)
+    _lib.set_option("link_variant", variant)
     try:
         _lib.call(f"su3g_link_product_{SFX[dt]}", gU.ptr, ga.ptr, *dims, float(dt(1 / 6)), 1, _stream())
         torch.cuda.synchronize()

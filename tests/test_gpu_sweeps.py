@@ -100,7 +100,7 @@ def test_link_product_config3_full_size(variant):
         del got
         assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-12
         if variant == 0:
-            assert _lib.last_kernel().startswith("k_link_pair<f64,48x3x1"), _lib.last_kernel()
+            assert _lib.last_kernel().startswith("k_link_fact<f64,48x3x1"), _lib.last_kernel()
     finally:
         _lib.set_option("link_variant", 0)
 
@@ -116,7 +116,7 @@ def test_link_product_config3_f32_full_size():
     assert np.array_equal(sweeps.link_product_aos(U, dims, 1 / 6), want)
     assert _lib.last_kernel().startswith("k_link_walk<f32,48x3x1"), _lib.last_kernel()  # exact f32: the carried walk
     assert floored_rel_err(sweeps.link_product_aos(U, dims, 1 / 6, mode="fma"), want) <= 1e-5
-    assert _lib.last_kernel().startswith("k_link_pair<f32,48x3x1"), _lib.last_kernel()
+    assert _lib.last_kernel().startswith("k_link_fact<f32,48x3x1"), _lib.last_kernel()
 
 
 @pytest.mark.parametrize("C", [6, 18, 24, 72])
@@ -344,20 +344,21 @@ def test_link_product_bitwise(dims, precision, variant):
 @pytest.mark.parametrize(
     "dims", [(48, 3, 2, 3), (48, 6, 5, 7), (32, 8, 4, 6), (64, 4, 3, 5), (32, 4, 1, 2), (48, 48, 3, 4)]
 )
-def test_link_pair_walk(dims, precision):
-    """link_variant 4 (two lanes per site, three planes each; the FMA-mode default): within the
-    north-star tolerance of the composed reference, on lattices covering every block geometry and the
-    periodic wrap of the t-chunks; exact mode is refused."""
+@pytest.mark.parametrize("variant,kernel", [(4, "k_link_pair<"), (5, "k_link_fact<")], ids=["pair", "factored"])
+def test_link_pair_walk(dims, precision, variant, kernel):
+    """link_variant 4 (two lanes per site, three planes each) and 5 (the factored form, nine products
+    per site; the FMA-mode default): within the north-star tolerance of the composed reference, on
+    lattices covering every block geometry and the periodic wrap of the t-chunks; exact mode is refused."""
     from paper_1309_0551_b200 import _lib
 
     dt = _dt(precision)
     V = int(np.prod(dims))
     U = inputs.random_links(inputs.config_rng(4500 + V), V, 4, dtype=dt)
     want = coracle.link_product(U, dims, 1 / 6)
-    _lib.set_option("link_variant", 4)
+    _lib.set_option("link_variant", variant)
     try:
         got = sweeps.link_product_aos(U, dims, 1 / 6, mode="fma")
-        assert _lib.last_kernel().startswith("k_link_pair<"), _lib.last_kernel()
+        assert _lib.last_kernel().startswith(kernel), _lib.last_kernel()
         assert floored_rel_err(got, want) <= (1e-5 if dt == np.float32 else 1e-12)
         with pytest.raises(ValueError, match="FMA mode only"):
             sweeps.link_product_aos(U, dims, 1 / 6)

@@ -68,10 +68,10 @@ def test_tuning_knobs_validate_names_and_ranges_without_a_device():
     """su3g_set_option (include/su3g.h): every documented knob accepts its range, rejects the rest
     (the removed ring link walk included), and restores its default."""
     lib = _lib.load()
-    ok = {"nn_variant": (0, 1, 3, 4), "link_variant": (0, 1, 3, 4), "dslash_eo_variant": (0, 1, 2),
+    ok = {"nn_variant": (0, 1, 3, 4), "link_variant": (0, 1, 3, 4, 5), "dslash_eo_variant": (0, 1, 2),
           "dslash_eo_ring_cfg": (0, 1, 2), "link_pair_prefetch": (-1, 0, 1), "nn_ring_cfg": (0, 1, 2, 3, 4),
           "sm_reserve": (0, 4)}
-    bad = {"nn_variant": (2, 5), "link_variant": (2, 5, -1), "dslash_eo_variant": (3, -1),
+    bad = {"nn_variant": (2, 5), "link_variant": (2, 6, -1), "dslash_eo_variant": (3, -1),
            "dslash_eo_ring_cfg": (3,), "link_pair_prefetch": (2, -2), "nn_ring_cfg": (5,), "sm_reserve": (-1, 65)}
     try:
         for name, vals in ok.items():
