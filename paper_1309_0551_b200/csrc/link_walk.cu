@@ -598,14 +598,16 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
 // instead of 18.  Lanes 0-15 of a warp take mu = 0 (four products), lanes 16-31 mu = 1 and 2 (five);
 // every step has the same product type in both halves, so the warp runs five product steps with one
 // instruction stream (lanes 0-15 sit out the fifth):
-//   S1  M = B C^dag : B U_1(x+0), C U_0(x+1) [Y0]      | B U_2(x+1) [Y2], C U_1(x+2) [Z1]
-//   S2  M += B C^dag: B U_2(x+0), C U_0(x+2) [Z0]      | B U_3(x+1) [Y3], C U_1(x+t)
-//   S3  M += B C^dag: B U_3(x+0), C U_0(x+t)           | (M_1 set aside, M = 0) B U_3(x+2) [Z3], C U_2(x+t)
+//   S1  M = B C^dag : B U_3(x+0), C U_0(x+t)           | B U_3(x+1) [Y3], C U_1(x+t)        (M_1)
+//   S2  M += B C^dag: B U_1(x+0), C U_0(x+1) [Y0]      | B U_3(x+2) [Z3], C U_2(x+t)        (M_2, from zero)
+//   S3  M += B C^dag: B U_2(x+0), C U_0(x+2) [Z0]      | B U_2(x+1) [Y2], C U_1(x+2) [Z1]   (M_1 again)
 //   S4  acc = A M   : A U_0(x), M_0                    | A U_1(x), M_1
 //   S5  acc += A M  :                                  | A U_2(x), M_2
-// Same slots, barriers and block walk as k_link_pair; the producer issues a step's loads in the order
-// the previous step frees their slots (S1 frees Y0 / Y2 / Z1, S2 Z0 / Y3, S3 E3 / Z3, S4 U_0 / U_1,
-// S5 U_2).
+// Same slots and barriers as k_link_pair, but the block walk runs DOWN in t: slice t+1's U_0..U_2 are
+// then the previous step's own links, already resident, so the t-plane operands never wait, they are
+// used first (S1 / S2) and their buffers take slice t-1 with a whole step in flight.  The producer
+// issues a step's loads in the order the previous step frees their slots, which is also the order
+// the step needs them: Y3, E3, U_0, U_1 | Y0, Z3, U_2 | Z0, Y2, Z1.
 // ======================================================================================
 
 namespace {
@@ -676,7 +678,7 @@ __device__ __forceinline__ void am_fma(const T* as, int astr, const T* m, T* acc
 }  // namespace
 
 template <typename T, int NX, int BY, bool PF>
-__global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
+__global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 2 : 1)  // f32: two CTAs per SM
     k_link_fact(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapY,
                 T* __restrict__ acc_out, WalkParams p, T s) {
     using G = PairGeo<T, NX, BY>;
@@ -718,30 +720,28 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
             walk_item(p, item, blk, t0, t1);
             const int y0 = static_cast<int>(blk % p.nby) * BY, z0 = static_cast<int>(blk / p.nby);
             const int yup = (y0 + BY) % p.ny, zup = (z0 + 1) % p.nz;
-            for (int k = 0; k < 3; ++k) load_link(k, ne, t0, y0, z0);
+            // the slice above the item (U_0..U_2 only): the first step's U_mu(x+t)
+            for (int k = 0; k < 3; ++k) load_link(k, ne, t1 == p.nt ? 0 : t1, y0, z0);
             ++ne;
-            for (int t = t0; t < t1; ++t, ++ns) {
-                const int tn = (t + 1 == p.nt) ? 0 : t + 1;
-                if constexpr (PF) {  // L2 warm-up one step ahead: the next step's halos and U_3, slice t+2
-                    const int tn2 = (tn + 1 == p.nt) ? 0 : tn + 1;
-                    if (t + 1 < t1) {
-                        for (int k : {0, 36, 54}) tma_prefetch(&mapY, 0, yup, z0, tn * 72 + k);
-                        for (int k : {0, 18, 54}) tma_prefetch(&mapB, 0, y0, zup, tn * 72 + k);
-                        tma_prefetch(&mapB, 0, y0, z0, tn * 72 + 54);
-                        for (int k = 0; k < 3; ++k) tma_prefetch(&mapB, 0, y0, z0, tn2 * 72 + 18 * k);
+            for (int t = t1 - 1; t >= t0; --t, ++ns) {
+                if constexpr (PF) {  // L2 warm-up one step ahead: slice t-1
+                    if (t > t0) {
+                        for (int k : {0, 36, 54}) tma_prefetch(&mapY, 0, yup, z0, (t - 1) * 72 + k);
+                        for (int k : {0, 18, 54}) tma_prefetch(&mapB, 0, y0, zup, (t - 1) * 72 + k);
+                        for (int k = 0; k < 4; ++k) tma_prefetch(&mapB, 0, y0, z0, (t - 1) * 72 + 18 * k);
                     }
                 }
-                // issue order = the order the previous step releases the slots (every wait monotone)
-                load(B_Y + 0, ns, sm + G::OFF_Y, &mapY, yup, z0, t * 72, G::YSUB);
-                load(B_Y + 1, ns, sm + G::OFF_Y + G::YSUB, &mapY, yup, z0, t * 72 + 36, G::YSUB);
-                load(B_Z + 1, ns, sm + G::OFF_Z + G::BLK, &mapB, y0, zup, t * 72 + 18, G::BLK);
-                load(B_Z + 0, ns, sm + G::OFF_Z, &mapB, y0, zup, t * 72, G::BLK);
+                // issue order = the order the previous step releases the slots = the order this step needs them
                 load(B_Y + 2, ns, sm + G::OFF_Y + 2 * G::YSUB, &mapY, yup, z0, t * 72 + 54, G::YSUB);
                 load(B_E3, ns, sm + G::OFF_E3, &mapB, y0, z0, t * 72 + 54, G::BLK);
+                load_link(0, ne, t, y0, z0);
+                load_link(1, ne, t, y0, z0);
+                load(B_Y + 0, ns, sm + G::OFF_Y, &mapY, yup, z0, t * 72, G::YSUB);
                 load(B_Z + 2, ns, sm + G::OFF_Z + 2 * G::BLK, &mapB, y0, zup, t * 72 + 54, G::BLK);
-                load_link(1, ne, tn, y0, z0);
-                load_link(0, ne, tn, y0, z0);
-                load_link(2, ne, tn, y0, z0);
+                load_link(2, ne, t, y0, z0);
+                load(B_Z + 0, ns, sm + G::OFF_Z, &mapB, y0, zup, t * 72, G::BLK);
+                load(B_Y + 1, ns, sm + G::OFF_Y + G::YSUB, &mapY, yup, z0, t * 72 + 36, G::YSUB);
+                load(B_Z + 1, ns, sm + G::OFF_Z + G::BLK, &mapB, y0, zup, t * 72 + 18, G::BLK);
                 ++ne;
             }
         }
@@ -775,51 +775,59 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
         const int y = static_cast<int>(blk % p.nby) * BY + ly;
         const int z = static_cast<int>(blk / p.nby);
         const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
-        for (int t = t0; t < t1; ++t, ++ns) {
-            const uint32_t c = ne, n = ne + 1;  // slice loads of t and t+1
+        for (int t = t1 - 1; t >= t0; --t, ++ns) {
+            const uint32_t u = ne, c = ne + 1;  // slice loads of t+1 (resident since the previous step) and t
             const T *E0c = E(0, c), *E1c = E(1, c), *E2c = E(2, c);
-            for (int k = 0; k < 3; ++k) wait_full(2 * k + (c & 1), c >> 1);
             T m[18], m1[18], acc[18];
-            // ---- S1: B U_1(x+0), C U_0(x+1) | B U_2(x+1), C U_1(x+2)
-            wait_full(B_Y + 0, ns);
-            wait_full(B_Y + 1, ns);
-            wait_full(B_Z + 1, ns);
-            bcdag_fma<T, true>(h ? (y_in ? E2c + sl + NX : Y2 + lx) : E1c + ix_up, h ? ystr : N,
-                               h ? Z1 + sl : (y_in ? E0c + sl + NX : Y0 + lx), h ? N : ystr, m);
-            release(B_Y + 0);
-            release(B_Y + 1);
-            release(B_Z + 1);
-            // ---- S2: B U_2(x+0), C U_0(x+2) | B U_3(x+1), C U_1(x+t)
-            wait_full(B_Z + 0, ns);
+            // ---- S1: B U_3(x+0), C U_0(x+t) | B U_3(x+1), C U_1(x+t)
             wait_full(B_Y + 2, ns);
             wait_full(B_E3, ns);
-            wait_full(2 + (n & 1), n >> 1);
-            bcdag_fma<T, false>(h ? (y_in ? E3 + sl + NX : Y3 + lx) : E2c + ix_up, h ? ystr : N,
-                                h ? E(1, n) + sl : Z0 + sl, N, m);
-            release(B_Z + 0);
+            wait_full(0 + (u & 1), u >> 1);
+            wait_full(2 + (u & 1), u >> 1);
+            bcdag_fma<T, true>(h ? (y_in ? E3 + sl + NX : Y3 + lx) : E3 + ix_up, h ? ystr : N,
+                               (h ? E(1, u) : E(0, u)) + sl, N, m);
             release(B_Y + 2);
-            // lanes 16-31: M_1 is complete, M_2 starts from zero
+            release(B_E3);
+            release(0 + (u & 1));
+            release(2 + (u & 1));
+            // lanes 16-31: M_1 waits in m1, M_2 starts from zero
 #pragma unroll
             for (int q = 0; q < 18; ++q) {
                 m1[q] = m[q];
                 m[q] = h ? T(0) : m[q];
             }
-            // ---- S3: B U_3(x+0), C U_0(x+t) | B U_3(x+2), C U_2(x+t)
+            // ---- S2: B U_1(x+0), C U_0(x+1) | B U_3(x+2), C U_2(x+t)
+            wait_full(0 + (c & 1), c >> 1);
+            wait_full(2 + (c & 1), c >> 1);
+            wait_full(B_Y + 0, ns);
             wait_full(B_Z + 2, ns);
-            wait_full(0 + (n & 1), n >> 1);
-            wait_full(4 + (n & 1), n >> 1);
-            bcdag_fma<T, false>(h ? Z3 + sl : E3 + ix_up, N, (h ? E(2, n) : E(0, n)) + sl, N, m);
-            release(B_E3);
+            wait_full(4 + (u & 1), u >> 1);
+            bcdag_fma<T, false>(h ? Z3 + sl : E1c + ix_up, N,
+                                h ? E(2, u) + sl : (y_in ? E0c + sl + NX : Y0 + lx), h ? N : ystr, m);
+            release(B_Y + 0);
             release(B_Z + 2);
-            // ---- S4: acc = U_0(x) M_0 | acc = U_1(x) M_1
+            release(4 + (u & 1));
+            // lanes 16-31: M_2 is complete, back to M_1
 #pragma unroll
-            for (int q = 0; q < 18; ++q) m1[q] = h ? m1[q] : m[q];
-            am_fma<T, true>((h ? E1c : E0c) + sl, N, m1, acc);
-            release(0 + (c & 1));
-            release(2 + (c & 1));
+            for (int q = 0; q < 18; ++q) {
+                const T t2 = m[q];
+                m[q] = h ? m1[q] : t2;
+                m1[q] = t2;
+            }
+            // ---- S3: B U_2(x+0), C U_0(x+2) | B U_2(x+1), C U_1(x+2)
+            wait_full(4 + (c & 1), c >> 1);
+            wait_full(B_Z + 0, ns);
+            wait_full(B_Y + 1, ns);
+            wait_full(B_Z + 1, ns);
+            bcdag_fma<T, false>(h ? (y_in ? E2c + sl + NX : Y2 + lx) : E2c + ix_up, h ? ystr : N,
+                                (h ? Z1 : Z0) + sl, N, m);
+            release(B_Z + 0);
+            release(B_Y + 1);
+            release(B_Z + 1);
+            // ---- S4: acc = U_0(x) M_0 | acc = U_1(x) M_1
+            am_fma<T, true>((h ? E1c : E0c) + sl, N, m, acc);
             // ---- S5: lanes 16-31 acc += U_2(x) M_2
-            if (h) am_fma<T, false>(E2c + sl, N, m, acc);
-            release(4 + (c & 1));
+            if (h) am_fma<T, false>(E2c + sl, N, m1, acc);
             ++ne;
             // ---- the two half-sums meet: lanes 0-15 store elements 0..8, lanes 16-31 elements 9..17
             T* o = acc_out + int64_t(t) * 18 * p.F + s3;
@@ -831,7 +839,7 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
                 __stcs(o + (9 * h + k) * p.F, s * (mine + got));
             }
         }
-        // slice t1 (only the last step's t-planes read it)
+        // slice t0 stays resident for a next step that the item does not have
         for (int k = 0; k < 3; ++k) release(2 * k + (ne & 1));
         ++ne;
     }
