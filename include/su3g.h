@@ -63,7 +63,10 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "nn_ring_cfg":  f32 ring-walk slot / CTA configuration for A/B (0 = default)
  *   "link_variant": 0 auto, 1 rows gather, 3 row-split carried t-walk, 4 two-lane pair walk (FMA mode),
  *                   5 factored two-lane pair walk (FMA mode, nine products per site)
- *   "link_pair_prefetch": -1 auto (f32), 0 / 1: L2 prefetch one step ahead in the pair walk
+ *   "link_pair_prefetch": -1 auto (the plane-by-plane pair walk at f32 only), 0 / 1: L2 prefetch one step
+ *                   ahead in the pair walks
+ *   "link_chunk":   t-chunk length of the pair walks' work items (0 = auto, balances the wave)
+ *   "link_zdown":   0 / 1: the factored pair walk visits z-planes downwards (A/B; no measured effect)
  *   "dslash_eo_variant": 0 auto, 1 gather kernel, 2 half-lattice ring walk (nx in {32, 64}, even ny, nz)
  *   "dslash_eo_ring_cfg": slot / CTA configuration of that ring walk for A/B (0 = default)
  *   "nn_tma_chunk": t-chunk length of the TMA walk's work items (0 = auto, balances the wave)
