@@ -53,7 +53,9 @@ struct WalkParams {
     int64_t nblocks;
     int chunk;
     int64_t nitems;
-    int zdown;  // k_link_fact: block z-planes in descending order
+    int zdown;       // k_link_fact: block z-planes in descending order
+    int64_t n_full;  // the first n_full items are whole t-columns of blocks 0..n_full-1; the other
+                     // blocks are cut into t-chunks of `chunk` slices, chunk-major (n_full = 0: all of them)
 };
 
 template <int NX, int BY>
@@ -74,8 +76,15 @@ struct WalkGeo {
 };
 
 __device__ __forceinline__ void walk_item(const WalkParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
-    const int64_t ch = item / p.nblocks;
-    blk = item - ch * p.nblocks;
+    if (item < p.n_full) {
+        blk = item;
+        t0 = 0;
+        t1 = p.nt;
+        return;
+    }
+    const int64_t r = item - p.n_full, nbt = p.nblocks - p.n_full;
+    const int64_t ch = r / nbt;
+    blk = p.n_full + (r - ch * nbt);
     t0 = static_cast<int>(ch) * p.chunk;
     t1 = min(t0 + p.chunk, p.nt);
 }
@@ -891,15 +900,38 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, smem);
     const int Gfull = di.num_sms * std::max(per_sm, 1);
-    p.chunk = pick_chunk(p.nblocks, nt, Gfull, 0.5);  // an item of L slices loads L+1 E slices
+    // an item of L slices loads L+1 E slices: prologue = 0.5 step
+    p.chunk = pick_chunk(p.nblocks, nt, Gfull, 0.5);
+    double cost_uniform;
+    {
+        const int64_t items = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
+        cost_uniform = double((items + Gfull - 1) / Gfull) * (p.chunk + 0.5);
+    }
+    // columns schedule: whole rounds of Gfull blocks walk all of t as one item each (one prologue
+    // per column, and no slice above a chunk is read twice), the remaining blocks are cut into
+    // t-chunks that fill one more round
+    const int64_t n_full = (p.nblocks / Gfull) * Gfull, nbt = p.nblocks - n_full;
+    if (FACT && g_link_chunk == 0 && n_full > 0) {
+        int Lt = 0;
+        double cost_cols = double(n_full / Gfull) * (nt + 0.5);
+        if (nbt > 0) {
+            Lt = pick_chunk(nbt, nt, Gfull, 0.5);
+            const int64_t items_t = nbt * ((nt + Lt - 1) / Lt);
+            cost_cols += double((items_t + Gfull - 1) / Gfull) * (Lt + 0.5);
+        }
+        if (cost_cols < cost_uniform) {
+            p.n_full = n_full;
+            p.chunk = nbt > 0 ? Lt : nt;
+        }
+    }
     if (g_link_chunk > 0) p.chunk = std::min(g_link_chunk, nt);
     p.zdown = g_link_zdown;
-    p.nitems = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
+    p.nitems = p.n_full + (p.nblocks - p.n_full) * ((nt + p.chunk - 1) / p.chunk);
     const int grid = static_cast<int>(std::min<int64_t>(Gfull, p.nitems));
     kern<<<grid, G::THREADS, smem, st>>>(mB, mY, acc, p, s);
     note_kernel(std::string(FACT ? "k_link_fact<" : "k_link_pair<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
                 std::to_string(BY) + "x1" + (pf ? ",L2 prefetch" : "") + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
-                ",chunk " + std::to_string(p.chunk) + ">");
+                (p.n_full ? "," + std::to_string(p.n_full) + " columns" : "") + ",chunk " + std::to_string(p.chunk) + ">");
     return check_launch(FACT ? "link_product(fact)" : "link_product(pair)");
 }
 

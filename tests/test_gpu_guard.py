@@ -226,7 +226,7 @@ def test_link_product_guarded(dt, dims, variant):
 
 
 @pytest.mark.parametrize("variant", [4, 5], ids=["pair", "factored"])
-@pytest.mark.parametrize("dims", [(48, 6, 5, 7), (32, 8, 4, 6), (48, 3, 2, 3)])
+@pytest.mark.parametrize("dims", [(48, 6, 5, 7), (32, 8, 4, 6), (48, 3, 2, 3), (48, 48, 20, 2)])
 def test_link_pair_fma_guarded(dt, dims, variant):
     """the FMA-only pair kernels: guards intact, result within tolerance (a NaN read would not be)"""
     from oracle.compare import floored_rel_err

@@ -342,7 +342,8 @@ def test_link_product_bitwise(dims, precision, variant):
 
 
 @pytest.mark.parametrize(
-    "dims", [(48, 3, 2, 3), (48, 6, 5, 7), (32, 8, 4, 6), (64, 4, 3, 5), (32, 4, 1, 2), (48, 48, 3, 4)]
+    "dims", [(48, 3, 2, 3), (48, 6, 5, 7), (32, 8, 4, 6), (64, 4, 3, 5), (32, 4, 1, 2), (48, 48, 3, 4),
+             (48, 48, 20, 3)]  # the last: more blocks than CTAs, so the factored walk's columns schedule runs
 )
 @pytest.mark.parametrize("variant,kernel", [(4, "k_link_pair<"), (5, "k_link_fact<")], ids=["pair", "factored"])
 def test_link_pair_walk(dims, precision, variant, kernel):
@@ -359,6 +360,8 @@ def test_link_pair_walk(dims, precision, variant, kernel):
     try:
         got = sweeps.link_product_aos(U, dims, 1 / 6, mode="fma")
         assert _lib.last_kernel().startswith(kernel), _lib.last_kernel()
+        if variant == 5 and dims == (48, 48, 20, 3):
+            assert "columns" in _lib.last_kernel(), _lib.last_kernel()
         assert floored_rel_err(got, want) <= (1e-5 if dt == np.float32 else 1e-12)
         with pytest.raises(ValueError, match="FMA mode only"):
             sweeps.link_product_aos(U, dims, 1 / 6)
