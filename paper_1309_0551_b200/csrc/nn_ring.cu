@@ -34,6 +34,8 @@
 
 namespace su3g {
 
+int g_ring_columns = 1;  // su3g_set_option("nn_ring_columns"): the columns schedule of the work items (A/B)
+
 namespace {
 
 struct RingParams {
@@ -44,6 +46,8 @@ struct RingParams {
     int t_begin, t_end;
     int chunk;       // t-chunk length of one work item
     int64_t nitems;  // nblocks * ceil((t_end - t_begin) / chunk), chunk-major; EDGES: nblocks * (boundary slices)
+    int64_t n_full;  // columns schedule: the first n_full items are whole [t_begin, t_end) columns of blocks
+                     // 0..n_full-1, the other blocks are cut into t-chunks, chunk-major (0: every block is)
     int has_vhi;
     void* w_next;    // EDGES: w = U_t^dag out on slice nt-1 (the next application's halo), or null
 };
@@ -73,12 +77,21 @@ struct RingX {
 
 template <bool EDGES = false>
 __device__ __forceinline__ void item_of(const RingParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
-    const int64_t ch = item / p.nblocks;
-    blk = item - ch * p.nblocks;
     if constexpr (EDGES) {  // the boundary slices of a t-slab: t = 0 for every block, then t = nt - 1
+        const int64_t ch = item / p.nblocks;
+        blk = item - ch * p.nblocks;
         t0 = ch == 0 ? 0 : p.nt - 1;
         t1 = t0 + 1;
     } else {
+        if (item < p.n_full) {
+            blk = item;
+            t0 = p.t_begin;
+            t1 = p.t_end;
+            return;
+        }
+        const int64_t r = item - p.n_full, nbt = p.nblocks - p.n_full;
+        const int64_t ch = r / nbt;
+        blk = p.n_full + (r - ch * nbt);
         t0 = p.t_begin + static_cast<int>(ch) * p.chunk;
         t1 = min(t0 + p.chunk, p.t_end);
     }
@@ -375,7 +388,28 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     // A/B of the chunk picker's cost (profiles/r02/ab_nn_ring_prologue.txt): 32^4 f32 0.799 / f64 0.754
     // at 0.5 against 0.785 / 0.724 at the walk kernels' 2.0; 64^3x16 and 64^3x128 unchanged
     p.chunk = pick_chunk(p.nblocks, L, G_full, 0.5);
-    p.nitems = p.nblocks * ((L + p.chunk - 1) / p.chunk);
+    // columns schedule (as k_link_fact, link_walk.cu): whole rounds of G_full blocks walk [t_begin, t_end)
+    // as one item each (one prologue per column), the remaining blocks fill the last rounds with t-chunks.
+    // Only with the full grid (no SMs reserved for NCCL: the round structure depends on the grid).
+    if (!EDGES && g_ring_columns && sm_reserve() == 0) {
+        const int64_t n_full = (p.nblocks / G_full) * G_full, nbt = p.nblocks - n_full;
+        if (n_full > 0) {
+            const int64_t items_u = p.nblocks * ((L + p.chunk - 1) / p.chunk);
+            const double cost_uniform = double((items_u + G_full - 1) / G_full) * (p.chunk + 0.5);
+            double cost_cols = double(n_full / G_full) * (L + 0.5);
+            int Lt = L;
+            if (nbt > 0) {
+                Lt = pick_chunk(nbt, L, G_full, 0.5);
+                const int64_t items_t = nbt * ((L + Lt - 1) / Lt);
+                cost_cols += double((items_t + G_full - 1) / G_full) * (Lt + 0.5);
+            }
+            if (cost_cols < cost_uniform) {
+                p.n_full = n_full;
+                p.chunk = Lt;
+            }
+        }
+    }
+    p.nitems = p.n_full + (p.nblocks - p.n_full) * ((L + p.chunk - 1) / p.chunk);
     p.w_next = w_next;
     if constexpr (EDGES) p.nitems = p.nblocks * (nt > 1 ? 2 : 1);
     int Gr = G_full;
@@ -389,7 +423,7 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     kern<<<grid, G::N + 32, smem, st>>>(mU, mV, mVhi, mUy, mUz, mVy, mVz, U, v, out, w_lo, p);
     note_kernel(std::string("k_nn_ring<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x2x2," +
                 std::to_string(S) + " slots" + (DB ? ",1 barrier" : "") + (per > 1 ? "," + std::to_string(per) + " CTAs/SM" : "") +
-                (EDGES ? ",edges" : "") + ">" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
+                (EDGES ? ",edges" : "") + (p.n_full ? "," + std::to_string(p.n_full) + " columns" : "") + ">" + (grid < G_full ? " grid " + std::to_string(grid) : std::string()));
     return check_launch("nn_sweep(ring)");
 }
 

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256)
 
 extern int g_pair_prefetch;
 extern int g_link_chunk;
+extern int g_ring_columns;
 extern int g_link_zdown;
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
 static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 3 row-split carried t-walk, 4 two-lane pair walk (FMA)
@@ -381,6 +382,11 @@ int su3g_set_option(const char* name, int64_t value) {
     if (std::strcmp(name, "link_chunk") == 0) {
         if (value < 0 || value > 4096) return fail_invalid("set_option: link_chunk must be in [0, 4096] (0 = auto)");
         g_link_chunk = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "nn_ring_columns") == 0) {
+        if (value < 0 || value > 1) return fail_invalid("set_option: nn_ring_columns must be 0 or 1");
+        g_ring_columns = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_zdown") == 0) {

@@ -428,6 +428,31 @@ def test_nn_tma_multi_item_schedules(dims, precision):
             _lib.set_option("nn_variant", 0)
 
 
+@pytest.mark.parametrize("dims", [(64, 36, 36, 3), (32, 52, 48, 2), (48, 36, 36, 3)])
+def test_nn_ring_columns_schedule(dims, precision):
+    """More blocks than resident CTAs: the ring walk's columns schedule (whole t-columns for full rounds
+    of blocks, t-chunks for the rest) and the uniform chunk-major schedule both match the oracle bit for bit."""
+    from paper_1309_0551_b200 import _lib
+
+    dt = _dt(precision)
+    V = int(np.prod(dims))
+    rng = inputs.config_rng(9100 + V)
+    U = inputs.random_links(rng, V, 4, dtype=dt)
+    v = inputs.random_vectors(rng, V, None, dtype=dt)
+    want = coracle.nn_sweep(U, v, dims)
+    _lib.set_option("nn_variant", 4)
+    try:
+        for columns in (1, 0):
+            _lib.set_option("nn_ring_columns", columns)
+            got = sweeps.nn_sweep_aos(U, v, dims)
+            assert ("columns" in _lib.last_kernel()) == bool(columns), _lib.last_kernel()
+            bad = np.argwhere(np.any(got != want, axis=(1, 2)))
+            assert bad.size == 0, f"columns {columns}: {bad.size} wrong sites, first {bad[:5].ravel()} ({_lib.last_kernel()})"
+    finally:
+        _lib.set_option("nn_ring_columns", 1)
+        _lib.set_option("nn_variant", 0)
+
+
 @pytest.mark.parametrize("threads", [128, 256])
 @pytest.mark.parametrize("dims", [(32, 8, 8, 12), (32, 32, 32, 4)])
 def test_nn_tma_block_sizes(threads, dims):
