@@ -745,8 +745,15 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
         uint32_t ne = 0, ns = 0;  // slices loaded (buffer ne & 1); steps issued (halo slot uses)
         auto begin = [&](int bar, uint32_t use, int reals) {
             if (use) mbar_wait(&empty[bar], (use - 1) & 1);
+#ifdef FACT_NOLOAD  // floor build: the slots are never filled, the barriers complete at once (compute only)
+            mbar_arrive(&full[bar]);
+#else
             mbar_arrive_expect_tx(&full[bar], reals * sizeof(T));
+#endif
         };
+#ifdef FACT_NOLOAD
+#define tma_load_4d(...) ((void)0)
+#endif
         auto Ew = [&](int k, uint32_t slice_no) { return sm + G::OFF_E + (2 * k + (slice_no & 1)) * G::BLK; };
         for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
             int64_t blk;
@@ -792,6 +799,9 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
             }
         }
         return;
+#ifdef FACT_NOLOAD
+#undef tma_load_4d
+#endif
     }
 
     // ------------------------------------------------------------------ compute warps
@@ -813,22 +823,32 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
     auto wait_full = [&](int bar, uint32_t use) { mbar_wait(&full[bar], use & 1); };
     auto E = [&](int k, uint32_t slice_no) { return sm + G::OFF_E + (2 * k + (slice_no & 1)) * G::BLK; };
 
+    // a barrier is polled once, early (before the arithmetic of the operand in front of it), and
+    // waited on only if that poll failed: the poll's latency hides behind the FMAs
+    auto test_full = [&](int bar, uint32_t use) { return mbar_test(&full[bar], use & 1); };
+    auto wait_if = [&](uint32_t done, int bar, uint32_t use) {
+        if (!done) mbar_wait(&full[bar], use & 1);
+    };
     uint32_t ne = 0, ns = 0;
     for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
         int64_t blk;
         int t0, t1;
         walk_item(p, item, blk, t0, t1);
         const int y = static_cast<int>(blk % p.nby) * BY + ly;
-        const int z = static_cast<int>(blk / p.nby);
+        const int zq = static_cast<int>(blk / p.nby);
+        const int z = p.zdown ? p.nz - 1 - zq : zq;
         const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
+        // the slice above the item: the only step whose U_mu(x+t) buffers were not waited on as own links
+        wait_full(B_E01 + (ne & 1), ne >> 1);
+        wait_full(B_E2 + (ne & 1), ne >> 1);
+        uint32_t okA = test_full(B_A, ns);
         for (int t = t1 - 1; t >= t0; --t, ++ns) {
             const uint32_t u = ne, c = ne + 1;  // slice loads of t+1 (resident since the previous step) and t
             const T *E0c = E(0, c), *E1c = E(1, c), *E2c = E(2, c);
             T m[18], m2[18], acc[18];
             // ---- S1: B U_3(x+0), C U_0(x+t) | B U_3(x+2), C U_2(x+t)   (M_0 | M_2)
-            wait_full(B_A, ns);
-            wait_full(B_E01 + (u & 1), u >> 1);
-            wait_full(B_E2 + (u & 1), u >> 1);
+            wait_if(okA, B_A, ns);
+            const uint32_t okB = test_full(B_B, ns), okD = test_full(B_E01 + (c & 1), c >> 1);
             bcdag_fma<T, true>(h ? Z3 + sl : E3 + ix_up, N, (h ? E(2, u) : E(0, u)) + sl, N, m);
             release(B_E2 + (u & 1));
             // lanes 16-31: M_2 is complete, M_1 starts from zero
@@ -838,19 +858,21 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
                 m[q] = h ? T(0) : m[q];
             }
             // ---- S2: B U_1(x+0), C U_0(x+1) | B U_3(x+1), C U_1(x+t)   (M_0 | M_1)
-            wait_full(B_B, ns);
-            wait_full(B_E01 + (c & 1), c >> 1);
+            wait_if(okB, B_B, ns);
+            wait_if(okD, B_E01 + (c & 1), c >> 1);
+            const uint32_t okC = test_full(B_C, ns), okE = test_full(B_E2 + (c & 1), c >> 1);
             bcdag_fma<T, false>(h ? (y_in ? E3 + sl + NX : Y3 + lx) : E1c + ix_up, h ? ystr : N,
                                 h ? E(1, u) + sl : (y_in ? E0c + sl + NX : Y0 + lx), h ? N : ystr, m);
             release(B_A);
             release(B_B);
             release(B_E01 + (u & 1));
             // ---- S3: B U_2(x+0), C U_0(x+2) | B U_2(x+1), C U_1(x+2)   (M_0 | M_1)
-            wait_full(B_C, ns);
-            wait_full(B_E2 + (c & 1), c >> 1);
+            wait_if(okC, B_C, ns);
+            wait_if(okE, B_E2 + (c & 1), c >> 1);
             bcdag_fma<T, false>(h ? (y_in ? E2c + sl + NX : Y2 + lx) : E2c + ix_up, h ? ystr : N,
                                 (h ? Z1 : Z0) + sl, N, m);
             release(B_C);
+            if (t > t0) okA = test_full(B_A, ns + 1);  // the next step's first operands
             // ---- S4: acc = U_0(x) M_0 | acc = U_1(x) M_1
             am_fma<T, true>((h ? E1c : E0c) + sl, N, m, acc);
             // ---- S5: lanes 16-31 acc += U_2(x) M_2
