@@ -65,7 +65,8 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *                   5 factored two-lane pair walk (FMA mode, nine products per site)
  *   "link_pair_prefetch": -1 auto (the plane-by-plane pair walk at f32 only), 0 / 1: L2 prefetch one step
  *                   ahead in the pair walks
- *   "nn_ring_columns": 0 / 1: the ring walk's columns schedule (whole t-columns for full rounds of blocks; default 1)
+ *   "nn_ring_columns": 0 / 1: the ring walks' (NN sweep, checkerboarded dslash) columns schedule: whole t-columns
+ *                   for full rounds of blocks, t-chunks for the rest (default 1)
  *   "link_chunk":   t-chunk length of the pair walks' work items (0 = auto, balances the wave)
  *   "link_zdown":   0 / 1: the factored pair walk visits z-planes downwards (A/B; no measured effect)
  *   "dslash_eo_variant": 0 auto, 1 gather kernel, 2 half-lattice ring walk (nx in {32, 64}, even ny, nz)

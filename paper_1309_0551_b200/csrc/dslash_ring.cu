@@ -39,6 +39,7 @@ struct DParams {
     int64_t nblocks;
     int chunk;
     int64_t nitems;
+    int64_t n_full;  // columns schedule (sweep_common.cuh)
     int parity;
 };
 
@@ -79,10 +80,7 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, i
 }
 
 __device__ __forceinline__ void ditem(const DParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
-    const int64_t ch = item / p.nblocks;
-    blk = item - ch * p.nblocks;
-    t0 = static_cast<int>(ch) * p.chunk;
-    t1 = min(t0 + p.chunk, p.nt);
+    schedule_item(p.n_full, p.nblocks, p.chunk, 0, p.nt, item, blk, t0, t1);
 }
 
 }  // namespace
@@ -352,12 +350,15 @@ static int run_dslash_ring(const T* U, const T* v, T* out, int nx, int ny, int n
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::N + 32, smem);
     const int per = std::max(per_sm, 1);
     const int G_full = di.num_sms * per;
-    p.chunk = pick_chunk(p.nblocks, nt, G_full);
-    p.nitems = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
+    const WalkSchedule ws = pick_schedule(p.nblocks, nt, G_full, g_prologue_cost, g_ring_columns != 0);
+    p.n_full = ws.n_full;
+    p.chunk = ws.chunk;
+    p.nitems = ws.nitems;
     const int grid = static_cast<int>(std::min<int64_t>(G_full, p.nitems));
     kern<<<grid, G::N + 32, smem, st>>>(mU, mV, mUy, mUz, mVy, mVz, U, v, out, p);
     note_kernel(std::string("k_dslash_ring<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NXH) + "x2x2," +
-                std::to_string(S) + " slots" + (per > 1 ? "," + std::to_string(per) + " CTAs/SM" : "") + ">");
+                std::to_string(S) + " slots" + (per > 1 ? "," + std::to_string(per) + " CTAs/SM" : "") +
+                (p.n_full ? "," + std::to_string(p.n_full) + " columns" : "") + ">");
     return check_launch("dslash_eo(ring)");
 }
 

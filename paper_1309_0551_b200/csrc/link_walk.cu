@@ -76,17 +76,7 @@ struct WalkGeo {
 };
 
 __device__ __forceinline__ void walk_item(const WalkParams& p, int64_t item, int64_t& blk, int& t0, int& t1) {
-    if (item < p.n_full) {
-        blk = item;
-        t0 = 0;
-        t1 = p.nt;
-        return;
-    }
-    const int64_t r = item - p.n_full, nbt = p.nblocks - p.n_full;
-    const int64_t ch = r / nbt;
-    blk = p.n_full + (r - ch * nbt);
-    t0 = static_cast<int>(ch) * p.chunk;
-    t1 = min(t0 + p.chunk, p.nt);
+    schedule_item(p.n_full, p.nblocks, p.chunk, 0, p.nt, item, blk, t0, t1);
 }
 
 // row r of T = A B: a = row r of A (6 reals), B element (j, k) at bs[((3j+k)*2+q) * bstr]
@@ -922,30 +912,11 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, smem);
     const int Gfull = di.num_sms * std::max(per_sm, 1);
-    // an item of L slices loads L+1 E slices: prologue = 0.5 step
-    p.chunk = pick_chunk(p.nblocks, nt, Gfull, 0.5);
-    double cost_uniform;
-    {
-        const int64_t items = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
-        cost_uniform = double((items + Gfull - 1) / Gfull) * (p.chunk + 0.5);
-    }
-    // columns schedule: whole rounds of Gfull blocks walk all of t as one item each (one prologue
-    // per column, and no slice above a chunk is read twice), the remaining blocks are cut into
-    // t-chunks that fill one more round
-    const int64_t n_full = (p.nblocks / Gfull) * Gfull, nbt = p.nblocks - n_full;
-    if (FACT && g_link_chunk == 0 && n_full > 0) {
-        int Lt = 0;
-        double cost_cols = double(n_full / Gfull) * (nt + 0.5);
-        if (nbt > 0) {
-            Lt = pick_chunk(nbt, nt, Gfull, 0.5);
-            const int64_t items_t = nbt * ((nt + Lt - 1) / Lt);
-            cost_cols += double((items_t + Gfull - 1) / Gfull) * (Lt + 0.5);
-        }
-        if (cost_cols < cost_uniform) {
-            p.n_full = n_full;
-            p.chunk = nbt > 0 ? Lt : nt;
-        }
-    }
+    // an item of L slices loads L+1 E slices: prologue = 0.5 step; the columns schedule (sweep_common.cuh)
+    // for the factored walk unless a chunk length is forced
+    const WalkSchedule ws = pick_schedule(p.nblocks, nt, Gfull, 0.5, FACT && g_link_chunk == 0);
+    p.n_full = ws.n_full;
+    p.chunk = ws.chunk;
     if (g_link_chunk > 0) p.chunk = std::min(g_link_chunk, nt);
     p.zdown = g_link_zdown;
     p.nitems = p.n_full + (p.nblocks - p.n_full) * ((nt + p.chunk - 1) / p.chunk);

@@ -34,7 +34,7 @@
 
 namespace su3g {
 
-int g_ring_columns = 1;  // su3g_set_option("nn_ring_columns"): the columns schedule of the work items (A/B)
+int g_ring_columns = 1;  // su3g_set_option("nn_ring_columns"): the columns schedule of the ring walks' work items (A/B)
 
 namespace {
 
@@ -83,17 +83,7 @@ __device__ __forceinline__ void item_of(const RingParams& p, int64_t item, int64
         t0 = ch == 0 ? 0 : p.nt - 1;
         t1 = t0 + 1;
     } else {
-        if (item < p.n_full) {
-            blk = item;
-            t0 = p.t_begin;
-            t1 = p.t_end;
-            return;
-        }
-        const int64_t r = item - p.n_full, nbt = p.nblocks - p.n_full;
-        const int64_t ch = r / nbt;
-        blk = p.n_full + (r - ch * nbt);
-        t0 = p.t_begin + static_cast<int>(ch) * p.chunk;
-        t1 = min(t0 + p.chunk, p.t_end);
+        schedule_item(p.n_full, p.nblocks, p.chunk, p.t_begin, p.t_end, item, blk, t0, t1);
     }
 }
 
@@ -387,29 +377,12 @@ static int run_ring(const T* U, const T* v, T* out, int nx, int ny, int nz, int 
     // a ring work item's prologue (v(t0) and w_t(t0-1) from global) costs about half a step: same-box
     // A/B of the chunk picker's cost (profiles/r02/ab_nn_ring_prologue.txt): 32^4 f32 0.799 / f64 0.754
     // at 0.5 against 0.785 / 0.724 at the walk kernels' 2.0; 64^3x16 and 64^3x128 unchanged
-    p.chunk = pick_chunk(p.nblocks, L, G_full, 0.5);
-    // columns schedule (as k_link_fact, link_walk.cu): whole rounds of G_full blocks walk [t_begin, t_end)
-    // as one item each (one prologue per column), the remaining blocks fill the last rounds with t-chunks.
-    // Only with the full grid (no SMs reserved for NCCL: the round structure depends on the grid).
-    if (!EDGES && g_ring_columns && sm_reserve() == 0) {
-        const int64_t n_full = (p.nblocks / G_full) * G_full, nbt = p.nblocks - n_full;
-        if (n_full > 0) {
-            const int64_t items_u = p.nblocks * ((L + p.chunk - 1) / p.chunk);
-            const double cost_uniform = double((items_u + G_full - 1) / G_full) * (p.chunk + 0.5);
-            double cost_cols = double(n_full / G_full) * (L + 0.5);
-            int Lt = L;
-            if (nbt > 0) {
-                Lt = pick_chunk(nbt, L, G_full, 0.5);
-                const int64_t items_t = nbt * ((L + Lt - 1) / Lt);
-                cost_cols += double((items_t + G_full - 1) / G_full) * (Lt + 0.5);
-            }
-            if (cost_cols < cost_uniform) {
-                p.n_full = n_full;
-                p.chunk = Lt;
-            }
-        }
-    }
-    p.nitems = p.n_full + (p.nblocks - p.n_full) * ((L + p.chunk - 1) / p.chunk);
+    // columns schedule (sweep_common.cuh): only with the full grid (no SMs reserved for NCCL: the round
+    // structure depends on the grid)
+    const WalkSchedule ws = pick_schedule(p.nblocks, L, G_full, 0.5, !EDGES && g_ring_columns && sm_reserve() == 0);
+    p.n_full = ws.n_full;
+    p.chunk = ws.chunk;
+    p.nitems = ws.nitems;
     p.w_next = w_next;
     if constexpr (EDGES) p.nitems = p.nblocks * (nt > 1 ? 2 : 1);
     int Gr = G_full;

@@ -63,6 +63,57 @@ inline int pick_chunk(int64_t nblocks, int nt_range, int G, double prologue = -1
 }
 
 
+// Work-item schedule of the persistent t-walks (ring NN sweep, checkerboarded dslash, factored link
+// product).  A walk's items are (block, t-range); an item's prologue costs `prologue` steps and re-reads a
+// slice.  Uniform: every block is cut into t-chunks of `chunk`, items chunk-major.  Columns: whole rounds
+// of G blocks walk all L slices as one item each (the first n_full items), the remaining blocks are cut
+// into t-chunks, chunk-major, and fill the last round(s).  The cheaper of the two by the round count.
+struct WalkSchedule {
+    int64_t n_full;  // leading whole-column items (0: uniform)
+    int chunk;       // t-chunk length of the other blocks' items
+    int64_t nitems;
+};
+
+inline WalkSchedule pick_schedule(int64_t nblocks, int L, int G, double prologue, bool columns) {
+    WalkSchedule w{0, pick_chunk(nblocks, L, G, prologue), 0};
+    const int64_t n_full = (nblocks / G) * G, nbt = nblocks - n_full;
+    if (columns && n_full > 0) {
+        const int64_t items_u = nblocks * ((L + w.chunk - 1) / w.chunk);
+        const double cost_uniform = double((items_u + G - 1) / G) * (w.chunk + prologue);
+        double cost_cols = double(n_full / G) * (L + prologue);
+        int Lt = L;
+        if (nbt > 0) {
+            Lt = pick_chunk(nbt, L, G, prologue);
+            const int64_t items_t = nbt * ((L + Lt - 1) / Lt);
+            cost_cols += double((items_t + G - 1) / G) * (Lt + prologue);
+        }
+        if (cost_cols < cost_uniform) {
+            w.n_full = n_full;
+            w.chunk = Lt;
+        }
+    }
+    w.nitems = w.n_full + (nblocks - w.n_full) * ((L + w.chunk - 1) / w.chunk);
+    return w;
+}
+
+// item -> (block, [t0, t1)) of a schedule over slices [lo, hi)
+__device__ __forceinline__ void schedule_item(int64_t n_full, int64_t nblocks, int chunk, int lo, int hi, int64_t item,
+                                              int64_t& blk, int& t0, int& t1) {
+    if (item < n_full) {
+        blk = item;
+        t0 = lo;
+        t1 = hi;
+        return;
+    }
+    const int64_t r = item - n_full, nbt = nblocks - n_full;
+    const int64_t ch = r / nbt;
+    blk = n_full + (r - ch * nbt);
+    t0 = lo + static_cast<int>(ch) * chunk;
+    t1 = min(t0 + chunk, hi);
+}
+
+extern int g_ring_columns;  // su3g_set_option("nn_ring_columns"): the columns schedule of the ring walks (A/B)
+
 // TMA-staged t-walk NN sweep (nn_tma.cu); returns SU3G_EINVAL-style status, or
 // 1 when the lattice does not meet its constraints (caller falls back).
 template <typename T>
