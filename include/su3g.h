@@ -67,6 +67,8 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *                   ahead in the pair walks
  *   "nn_ring_columns": 0 / 1: the ring walks' (NN sweep, checkerboarded dslash) columns schedule: whole t-columns
  *                   for full rounds of blocks, t-chunks for the rest (default 1)
+ *   "link_rows_cfg": f64 rows-gather register budget / gather order for A/B: 0 default, 1 three CTAs/SM with C
+ *                   gathered early, 2 four with early C, 3 three, 4 two with early C (all within 2%)
  *   "link_chunk":   t-chunk length of the pair walks' work items (0 = auto, balances the wave)
  *   "link_zdown":   0 / 1: the factored pair walk visits z-planes downwards (A/B; no measured effect)
  *   "dslash_eo_variant": 0 auto, 1 gather kernel, 2 half-lattice ring walk (nx in {32, 64}, even ny, nz)

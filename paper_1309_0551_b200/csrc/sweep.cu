@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(256)
 
 extern int g_pair_prefetch;
 extern int g_link_chunk;
+extern int g_link_rows_cfg;
 extern int g_ring_columns;
 extern int g_link_zdown;
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
@@ -382,6 +383,11 @@ int su3g_set_option(const char* name, int64_t value) {
     if (std::strcmp(name, "link_chunk") == 0) {
         if (value < 0 || value > 4096) return fail_invalid("set_option: link_chunk must be in [0, 4096] (0 = auto)");
         g_link_chunk = static_cast<int>(value);
+        return SU3G_OK;
+    }
+    if (std::strcmp(name, "link_rows_cfg") == 0) {
+        if (value < 0 || value > 4) return fail_invalid("set_option: link_rows_cfg must be in [0, 4]");
+        g_link_rows_cfg = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "nn_ring_columns") == 0) {
