@@ -306,8 +306,8 @@ def run_b200(args, rank, world, local):
                      ("SU3G_SWEEP_L2_HINTS", "sweep_l2_hints"), ("SU3G_NN_TMA_L2_HINTS", "nn_tma_l2_hints"),
                      ("SU3G_NN_TMA_CHUNK", "nn_tma_chunk"), ("SU3G_DSLASH_EO_ZC", "dslash_eo_zc"),
                      ("SU3G_DSLASH_EO_HINTS", "dslash_eo_hints"), ("SU3G_NN_RING_CFG", "nn_ring_cfg"),
-                     ("SU3G_LINK_VARIANT", "link_variant"), ("SU3G_LINK_PAIR_PREFETCH", "link_pair_prefetch"),
-                     ("SU3G_LINK_CHUNK", "link_chunk"), ("SU3G_LINK_ROWS_CFG", "link_rows_cfg"), ("SU3G_NN_RING_COLUMNS", "nn_ring_columns"), ("SU3G_LINK_ZDOWN", "link_zdown"),
+                     ("SU3G_LINK_VARIANT", "link_variant"),
+                     ("SU3G_LINK_CHUNK", "link_chunk"), ("SU3G_NN_RING_COLUMNS", "nn_ring_columns"),
                      ("SU3G_DSLASH_EO_VARIANT", "dslash_eo_variant"), ("SU3G_DSLASH_EO_RING_CFG", "dslash_eo_ring_cfg")):
         if os.environ.get(env):
             _l.set_option(opt, int(os.environ[env]))

@@ -61,16 +61,11 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *   "nn_variant":   0 auto, 1 generic one-thread-per-site (z-chunked order), 3 TMA t-walk,
  *                   4 TMA ring walk (the default where it applies: nx in {32, 48, 64}, even ny, nz)
  *   "nn_ring_cfg":  f32 ring-walk slot / CTA configuration for A/B (0 = default)
- *   "link_variant": 0 auto, 1 rows gather, 3 row-split carried t-walk, 4 two-lane pair walk (FMA mode),
- *                   5 factored two-lane pair walk (FMA mode, nine products per site)
- *   "link_pair_prefetch": -1 auto (the plane-by-plane pair walk at f32 only), 0 / 1: L2 prefetch one step
- *                   ahead in the pair walks
+ *   "link_variant": 0 auto, 1 rows gather, 3 row-split carried t-walk, 5 factored two-lane pair walk (FMA mode,
+ *                   nine products per site; the FMA default)
  *   "nn_ring_columns": 0 / 1: the ring walks' (NN sweep, checkerboarded dslash) columns schedule: whole t-columns
  *                   for full rounds of blocks, t-chunks for the rest (default 1)
- *   "link_rows_cfg": f64 rows-gather register budget / gather order for A/B: 0 default, 1 three CTAs/SM with C
- *                   gathered early, 2 four with early C, 3 three, 4 two with early C (all within 2%)
- *   "link_chunk":   t-chunk length of the pair walks' work items (0 = auto, balances the wave)
- *   "link_zdown":   0 / 1: the factored pair walk visits z-planes downwards (A/B; no measured effect)
+ *   "link_chunk":   t-chunk length of the factored walk's work items (0 = auto: the columns schedule)
  *   "dslash_eo_variant": 0 auto, 1 gather kernel, 2 half-lattice ring walk (nx in {32, 64}, even ny, nz)
  *   "dslash_eo_ring_cfg": slot / CTA configuration of that ring walk for A/B (0 = default)
  *   "nn_tma_chunk": t-chunk length of the TMA walk's work items (0 = auto, balances the wave)

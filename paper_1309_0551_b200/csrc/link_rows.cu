@@ -119,8 +119,6 @@ __global__ void __launch_bounds__(128, MINB)
     for (int k = 0; k < 18; ++k) __stcs(acc_out + (int64_t(t) * 18 + k) * g.F + s3, acc[k * 128]);
 }
 
-int g_link_rows_cfg = 0;  // su3g_set_option("link_rows_cfg"): f64 register budget / gather order of the rows kernel (A/B)
-
 template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st) {
     const int64_t n = g.F * g.nt;
@@ -130,17 +128,11 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     // r02: dropping the per-load 64-bit site division took f64 exact 0.450 -> 0.497 (same box); a fully
     // unrolled plane loop (compile-time mu, nu) measured 0.362 (loads hoisted across planes), 5 / 6 CTAs
     // per SM (96 / 80 registers, spills) 0.430 / 0.379 against 0.480 at 4 (profiles/r02/ab_link_rows_unroll.txt)
-    if constexpr (sizeof(T) == 4) {
-        k_link_rows<T, FUSED, 6, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
-    } else {
-        switch (g_link_rows_cfg) {
-            case 1: k_link_rows<T, FUSED, 3, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-            case 2: k_link_rows<T, FUSED, 4, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-            case 3: k_link_rows<T, FUSED, 3, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-            case 4: k_link_rows<T, FUSED, 2, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC); break;
-            default: k_link_rows<T, FUSED, FUSED ? 3 : 4, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
-        }
-    }
+    // r02 last session: for f64 exact, 2 / 3 / 4 CTAs per SM with or without the early C gather all measure
+    // 0.476-0.487 (two CTAs 0.437; profiles/r02/ab_link_rows_cfg.txt): the gathers pull 2.6 KB per site through
+    // L2 (13.8 GB per 48^4 sweep, ~11.5 TB/s), which is the bound, not occupancy or the FP64 pipe
+    if constexpr (sizeof(T) == 4) k_link_rows<T, FUSED, 6, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
+    else k_link_rows<T, FUSED, FUSED ? 3 : 4, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     return check_launch("link_product(rows)");
 }
 

@@ -40,9 +40,7 @@
 
 namespace su3g {
 
-int g_pair_prefetch = -1;  // su3g_set_option("link_pair_prefetch"): L2 prefetch one step ahead in k_link_pair (-1 auto)
-int g_link_chunk = 0;      // su3g_set_option("link_chunk"): t-chunk length of the pair walks' work items (0 auto)
-int g_link_zdown = 0;      // su3g_set_option("link_zdown"): k_link_fact visits z-planes downwards (A/B)
+int g_link_chunk = 0;  // su3g_set_option("link_chunk"): t-chunk length of the factored walk's work items (0 auto)
 
 namespace {
 
@@ -53,7 +51,6 @@ struct WalkParams {
     int64_t nblocks;
     int chunk;
     int64_t nitems;
-    int zdown;       // k_link_fact: block z-planes in descending order
     int64_t n_full;  // the first n_full items are whole t-columns of blocks 0..n_full-1; the other
                      // blocks are cut into t-chunks of `chunk` slices, chunk-major (n_full = 0: all of them)
 };
@@ -346,21 +343,11 @@ static int run_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
 }
 
 // ======================================================================================
-// FMA mode: two lanes per site, three planes each (k_link_pair).
-//
-// With FMA chains the plane order is free (the north-star tolerance, not bit equality), so a site's
-// six planes split over two lanes that each own whole products, one plane per lane per phase, and
-// the two partial accumulators meet through one shuffle at the end.  Unlike the row split, each
-// lane reads a distinct operand, so shared memory delivers every staged link once per use, and a
-// warp covers 16 sites twice (lanes 0-15 | 16-31): each half-warp's 64-bit load is one slot, 128 B.
-// The t-planes read C = U_mu(x+t) from the NEXT slice's U_0..U_2, double-buffered per link, so the
-// block walk needs no carried state.  Phase p of a step (lanes 0-15 | lanes 16-31):
-//   p0  (0,2): A U_0, B U_2(x+0), C U_0(x+2) [Z0]       | (0,1): A U_0, B U_1(x+0), C U_0(x+1) [Y0]
-//   p1  (1,2): A U_1, B U_2(x+1) [Y2], C U_1(x+2) [Z1]  | (2,3): A U_2, B U_3(x+2) [Z3], C U_2(x+t)
-//   p2  (0,3): A U_0, B U_3(x+0), C U_0(x+t)            | (1,3): A U_1, B U_3(x+1) [Y3], C U_1(x+t)
-// Every halo chunk has its own slot and barrier, and the producer issues the loads in the order the
-// previous step frees their slots, so each load is in flight for at least two thirds of a step
-// before its phase: phase 0 frees Z0 / Y0, phase 1 Z1 / Z3 / Y2 / U_2, the end E3 / Y3 / U_0 / U_1.
+// FMA mode: two lanes per site (k_link_fact below).  Lanes 0-15 and 16-31 of a warp take the same 16
+// sites, each lane owns whole products, so every staged link is read once per use and a half-warp's
+// 64-bit shared load is one slot, 128 B.  (The plane-by-plane form of this walk, k_link_pair --
+// three planes per lane, twelve products per site, 0.611 of HBM at 48^4 f64 -- is in git history;
+// the factored form replaced it.)
 // ======================================================================================
 
 template <typename T, int NX, int BY>
@@ -380,216 +367,6 @@ struct PairGeo {
     static constexpr int NBAR = 13;
 };
 
-namespace {
-
-// acc (+)= s * (A B) C^dag with FMA chains; A in a[18] registers, B / C element (r, c) at ptr[((3r+c)*2+q) * str]
-template <typename T, bool FIRST>
-__device__ __forceinline__ void plane_fma(const T* a, const T* bs, int bstr, const T* cs, int cstr, T s, T* acc) {
-    T tm[18];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        T bc[6];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            bc[2 * j] = bs[((3 * j + k) * 2) * bstr];
-            bc[2 * j + 1] = bs[((3 * j + k) * 2 + 1) * bstr];
-        }
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            cdot_fma<T, PLAIN, 3>([&](int j, int q) { return a[(3 * i + j) * 2 + q]; },
-                                  [&](int j, int q) { return bc[2 * j + q]; }, tm[(3 * i + k) * 2],
-                                  tm[(3 * i + k) * 2 + 1]);
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        T cr[6];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            cr[2 * j] = cs[((3 * k + j) * 2) * cstr];
-            cr[2 * j + 1] = cs[((3 * k + j) * 2 + 1) * cstr];
-        }
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            T pr, pi;
-            cdot_fma<T, CONJ_Q, 3>([&](int j, int q) { return tm[(3 * i + j) * 2 + q]; },
-                                   [&](int j, int q) { return cr[2 * j + q]; }, pr, pi);
-            const int e = (3 * i + k) * 2;
-            acc[e] = fma(s, pr, FIRST ? T(0) : acc[e]);
-            acc[e + 1] = fma(s, pi, FIRST ? T(0) : acc[e + 1]);
-        }
-    }
-}
-
-}  // namespace
-
-template <typename T, int NX, int BY, bool PF>
-__global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
-    k_link_pair(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapY,
-                T* __restrict__ acc_out, WalkParams p, T s) {
-    using G = PairGeo<T, NX, BY>;
-    constexpr int N = G::N, NWC = G::NWC;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    T* sm = reinterpret_cast<T*>(smem_raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::TOTAL);
-    uint64_t* empty = full + G::NBAR;
-    constexpr int B_E3 = 6, B_Z = 7, B_Y = 10;  // Z: +0 U_0, +1 U_1, +2 U_3; Y: +0 U_0, +1 U_2, +2 U_3
-    const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int k = 0; k < G::NBAR; ++k) {
-            mbar_init(&full[k], 1);
-            mbar_init(&empty[k], NWC);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const int GR = gridDim.x;
-
-    if (tid >= 32 * NWC) {  // ------------------------------------------ producer warp
-        if (tid != 32 * NWC) return;
-        uint64_t pol;
-        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-        uint32_t ne = 0, ns = 0;  // slices loaded (buffer ne & 1); steps issued (E3 / Z / Y uses)
-        auto load = [&](int bar, uint32_t use, T* dst, const CUtensorMap* map, int y, int z, int plane, int reals) {
-            if (use) mbar_wait(&empty[bar], (use - 1) & 1);
-            mbar_arrive_expect_tx(&full[bar], reals * sizeof(T));
-            tma_load_4d(dst, map, 0, y, z, plane, &full[bar], pol);
-        };
-        auto load_link = [&](int k, uint32_t slice_no, int ts, int y0, int z0) {
-            const int b = slice_no & 1;
-            load(2 * k + b, slice_no >> 1, sm + G::OFF_E + (2 * k + b) * G::BLK, &mapB, y0, z0, ts * 72 + 18 * k,
-                 G::BLK);
-        };
-        for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
-            int64_t blk;
-            int t0, t1;
-            walk_item(p, item, blk, t0, t1);
-            const int y0 = static_cast<int>(blk % p.nby) * BY, z0 = static_cast<int>(blk / p.nby);
-            const int yup = (y0 + BY) % p.ny, zup = (z0 + 1) % p.nz;
-            for (int k = 0; k < 3; ++k) load_link(k, ne, t0, y0, z0);
-            ++ne;
-            for (int t = t0; t < t1; ++t, ++ns) {
-                const int tn = (t + 1 == p.nt) ? 0 : t + 1;
-                if constexpr (PF) {  // L2 warm-up one step ahead: the next step's halos and U_3, slice t+2
-                    const int tn2 = (tn + 1 == p.nt) ? 0 : tn + 1;
-                    if (t + 1 < t1) {
-                        for (int k : {0, 36, 54}) tma_prefetch(&mapY, 0, yup, z0, tn * 72 + k);
-                        for (int k : {0, 18, 54}) tma_prefetch(&mapB, 0, y0, zup, tn * 72 + k);
-                        tma_prefetch(&mapB, 0, y0, z0, tn * 72 + 54);
-                        for (int k = 0; k < 3; ++k) tma_prefetch(&mapB, 0, y0, z0, tn2 * 72 + 18 * k);
-                    }
-                }
-                // issue order = the order the previous step releases the slots, so every wait is
-                // monotone: phase 0 frees Z0 / Y0, phase 1 Z1 / Z3 / Y2 / U_2, the end E3 / Y3 / U_0 / U_1
-                load(B_Z + 0, ns, sm + G::OFF_Z, &mapB, y0, zup, t * 72, G::BLK);
-                load(B_Y + 0, ns, sm + G::OFF_Y, &mapY, yup, z0, t * 72, G::YSUB);
-                load(B_Z + 1, ns, sm + G::OFF_Z + G::BLK, &mapB, y0, zup, t * 72 + 18, G::BLK);
-                load(B_Z + 2, ns, sm + G::OFF_Z + 2 * G::BLK, &mapB, y0, zup, t * 72 + 54, G::BLK);
-                load(B_Y + 1, ns, sm + G::OFF_Y + G::YSUB, &mapY, yup, z0, t * 72 + 36, G::YSUB);
-                load_link(2, ne, tn, y0, z0);
-                load(B_E3, ns, sm + G::OFF_E3, &mapB, y0, z0, t * 72 + 54, G::BLK);
-                load(B_Y + 2, ns, sm + G::OFF_Y + 2 * G::YSUB, &mapY, yup, z0, t * 72 + 54, G::YSUB);
-                load_link(0, ne, tn, y0, z0);
-                load_link(1, ne, tn, y0, z0);
-                ++ne;
-            }
-        }
-        return;
-    }
-
-    // ------------------------------------------------------------------ compute warps
-    // a warp covers 16 consecutive sites twice: lanes 0-15 take planes (0,2) (1,2) (0,3), lanes 16-31
-    // (0,1) (2,3) (1,3), so every 64-bit shared load of a half-warp reads one slot, 16 sites, 128 B
-    const int lane = tid & 31;
-    const int sl = (tid >> 5) * 16 + (lane & 15);
-    const int h = lane >> 4;
-    const int lx = sl % NX, ly = sl / NX;
-    const int ix_up = (lx + 1 == NX) ? sl - lx : sl + 1;
-    const bool y_in = ly + 1 < BY;
-    const int ystr = y_in ? N : NX;
-    const T* const E3 = sm + G::OFF_E3;
-    const T* const Z0 = sm + G::OFF_Z;
-    const T* const Z1 = Z0 + G::BLK;
-    const T* const Z3 = Z1 + G::BLK;
-    const T* const Y0 = sm + G::OFF_Y;
-    const T* const Y2 = Y0 + G::YSUB;
-    const T* const Y3 = Y2 + G::YSUB;
-    auto release = [&](int bar) { warp_release(&empty[bar], lane); };
-    auto wait_full = [&](int bar, uint32_t use) { mbar_wait(&full[bar], use & 1); };
-    auto E = [&](int k, uint32_t slice_no) { return sm + G::OFF_E + (2 * k + (slice_no & 1)) * G::BLK; };
-
-    uint32_t ne = 0, ns = 0;
-    for (int64_t item = blockIdx.x; item < p.nitems; item += GR) {
-        int64_t blk;
-        int t0, t1;
-        walk_item(p, item, blk, t0, t1);
-        const int y = static_cast<int>(blk % p.nby) * BY + ly;
-        const int z = static_cast<int>(blk / p.nby);
-        const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
-        for (int t = t0; t < t1; ++t, ++ns) {
-            const uint32_t c = ne, n = ne + 1;  // slice loads of t and t+1
-            const T *E0c = E(0, c), *E1c = E(1, c), *E2c = E(2, c);
-            for (int k = 0; k < 3; ++k) wait_full(2 * k + (c & 1), c >> 1);
-            T acc[18], a[18];
-            // ---- phase 0: (0,2) B = U_2(x+0), C = U_0(x+2) [Z0] | (0,1) B = U_1(x+0), C = U_0(x+1)
-            wait_full(B_Z + 0, ns);
-            wait_full(B_Y + 0, ns);
-#pragma unroll
-            for (int q = 0; q < 18; ++q) a[q] = E0c[q * N + sl];  // U_0(x)
-            plane_fma<T, true>(a, (h ? E1c : E2c) + ix_up, N, h ? (y_in ? E0c + sl + NX : Y0 + lx) : Z0 + sl,
-                               h ? ystr : N, s, acc);
-            release(B_Z + 0);
-            release(B_Y + 0);
-            // ---- phase 1: (1,2) A = U_1, B = U_2(x+1), C = U_1(x+2) [Z1] | (2,3) A = U_2, B = U_3(x+2) [Z3], C = U_2(x+t)
-            wait_full(B_Z + 1, ns);
-            wait_full(B_Z + 2, ns);
-            wait_full(B_Y + 1, ns);
-            wait_full(4 + (n & 1), n >> 1);
-            {
-                const T* as = h ? E2c : E1c;
-#pragma unroll
-                for (int q = 0; q < 18; ++q) a[q] = as[q * N + sl];
-                const T* bs = h ? Z3 + sl : (y_in ? E2c + sl + NX : Y2 + lx);
-                const T* cs = h ? E(2, n) + sl : Z1 + sl;
-                plane_fma<T, false>(a, bs, h ? N : ystr, cs, N, s, acc);
-            }
-            release(B_Z + 1);
-            release(B_Z + 2);
-            release(B_Y + 1);
-            release(4 + (c & 1));  // U_2 of slice t: its buffer takes U_2 of slice t+2
-            // ---- phase 2: (0,3) A = U_0, B = U_3(x+0), C = U_0(x+t) | (1,3) A = U_1, B = U_3(x+1), C = U_1(x+t)
-            wait_full(B_E3, ns);
-            wait_full(B_Y + 2, ns);
-            wait_full(0 + (n & 1), n >> 1);
-            wait_full(2 + (n & 1), n >> 1);
-            {
-                const T* as = h ? E1c : E0c;
-#pragma unroll
-                for (int q = 0; q < 18; ++q) a[q] = as[q * N + sl];
-                const T* bs = h ? (y_in ? E3 + sl + NX : Y3 + lx) : E3 + ix_up;
-                const T* cs = (h ? E(1, n) : E(0, n)) + sl;
-                plane_fma<T, false>(a, bs, h ? ystr : N, cs, N, s, acc);
-            }
-            release(B_E3);
-            release(B_Y + 2);
-            release(0 + (c & 1));
-            release(2 + (c & 1));
-            ++ne;
-            // ---- the two half-sums meet: lanes 0-15 store elements 0..8, lanes 16-31 elements 9..17
-            T* o = acc_out + int64_t(t) * 18 * p.F + s3;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                const T mine = h ? acc[9 + k] : acc[k];
-                const T give = h ? acc[k] : acc[9 + k];
-                const T got = __shfl_xor_sync(0xffffffffu, give, 16);
-                __stcs(o + (9 * h + k) * p.F, mine + got);
-            }
-        }
-        // slice t1 (only the last step's t-planes read it)
-        for (int k = 0; k < 3; ++k) release(2 * k + (ne & 1));
-        ++ne;
-    }
-}
-
 // ======================================================================================
 // FMA mode, factored: two lanes per site, nine matrix products instead of twelve (k_link_fact).
 //
@@ -605,7 +382,7 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, 1)
 //   S3  M += B C^dag: B U_2(x+0), C U_0(x+2) [Z0]      | B U_2(x+1) [Y2], C U_1(x+2) [Z1]   (M_1)
 //   S4  acc = A M   : A U_0(x), M_0                    | A U_1(x), M_1
 //   S5  acc += A M  :                                  | A U_2(x), M_2
-// Same slots and barriers as k_link_pair, but the block walk runs DOWN in t: slice t+1's U_0..U_2 are
+// The block walk runs DOWN in t: slice t+1's U_0..U_2 are
 // then the previous step's own links, already resident, so the t-plane operands never wait, they are
 // used first (S1 / S2) and their buffers take slice t-1 with a whole step in flight.  Slots that are
 // needed and freed together share one full / empty barrier pair (U_0 + U_1 of a slice buffer, U_2 of
@@ -701,7 +478,7 @@ __device__ __forceinline__ void am_fma(const T* as, int astr, const T* m, T* acc
 
 }  // namespace
 
-template <typename T, int NX, int BY, bool PF>
+template <typename T, int NX, int BY>
 __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 2 : 1)  // f32: two CTAs per SM
     k_link_fact(const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapY,
                 T* __restrict__ acc_out, WalkParams p, T s) {
@@ -761,13 +538,6 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
                 ++ne;
             }
             for (int t = t1 - 1; t >= t0; --t, ++ns) {
-                if constexpr (PF) {  // L2 warm-up one step ahead: slice t-1
-                    if (t > t0) {
-                        for (int k : {0, 36, 54}) tma_prefetch(&mapY, 0, yup, z0, (t - 1) * 72 + k);
-                        for (int k : {0, 18, 54}) tma_prefetch(&mapB, 0, y0, zup, (t - 1) * 72 + k);
-                        for (int k = 0; k < 4; ++k) tma_prefetch(&mapB, 0, y0, z0, (t - 1) * 72 + 18 * k);
-                    }
-                }
                 // issue order = the order the previous step frees the barriers' slots
                 const int tp = t * 72, b = ne & 1;
                 begin(B_E2 + b, ne >> 1, G::BLK);
@@ -825,8 +595,7 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
         int t0, t1;
         walk_item(p, item, blk, t0, t1);
         const int y = static_cast<int>(blk % p.nby) * BY + ly;
-        const int zq = static_cast<int>(blk / p.nby);
-        const int z = p.zdown ? p.nz - 1 - zq : zq;
+        const int z = static_cast<int>(blk / p.nby);
         const int64_t s3 = lx + int64_t(NX) * (y + int64_t(p.ny) * z);
         // the slice above the item: the only step whose U_mu(x+t) buffers were not waited on as own links
         wait_full(B_E01 + (ne & 1), ne >> 1);
@@ -889,8 +658,8 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
     }
 }
 
-template <typename T, int NX, int BY, bool FACT>
-static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
+template <typename T, int NX, int BY>
+static int run_link_fact(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
     using G = PairGeo<T, NX, BY>;
     CUtensorMap mB, mY;
     if (!make_map<T>(&mB, U, nx, ny, nz, int64_t(nt) * 72, BY, 1, 18) ||
@@ -899,10 +668,8 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     const size_t smem = size_t(G::TOTAL) * sizeof(T) + 2 * G::NBAR * sizeof(uint64_t);
     const DeviceInfo& di = device_info();
     if (smem > size_t(di.max_smem_optin)) return 1;
-    // auto: the plane-by-plane pair walk at f32 only; never the factored walk (A/B: f64 0.726 -> 0.693, f32 0.575 -> 0.569)
-    const bool pf = g_pair_prefetch < 0 ? (sizeof(T) == 4 && !FACT) : g_pair_prefetch != 0;
-    auto kern = FACT ? (pf ? k_link_fact<T, NX, BY, true> : k_link_fact<T, NX, BY, false>)
-                     : (pf ? k_link_pair<T, NX, BY, true> : k_link_pair<T, NX, BY, false>);
+    // (an L2 prefetch one step ahead measured slower: f64 0.726 -> 0.693, f32 0.575 -> 0.569; in git history)
+    auto kern = k_link_fact<T, NX, BY>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     WalkParams p{};
     p.ny = ny; p.nz = nz; p.nt = nt;
@@ -913,35 +680,32 @@ static int run_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, smem);
     const int Gfull = di.num_sms * std::max(per_sm, 1);
     // an item of L slices loads L+1 E slices: prologue = 0.5 step; the columns schedule (sweep_common.cuh)
-    // for the factored walk unless a chunk length is forced
-    const WalkSchedule ws = pick_schedule(p.nblocks, nt, Gfull, 0.5, FACT && g_link_chunk == 0);
+    // unless a chunk length is forced
+    const WalkSchedule ws = pick_schedule(p.nblocks, nt, Gfull, 0.5, g_link_chunk == 0);
     p.n_full = ws.n_full;
     p.chunk = ws.chunk;
     if (g_link_chunk > 0) p.chunk = std::min(g_link_chunk, nt);
-    p.zdown = g_link_zdown;
     p.nitems = p.n_full + (p.nblocks - p.n_full) * ((nt + p.chunk - 1) / p.chunk);
     const int grid = static_cast<int>(std::min<int64_t>(Gfull, p.nitems));
     kern<<<grid, G::THREADS, smem, st>>>(mB, mY, acc, p, s);
-    note_kernel(std::string(FACT ? "k_link_fact<" : "k_link_pair<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
-                std::to_string(BY) + "x1" + (pf ? ",L2 prefetch" : "") + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
+    note_kernel(std::string("k_link_fact<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
+                std::to_string(BY) + "x1" + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
                 (p.n_full ? "," + std::to_string(p.n_full) + " columns" : "") + ",chunk " + std::to_string(p.chunk) + ">");
-    return check_launch(FACT ? "link_product(fact)" : "link_product(pair)");
+    return check_launch("link_product(fact)");
 }
 
 // FMA mode only; 1 = not applicable to this lattice
-template <typename T, bool FACT>
-int launch_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
+template <typename T>
+int launch_link_fact(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st) {
     if (!aligned16(U)) return 1;
-    if (nx == 48 && ny % 3 == 0) return run_link_pair<T, 48, 3, FACT>(U, acc, nx, ny, nz, nt, s, st);
-    if (nx == 32 && ny % 4 == 0) return run_link_pair<T, 32, 4, FACT>(U, acc, nx, ny, nz, nt, s, st);
-    if (nx == 64 && ny % 2 == 0) return run_link_pair<T, 64, 2, FACT>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 48 && ny % 3 == 0) return run_link_fact<T, 48, 3>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 32 && ny % 4 == 0) return run_link_fact<T, 32, 4>(U, acc, nx, ny, nz, nt, s, st);
+    if (nx == 64 && ny % 2 == 0) return run_link_fact<T, 64, 2>(U, acc, nx, ny, nz, nt, s, st);
     return 1;
 }
 
-template int launch_link_pair<float, false>(const float*, float*, int, int, int, int, float, cudaStream_t);
-template int launch_link_pair<double, false>(const double*, double*, int, int, int, int, double, cudaStream_t);
-template int launch_link_pair<float, true>(const float*, float*, int, int, int, int, float, cudaStream_t);
-template int launch_link_pair<double, true>(const double*, double*, int, int, int, int, double, cudaStream_t);
+template int launch_link_fact<float>(const float*, float*, int, int, int, int, float, cudaStream_t);
+template int launch_link_fact<double>(const double*, double*, int, int, int, int, double, cudaStream_t);
 
 // 1 = not applicable to this lattice (caller falls back)
 template <typename T, bool FUSED>

@@ -149,13 +149,10 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-extern int g_pair_prefetch;
 extern int g_link_chunk;
-extern int g_link_rows_cfg;
 extern int g_ring_columns;
-extern int g_link_zdown;
 static std::atomic<int> g_nn_variant{0};  // 0 auto, 1 generic, 3 TMA walk, 4 TMA ring walk
-static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 3 row-split carried t-walk, 4 two-lane pair walk (FMA)
+static std::atomic<int> g_link_variant{0};  // 0 auto, 1 rows (gather), 3 row-split carried t-walk, 5 factored two-lane pair walk (FMA)
 
 // largest divisor of nz that is <= cap (the z-chunk of the cache-friendly visiting orders)
 static int chunk_planes(int nz, int cap) {
@@ -316,15 +313,9 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     // an exact pair walk 0.413)
     if (lv == 5 || (lv == 0 && mode == SU3G_FMA)) {
         if (mode != SU3G_FMA) return fail_invalid("link_product: the factored pair walk (link_variant 5) is FMA mode only");
-        const int rc = launch_link_pair<T, true>(U, acc, nx, ny, nz, nt, s, st);
+        const int rc = launch_link_fact<T>(U, acc, nx, ny, nz, nt, s, st);
         if (rc != 1) return rc;
         if (lv == 5) return fail_invalid("link_product: factored pair kernel not applicable to this lattice");
-    }
-    if (lv == 4) {
-        if (mode != SU3G_FMA) return fail_invalid("link_product: the pair walk (link_variant 4) is FMA mode only");
-        const int rc = launch_link_pair<T, false>(U, acc, nx, ny, nz, nt, s, st);
-        if (rc != 1) return rc;
-        return fail_invalid("link_product: pair kernel not applicable to this lattice");
     }
     if (lv == 3 || (lv == 0 && sizeof(T) == 4 && mode == SU3G_EXACT)) {
         const int rc = mode == SU3G_FMA ? launch_link_walk<T, true>(U, acc, nx, ny, nz, nt, s, st)
@@ -357,10 +348,10 @@ int su3g_set_option(const char* name, int64_t value) {
         return SU3G_OK;
     }
     if (std::strcmp(name, "link_variant") == 0) {
-        if (value < 0 || value > 5 || value == 2)
-            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 3 (row-split walk), "
-                                "4 (two-lane pair walk, FMA) or 5 (factored pair walk, FMA); 2 (the ring walk) was "
-                                "removed, measured slower");
+        if (value < 0 || value > 5 || value == 2 || value == 4)
+            return fail_invalid("set_option: link_variant must be 0 (auto), 1 (rows gather), 3 (row-split walk) or "
+                                "5 (factored pair walk, FMA); 2 (the ring walk) and 4 (the plane-by-plane pair "
+                                "walk) were removed, measured slower");
         g_link_variant.store(static_cast<int>(value));
         return SU3G_OK;
     }
@@ -375,29 +366,14 @@ int su3g_set_option(const char* name, int64_t value) {
         g_eo_ring_cfg = static_cast<int>(value);
         return SU3G_OK;
     }
-    if (std::strcmp(name, "link_pair_prefetch") == 0) {
-        if (value < -1 || value > 1) return fail_invalid("set_option: link_pair_prefetch must be -1 (auto), 0 or 1");
-        g_pair_prefetch = static_cast<int>(value);
-        return SU3G_OK;
-    }
     if (std::strcmp(name, "link_chunk") == 0) {
         if (value < 0 || value > 4096) return fail_invalid("set_option: link_chunk must be in [0, 4096] (0 = auto)");
         g_link_chunk = static_cast<int>(value);
         return SU3G_OK;
     }
-    if (std::strcmp(name, "link_rows_cfg") == 0) {
-        if (value < 0 || value > 4) return fail_invalid("set_option: link_rows_cfg must be in [0, 4]");
-        g_link_rows_cfg = static_cast<int>(value);
-        return SU3G_OK;
-    }
     if (std::strcmp(name, "nn_ring_columns") == 0) {
         if (value < 0 || value > 1) return fail_invalid("set_option: nn_ring_columns must be 0 or 1");
         g_ring_columns = static_cast<int>(value);
-        return SU3G_OK;
-    }
-    if (std::strcmp(name, "link_zdown") == 0) {
-        if (value < 0 || value > 1) return fail_invalid("set_option: link_zdown must be 0 or 1");
-        g_link_zdown = static_cast<int>(value);
         return SU3G_OK;
     }
     if (std::strcmp(name, "nn_ring_cfg") == 0) {

@@ -137,10 +137,10 @@ int launch_dslash_tma(const T* U, const T* v, T* out, int nx, int ny, int nz, in
 // row-split t-walk with carried t-planes (link_walk.cu); 1 = not applicable
 template <typename T, bool FUSED>
 int launch_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
-// two lanes per site, FMA mode (link_walk.cu): three planes each, or (FACT) the factored form
-// sum_mu U_mu(x) sum_nu U_nu(x+mu) U_mu(x+nu)^dag, nine products per site; 1 = not applicable
-template <typename T, bool FACT>
-int launch_link_pair(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
+// two lanes per site, FMA mode, the factored form sum_mu U_mu(x) sum_nu U_nu(x+mu) U_mu(x+nu)^dag, nine
+// products per site (link_walk.cu); 1 = not applicable
+template <typename T>
+int launch_link_fact(const T* U, T* acc, int nx, int ny, int nz, int nt, T s, cudaStream_t st);
 template <typename T, bool FUSED>
 int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_t st);
 

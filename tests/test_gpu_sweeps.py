@@ -345,11 +345,10 @@ def test_link_product_bitwise(dims, precision, variant):
     "dims", [(48, 3, 2, 3), (48, 6, 5, 7), (32, 8, 4, 6), (64, 4, 3, 5), (32, 4, 1, 2), (48, 48, 3, 4),
              (48, 48, 20, 3)]  # the last: more blocks than CTAs, so the factored walk's columns schedule runs
 )
-@pytest.mark.parametrize("variant,kernel", [(4, "k_link_pair<"), (5, "k_link_fact<")], ids=["pair", "factored"])
-def test_link_pair_walk(dims, precision, variant, kernel):
-    """link_variant 4 (two lanes per site, three planes each) and 5 (the factored form, nine products
-    per site; the FMA-mode default): within the north-star tolerance of the composed reference, on
-    lattices covering every block geometry and the periodic wrap of the t-chunks; exact mode is refused."""
+def test_link_pair_walk(dims, precision, variant=5, kernel="k_link_fact<"):
+    """link_variant 5 (two lanes per site, the factored form, nine products per site; the FMA-mode
+    default): within the north-star tolerance of the composed reference, on lattices covering every block
+    geometry, the periodic wrap of the t-chunks and both work-item schedules; exact mode is refused."""
     from paper_1309_0551_b200 import _lib
 
     dt = _dt(precision)
@@ -360,8 +359,15 @@ def test_link_pair_walk(dims, precision, variant, kernel):
     try:
         got = sweeps.link_product_aos(U, dims, 1 / 6, mode="fma")
         assert _lib.last_kernel().startswith(kernel), _lib.last_kernel()
-        if variant == 5 and dims == (48, 48, 20, 3):
+        if dims == (48, 48, 20, 3):
             assert "columns" in _lib.last_kernel(), _lib.last_kernel()
+            _lib.set_option("link_chunk", 2)  # the uniform chunk-major schedule on the same lattice
+            try:
+                got_u = sweeps.link_product_aos(U, dims, 1 / 6, mode="fma")
+                assert "columns" not in _lib.last_kernel(), _lib.last_kernel()
+            finally:
+                _lib.set_option("link_chunk", 0)
+            assert np.array_equal(got_u, got)  # same per-site arithmetic, whatever the schedule
         assert floored_rel_err(got, want) <= (1e-5 if dt == np.float32 else 1e-12)
         with pytest.raises(ValueError, match="FMA mode only"):
             sweeps.link_product_aos(U, dims, 1 / 6)

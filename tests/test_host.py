@@ -68,12 +68,12 @@ def test_tuning_knobs_validate_names_and_ranges_without_a_device():
     """su3g_set_option (include/su3g.h): every documented knob accepts its range, rejects the rest
     (the removed ring link walk included), and restores its default."""
     lib = _lib.load()
-    ok = {"nn_variant": (0, 1, 3, 4), "link_variant": (0, 1, 3, 4, 5), "dslash_eo_variant": (0, 1, 2),
-          "dslash_eo_ring_cfg": (0, 1, 2), "link_pair_prefetch": (-1, 0, 1), "nn_ring_cfg": (0, 1, 2, 3, 4),
-          "sm_reserve": (0, 4), "link_chunk": (0, 12, 4096), "link_zdown": (0, 1), "nn_ring_columns": (0, 1), "link_rows_cfg": (0, 1, 2, 3, 4)}
-    bad = {"nn_variant": (2, 5), "link_variant": (2, 6, -1), "dslash_eo_variant": (3, -1),
-           "dslash_eo_ring_cfg": (3,), "link_pair_prefetch": (2, -2), "nn_ring_cfg": (5,), "sm_reserve": (-1, 65),
-           "link_chunk": (-1, 4097), "link_zdown": (-1, 2), "nn_ring_columns": (-1, 2), "link_rows_cfg": (-1, 5)}
+    ok = {"nn_variant": (0, 1, 3, 4), "link_variant": (0, 1, 3, 5), "dslash_eo_variant": (0, 1, 2),
+          "dslash_eo_ring_cfg": (0, 1, 2), "nn_ring_cfg": (0, 1, 2, 3, 4),
+          "sm_reserve": (0, 4), "link_chunk": (0, 12, 4096), "nn_ring_columns": (0, 1)}
+    bad = {"nn_variant": (2, 5), "link_variant": (2, 4, 6, -1), "dslash_eo_variant": (3, -1),
+           "dslash_eo_ring_cfg": (3,), "nn_ring_cfg": (5,), "sm_reserve": (-1, 65),
+           "link_chunk": (-1, 4097), "nn_ring_columns": (-1, 2), "link_pair_prefetch": (0,), "link_zdown": (0,)}
     try:
         for name, vals in ok.items():
             for v in vals:
@@ -86,8 +86,8 @@ def test_tuning_knobs_validate_names_and_ranges_without_a_device():
         assert lib.su3g_set_option(b"no_such_knob", 0) == _lib.SU3G_EINVAL
     finally:
         for name, default in (("nn_variant", 0), ("link_variant", 0), ("dslash_eo_variant", 0),
-                              ("dslash_eo_ring_cfg", 0), ("link_pair_prefetch", -1), ("nn_ring_cfg", 0),
-                              ("sm_reserve", 0), ("link_chunk", 0), ("link_zdown", 0), ("nn_ring_columns", 1), ("link_rows_cfg", 0)):
+                              ("dslash_eo_ring_cfg", 0), ("nn_ring_cfg", 0),
+                              ("sm_reserve", 0), ("link_chunk", 0), ("nn_ring_columns", 1)):
             lib.su3g_set_option(name.encode(), default)
 
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # link product: the link GPU tests, then a same-box A/B of link variants (FMA mode): tools/ab_link.sh [variants...]
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-VARS="${@:-4 5}"
+VARS="${@:-5}"
 timeout 900 python -m pytest tests/test_gpu_sweeps.py tests/test_gpu_guard.py -k "link" -q -x -p no:cacheprovider > gpurun_out/pytest_link.log 2>&1; echo "pytest=$?" >> gpurun_out/status.txt
 for rep in 1 2 3; do
 for v in $VARS; do
