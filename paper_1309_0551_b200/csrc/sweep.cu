@@ -307,7 +307,7 @@ static int link_product(const T* U, T* acc, int nx, int ny, int nz, int nt, T s,
     Geom g{nx, ny, nz, nt, int64_t(nx) * ny * nz};
     const int lv = g_link_variant.load();
     // auto (48^4 on B200, fraction of HBM; profiles/r02/ab_link_walk.md, ab_link_pair.txt, ab_link_fact.txt):
-    // FMA mode -> the factored two-lane pair walk (f64 0.677, f32 0.565; the plane-by-plane pair walk
+    // FMA mode -> the factored two-lane pair walk (f64 0.77, f32 0.63; the removed plane-by-plane pair walk
     // 0.611 / 0.429, the removed ring walk 0.546 / 0.397, rows 0.525 / 0.357);
     // exact f32 -> the row-split carried walk (0.351 vs rows 0.309); exact f64 -> rows (0.465; walk 0.461,
     // an exact pair walk 0.413)

@@ -4,7 +4,7 @@
 
 Covers the per-site stream kernels (all fifteen routines, both precisions), the layout transforms, the
 seeded fill, the NN sweep kernels (ring walk, f32 TMA walk, generic, t-slab edges / halo pack), the
-dslash (SoA parity kernels, checkerboarded fields), the link product (rows gather, row-split walk, pair walk), the
+dslash (SoA parity kernels, checkerboarded fields), the link product (rows gather, row-split walk, factored pair walk), the
 one-rank P2P boundary protocol and the one-rank NCCL slab driver.  Every result is compared with the
 CPU oracle, so a kernel that misbehaves under the tool is visible in the exit code too.
 """
