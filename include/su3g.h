@@ -65,7 +65,7 @@ SU3G_API int64_t su3g_device_l2_bytes(void);
  *                   nine products per site; the FMA default)
  *   "nn_ring_columns": 0 / 1: the ring walks' (NN sweep, checkerboarded dslash) columns schedule: whole t-columns
  *                   for full rounds of blocks, t-chunks for the rest (default 1)
- *   "link_chunk":   t-chunk length of the factored walk's work items (0 = auto: the columns schedule)
+ *   "link_chunk":   t-chunk length of the link walks' work items (0 = auto: the columns schedule)
  *   "dslash_eo_variant": 0 auto, 1 gather kernel, 2 half-lattice ring walk (nx in {32, 64}, even ny, nz)
  *   "dslash_eo_ring_cfg": slot / CTA configuration of that ring walk for A/B (0 = default)
  *   "nn_tma_chunk": t-chunk length of the TMA walk's work items (0 = auto, balances the wave)

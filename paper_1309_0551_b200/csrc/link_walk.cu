@@ -40,7 +40,7 @@
 
 namespace su3g {
 
-int g_link_chunk = 0;  // su3g_set_option("link_chunk"): t-chunk length of the factored walk's work items (0 auto)
+int g_link_chunk = 0;  // su3g_set_option("link_chunk"): t-chunk length of the link walks' work items (0 auto: the columns schedule)
 
 namespace {
 
@@ -331,14 +331,18 @@ static int run_link_walk(const T* U, T* acc, int nx, int ny, int nz, int nt, T s
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::THREADS, smem);
     const int Gfull = di.num_sms * std::max(per_sm, 1);
-    // an item of L slices costs L + 1 steps (the drain step loads three blocks and finishes)
-    p.chunk = pick_chunk(p.nblocks, nt, Gfull, 0.6);
-    p.nitems = p.nblocks * ((nt + p.chunk - 1) / p.chunk);
+    // an item of L slices costs L + 1 steps (the drain step loads three blocks and finishes); the columns
+    // schedule (sweep_common.cuh) unless a chunk length is forced
+    const WalkSchedule ws = pick_schedule(p.nblocks, nt, Gfull, 0.6, g_link_chunk == 0);
+    p.n_full = ws.n_full;
+    p.chunk = ws.chunk;
+    if (g_link_chunk > 0) p.chunk = std::min(g_link_chunk, nt);
+    p.nitems = p.n_full + (p.nblocks - p.n_full) * ((nt + p.chunk - 1) / p.chunk);
     const int grid = static_cast<int>(std::min<int64_t>(Gfull, p.nitems));
     kern<<<grid, G::THREADS, smem, st>>>(mB, mY, acc, p, s);
     note_kernel(std::string("k_link_walk<") + (sizeof(T) == 4 ? "f32," : "f64,") + std::to_string(NX) + "x" +
                 std::to_string(BY) + "x1" + (per_sm > 1 ? "," + std::to_string(per_sm) + " CTAs/SM" : "") +
-                ",chunk " + std::to_string(p.chunk) + ">");
+                (p.n_full ? "," + std::to_string(p.n_full) + " columns" : "") + ",chunk " + std::to_string(p.chunk) + ">");
     return check_launch("link_product(walk)");
 }
 
