@@ -130,7 +130,9 @@ int launch_link_rows(const T* U, T* acc, const Geom& g, T s, int ZC, cudaStream_
     // per SM (96 / 80 registers, spills) 0.430 / 0.379 against 0.480 at 4 (profiles/r02/ab_link_rows_unroll.txt)
     // r02 last session: for f64 exact, 2 / 3 / 4 CTAs per SM with or without the early C gather all measure
     // 0.476-0.487 (two CTAs 0.437; profiles/r02/ab_link_rows_cfg.txt): the gathers pull 2.6 KB per site through
-    // L2 (13.8 GB per 48^4 sweep, ~11.5 TB/s), which is the bound, not occupancy or the FP64 pipe
+    // L2 (13.8 GB per 48^4 sweep, ~11.5 TB/s).  Holding A = U_mu(x) in registers for a mu's planes (15
+    // gathers per site instead of 18, 168 registers) measured slower at f64: exact 0.465, FMA 0.480 against
+    // 0.476 / 0.525 (f32 0.349 against 0.309, below the walk's 0.354; profiles/r02/ab_link_rows_hold_a.txt)
     if constexpr (sizeof(T) == 4) k_link_rows<T, FUSED, 6, true><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     else k_link_rows<T, FUSED, FUSED ? 3 : 4, false><<<grid, 128, 0, st>>>(U, acc, g, s, ZC);
     return check_launch("link_product(rows)");
