@@ -203,11 +203,22 @@ def peak_hbm():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def _compute_floor(cfg, args, bytes_per_launch, kern_avg_ms):
+def _compute_floor(cfg, args, bytes_per_launch, kern_avg_ms, kernel=""):
     """Exact-mode FP-pipe time of one launch (every flop one FMUL/FADD or DMUL/DADD, flops.py) beside the
-    HBM time of its algorithmic bytes: which roof binds.  None for FMA mode (fused ops) and routines."""
+    HBM time of its algorithmic bytes: which roof binds.  FMA mode: only the link product (its factored
+    form's 990 fused instructions per site); None for the other FMA-mode sweeps and the routines."""
     from paper_1309_0551_b200 import flops as _flops
 
+    if cfg["kind"] == "link" and args.mode == "fma" and kern_avg_ms and (kernel or "").startswith("k_link_fact"):
+        # the factored walk issues 990 fused FP instructions per site (flops.LINK_FACTORED_FP_INSTRUCTIONS)
+        sites = bytes_per_launch / _flops.intensity("link", args.dtype)["bytes_per_site"]
+        fp_ms = _flops.fma_floor_s(_flops.LINK_FACTORED_FP_INSTRUCTIONS, args.dtype, int(sites)) * 1e3
+        hbm_ms = bytes_per_launch / (peak_hbm()[0] * 1e9) * 1e3
+        return {"fp_pipe_ms": fp_ms, "hbm_ms": hbm_ms, "bound": "fp-pipe" if fp_ms > hbm_ms else "hbm",
+                "max_hbm_frac": min(1.0, hbm_ms / fp_ms), "frac_of_binding_roof": max(fp_ms, hbm_ms) / kern_avg_ms,
+                "fp_instructions_per_site": _flops.LINK_FACTORED_FP_INSTRUCTIONS,
+                "pipe": "FP32 128 / FP64 64 lanes per SM per clock x 148 SMs x 1.965 GHz, factored form: "
+                        "nine 3x3 complex products of 108 FMAs + 18 multiplies per site"}
     if cfg["kind"] not in ("nn", "link", "dslash") or args.mode != "exact" or not kern_avg_ms:
         return None
     per_site = _flops.intensity(cfg["kind"], args.dtype)["bytes_per_site"]
@@ -661,7 +672,7 @@ def run_b200(args, rank, world, local):
             "traffic": traffic_for(args.workload, args.dtype, args.mode, dispatched),
             "algorithmic_bytes_per_launch": bytes_per_launch,
             "kernel_avg_ms": kern_avg_ms,
-            "compute_floor": _compute_floor(cfg, args, bytes_per_launch, kern_avg_ms),
+            "compute_floor": _compute_floor(cfg, args, bytes_per_launch, kern_avg_ms, dispatched),
         },
         "flops_per_site": intensity["flops_per_site"],
         "ai_flop_per_byte": intensity["ai_flop_per_byte"],

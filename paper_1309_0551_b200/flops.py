@@ -98,6 +98,17 @@ def compute_floor_s(name: str, dtype: str, sites: int, sms: int = 148, clock_hz:
     return fc.total * sites / (sms * lanes * clock_hz)
 
 
+# FMA mode of the link product in the factored form (csrc/link_walk.cu k_link_fact): nine 3x3 complex
+# products of 108 FMAs each and 18 multiplies by the scalar per site
+LINK_FACTORED_FP_INSTRUCTIONS = 9 * 108 + 18
+
+
+def fma_floor_s(instructions_per_site: int, dtype: str, sites: int, sms: int = 148, clock_hz: float = 1.965e9) -> float:
+    """Seconds the FP pipe needs for `sites` sites at `instructions_per_site` fused instructions each."""
+    lanes = 128 if dtype == "f32" else 64
+    return instructions_per_site * sites / (sms * lanes * clock_hz)
+
+
 def intensity(name: str, dtype: str) -> dict:
     """{'flops_per_site', 'bytes_per_site', 'ai_flop_per_byte'} of a routine or a sweep ('nn', 'link', 'dslash')."""
     esz = {"f32": 4, "f64": 8}[dtype]
