@@ -381,18 +381,19 @@ struct PairGeo {
 // instead of 18.  Lanes 0-15 of a warp take mu = 0 (four products), lanes 16-31 mu = 1 and 2 (five);
 // every step has the same product type in both halves, so the warp runs five product steps with one
 // instruction stream (lanes 0-15 sit out the fifth):
-//   S1  M = B C^dag : B U_3(x+0), C U_0(x+t)           | B U_3(x+2) [Z3], C U_2(x+t)        (M_2, set aside)
-//   S2  M += B C^dag: B U_1(x+0), C U_0(x+1) [Y0]      | B U_3(x+1) [Y3], C U_1(x+t)        (M_1, from zero)
-//   S3  M += B C^dag: B U_2(x+0), C U_0(x+2) [Z0]      | B U_2(x+1) [Y2], C U_1(x+2) [Z1]   (M_1)
+//   S1  M = B C^dag : B U_3(x+0), C U_0(x+t)           | B U_3(x+1) [Y3], C U_1(x+t)        (M_1)
+//   S2  M += B C^dag: B U_1(x+0), C U_0(x+1) [Y0]      | B U_3(x+2) [Z3], C U_2(x+t)        (M_2, from zero)
+//   S3  M += B C^dag: B U_2(x+0), C U_0(x+2) [Z0]      | B U_2(x+1) [Y2], C U_1(x+2) [Z1]   (M_1 again)
 //   S4  acc = A M   : A U_0(x), M_0                    | A U_1(x), M_1
 //   S5  acc += A M  :                                  | A U_2(x), M_2
 // The block walk runs DOWN in t: slice t+1's U_0..U_2 are
 // then the previous step's own links, already resident, so the t-plane operands never wait, they are
-// used first (S1 / S2) and their buffers take slice t-1 with a whole step in flight.  Slots that are
-// needed and freed together share one full / empty barrier pair (U_0 + U_1 of a slice buffer, U_2 of
-// a slice buffer, E3 + Z3, Y3 + Y0, Z0 + Y2 + Z1: 8 waits and 5 releases per step), and the
-// producer issues a step's loads in the order the previous step frees them: U_2 | E3 Z3, Y3 Y0,
-// U_0 U_1 | Z0 Y2 Z1.
+// used first (S1 / S2) and their buffers take slice t-1 with more than a step in flight.  Every
+// single-buffered slot is read in exactly one product step (both users of E3 share S1), so it is freed
+// in the step that needs it and its refill has a whole step in flight.  Slots of one step share one
+// full / empty barrier pair (U_0 + U_1 of a slice buffer, U_2 of a slice buffer, E3 + Y3, Y0 + Z3,
+// Z0 + Y2 + Z1), and the producer issues a step's loads in the order the previous step frees them,
+// which is the order the step needs them: E3 Y3, U_0 U_1 | Y0 Z3, U_2 | Z0 Y2 Z1.
 // ======================================================================================
 
 namespace {
@@ -492,8 +493,8 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
     T* sm = reinterpret_cast<T*>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + G::TOTAL);
     uint64_t* empty = full + G::NBAR;
-    // slots that are needed and freed together share a barrier: U_0 + U_1 of a slice buffer (0, 1),
-    // U_2 of a slice buffer (2, 3), E3 + Z3 (4), Y3 + Y0 (5), Z0 + Y2 + Z1 (6)
+    // slots that are needed and freed in the same product step share a barrier: U_0 + U_1 of a slice
+    // buffer (0, 1), U_2 of a slice buffer (2, 3), E3 + Y3 (4), Y0 + Z3 (5), Z0 + Y2 + Z1 (6)
     constexpr int B_E01 = 0, B_E2 = 2, B_A = 4, B_B = 5, B_C = 6, NB = 7;
     const int tid = threadIdx.x;
     if (tid == 0) {
@@ -534,27 +535,28 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
             const int yup = (y0 + BY) % p.ny, zup = (z0 + 1) % p.nz;
             {  // the slice above the item (U_0..U_2 only): the first step's U_mu(x+t)
                 const int tu = (t1 == p.nt ? 0 : t1) * 72, b = ne & 1;
-                begin(B_E2 + b, ne >> 1, G::BLK);
-                tma_load_4d(Ew(2, ne), &mapB, 0, y0, z0, tu + 36, &full[B_E2 + b], pol);
                 begin(B_E01 + b, ne >> 1, 2 * G::BLK);
                 tma_load_4d(Ew(0, ne), &mapB, 0, y0, z0, tu, &full[B_E01 + b], pol);
                 tma_load_4d(Ew(1, ne), &mapB, 0, y0, z0, tu + 18, &full[B_E01 + b], pol);
+                begin(B_E2 + b, ne >> 1, G::BLK);
+                tma_load_4d(Ew(2, ne), &mapB, 0, y0, z0, tu + 36, &full[B_E2 + b], pol);
                 ++ne;
             }
             for (int t = t1 - 1; t >= t0; --t, ++ns) {
-                // issue order = the order the previous step frees the barriers' slots
+                // issue order = the order the previous step frees the barriers' slots = the order this step
+                // needs them: every load has a whole step in flight
                 const int tp = t * 72, b = ne & 1;
-                begin(B_E2 + b, ne >> 1, G::BLK);
-                tma_load_4d(Ew(2, ne), &mapB, 0, y0, z0, tp + 36, &full[B_E2 + b], pol);
-                begin(B_A, ns, 2 * G::BLK);
+                begin(B_A, ns, G::BLK + G::YSUB);
                 tma_load_4d(E3w, &mapB, 0, y0, z0, tp + 54, &full[B_A], pol);
-                tma_load_4d(Z0w + 2 * G::BLK, &mapB, 0, y0, zup, tp + 54, &full[B_A], pol);
-                begin(B_B, ns, 2 * G::YSUB);
-                tma_load_4d(Y0w + 2 * G::YSUB, &mapY, 0, yup, z0, tp + 54, &full[B_B], pol);
-                tma_load_4d(Y0w, &mapY, 0, yup, z0, tp, &full[B_B], pol);
+                tma_load_4d(Y0w + 2 * G::YSUB, &mapY, 0, yup, z0, tp + 54, &full[B_A], pol);
                 begin(B_E01 + b, ne >> 1, 2 * G::BLK);
                 tma_load_4d(Ew(0, ne), &mapB, 0, y0, z0, tp, &full[B_E01 + b], pol);
                 tma_load_4d(Ew(1, ne), &mapB, 0, y0, z0, tp + 18, &full[B_E01 + b], pol);
+                begin(B_B, ns, G::BLK + G::YSUB);
+                tma_load_4d(Y0w, &mapY, 0, yup, z0, tp, &full[B_B], pol);
+                tma_load_4d(Z0w + 2 * G::BLK, &mapB, 0, y0, zup, tp + 54, &full[B_B], pol);
+                begin(B_E2 + b, ne >> 1, G::BLK);
+                tma_load_4d(Ew(2, ne), &mapB, 0, y0, z0, tp + 36, &full[B_E2 + b], pol);
                 begin(B_C, ns, 2 * G::BLK + G::YSUB);
                 tma_load_4d(Z0w, &mapB, 0, y0, zup, tp, &full[B_C], pol);
                 tma_load_4d(Y0w + G::YSUB, &mapY, 0, yup, z0, tp + 36, &full[B_C], pol);
@@ -609,29 +611,37 @@ __global__ void __launch_bounds__(PairGeo<T, NX, BY>::THREADS, sizeof(T) == 4 ? 
             const uint32_t u = ne, c = ne + 1;  // slice loads of t+1 (resident since the previous step) and t
             const T *E0c = E(0, c), *E1c = E(1, c), *E2c = E(2, c);
             T m[18], m2[18], acc[18];
-            // ---- S1: B U_3(x+0), C U_0(x+t) | B U_3(x+2), C U_2(x+t)   (M_0 | M_2)
+            // ---- S1: B U_3(x+0), C U_0(x+t) | B U_3(x+1), C U_1(x+t)   (M_0 | M_1)
             wait_if(okA, B_A, ns);
-            const uint32_t okB = test_full(B_B, ns), okD = test_full(B_E01 + (c & 1), c >> 1);
-            bcdag_fma<T, true>(h ? Z3 + sl : E3 + ix_up, N, (h ? E(2, u) : E(0, u)) + sl, N, m);
-            release(B_E2 + (u & 1));
-            // lanes 16-31: M_2 is complete, M_1 starts from zero
+            const uint32_t okD = test_full(B_E01 + (c & 1), c >> 1), okB = test_full(B_B, ns);
+            bcdag_fma<T, true>(h ? (y_in ? E3 + sl + NX : Y3 + lx) : E3 + ix_up, h ? ystr : N,
+                               (h ? E(1, u) : E(0, u)) + sl, N, m);
+            release(B_A);
+            release(B_E01 + (u & 1));
+            // lanes 16-31: M_1 waits in m2, M_2 starts from zero
 #pragma unroll
             for (int q = 0; q < 18; ++q) {
                 m2[q] = m[q];
                 m[q] = h ? T(0) : m[q];
             }
-            // ---- S2: B U_1(x+0), C U_0(x+1) | B U_3(x+1), C U_1(x+t)   (M_0 | M_1)
-            wait_if(okB, B_B, ns);
+            // ---- S2: B U_1(x+0), C U_0(x+1) | B U_3(x+2), C U_2(x+t)   (M_0 | M_2)
             wait_if(okD, B_E01 + (c & 1), c >> 1);
-            const uint32_t okC = test_full(B_C, ns), okE = test_full(B_E2 + (c & 1), c >> 1);
-            bcdag_fma<T, false>(h ? (y_in ? E3 + sl + NX : Y3 + lx) : E1c + ix_up, h ? ystr : N,
-                                h ? E(1, u) + sl : (y_in ? E0c + sl + NX : Y0 + lx), h ? N : ystr, m);
-            release(B_A);
+            wait_if(okB, B_B, ns);
+            const uint32_t okE = test_full(B_E2 + (c & 1), c >> 1), okC = test_full(B_C, ns);
+            bcdag_fma<T, false>(h ? Z3 + sl : E1c + ix_up, N,
+                                h ? E(2, u) + sl : (y_in ? E0c + sl + NX : Y0 + lx), h ? N : ystr, m);
             release(B_B);
-            release(B_E01 + (u & 1));
+            release(B_E2 + (u & 1));
+            // lanes 16-31: M_2 is complete (kept in m2), back to M_1
+#pragma unroll
+            for (int q = 0; q < 18; ++q) {
+                const T t2 = m[q];
+                m[q] = h ? m2[q] : t2;
+                m2[q] = t2;
+            }
             // ---- S3: B U_2(x+0), C U_0(x+2) | B U_2(x+1), C U_1(x+2)   (M_0 | M_1)
-            wait_if(okC, B_C, ns);
             wait_if(okE, B_E2 + (c & 1), c >> 1);
+            wait_if(okC, B_C, ns);
             bcdag_fma<T, false>(h ? (y_in ? E2c + sl + NX : Y2 + lx) : E2c + ix_up, h ? ystr : N,
                                 (h ? Z1 : Z0) + sl, N, m);
             release(B_C);
