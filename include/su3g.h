@@ -57,6 +57,15 @@ SU3G_API const char *su3g_last_kernel(void);
 /* number of SMs / L2 bytes of the current device (0 on failure) */
 SU3G_API int su3g_device_sm_count(void);
 SU3G_API int64_t su3g_device_l2_bytes(void);
+/* The work-item schedule of the persistent t-walks (ring NN sweep, checkerboarded dslash, link walks) for
+ * `nblocks` blocks x `nslices` t-slices on `ctas` resident CTAs (host arithmetic, no device needed; for tests
+ * and diagnostics).  Returns the item count (-1 on bad arguments); n_full = leading whole-column items and
+ * chunk = t-chunk length of the others (either may be null); when 0 <= item < count, also that item's block
+ * and slice range [t0, t1).  prologue_x10: an item's start-up cost in tenths of a step; columns: 0 forces the
+ * uniform chunk-major schedule. */
+SU3G_API int64_t su3g_walk_schedule(int64_t nblocks, int32_t nslices, int32_t ctas, int32_t prologue_x10,
+                                    int32_t columns, int64_t item, int64_t *blk, int32_t *t0, int32_t *t1,
+                                    int64_t *n_full, int32_t *chunk);
 /* process-wide tuning/debug knobs (not needed for normal use):
  *   "nn_variant":   0 auto, 1 generic one-thread-per-site (z-chunked order), 3 TMA t-walk,
  *                   4 TMA ring walk (the default where it applies: nx in {32, 48, 64}, even ny, nz)

@@ -54,6 +54,7 @@ def _signatures():
         "su3g_device_sm_count": ([], ctypes.c_int),
         "su3g_device_l2_bytes": ([], ctypes.c_int64),
         "su3g_set_option": ([ctypes.c_char_p, ctypes.c_int64], ctypes.c_int),
+        "su3g_walk_schedule": ([_i64, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp], ctypes.c_int64),
         "su3g_comm_unique_id": ([_vp], ctypes.c_int),
         "su3g_comm_init": ([_i32, _i32, _vp, _vp], ctypes.c_int),
         "su3g_comm_destroy": ([_vp], ctypes.c_int),

@@ -449,6 +449,24 @@ int su3g_nn_halo_w_f64(const double* U, const double* v, double* w, int32_t nx, 
                        int32_t mode, su3g_stream_t st) {
     return nn_halo_w<double>(U, v, w, nx, ny, nz, nt, mode, reinterpret_cast<cudaStream_t>(st));
 }
+int64_t su3g_walk_schedule(int64_t nblocks, int32_t nslices, int32_t ctas, int32_t prologue_x10, int32_t columns,
+                           int64_t item, int64_t* blk, int32_t* t0, int32_t* t1, int64_t* n_full, int32_t* chunk) {
+    if (nblocks <= 0 || nslices <= 0 || ctas <= 0 || prologue_x10 < 0) {
+        fail_invalid("walk_schedule: nblocks, nslices, ctas must be positive and prologue_x10 non-negative");
+        return -1;
+    }
+    const WalkSchedule w = pick_schedule(nblocks, nslices, ctas, prologue_x10 / 10.0, columns != 0);
+    if (n_full) *n_full = w.n_full;
+    if (chunk) *chunk = w.chunk;
+    if (item >= 0 && item < w.nitems && blk && t0 && t1) {
+        int a, b;
+        schedule_item(w.n_full, nblocks, w.chunk, 0, nslices, item, *blk, a, b);
+        *t0 = a;
+        *t1 = b;
+    }
+    return w.nitems;
+}
+
 int su3g_link_product_f32(const float* U, float* acc, int32_t nx, int32_t ny, int32_t nz, int32_t nt, float s,
                           int32_t mode, su3g_stream_t st) {
     return link_product<float>(U, acc, nx, ny, nz, nt, s, mode, reinterpret_cast<cudaStream_t>(st));

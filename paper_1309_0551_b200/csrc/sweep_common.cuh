@@ -97,7 +97,7 @@ inline WalkSchedule pick_schedule(int64_t nblocks, int L, int G, double prologue
 }
 
 // item -> (block, [t0, t1)) of a schedule over slices [lo, hi)
-__device__ __forceinline__ void schedule_item(int64_t n_full, int64_t nblocks, int chunk, int lo, int hi, int64_t item,
+__host__ __device__ __forceinline__ void schedule_item(int64_t n_full, int64_t nblocks, int chunk, int lo, int hi, int64_t item,
                                               int64_t& blk, int& t0, int& t1) {
     if (item < n_full) {
         blk = item;
@@ -109,7 +109,7 @@ __device__ __forceinline__ void schedule_item(int64_t n_full, int64_t nblocks, i
     const int64_t ch = r / nbt;
     blk = n_full + (r - ch * nbt);
     t0 = lo + static_cast<int>(ch) * chunk;
-    t1 = min(t0 + chunk, hi);
+    t1 = t0 + chunk < hi ? t0 + chunk : hi;
 }
 
 extern int g_ring_columns;  // su3g_set_option("nn_ring_columns"): the columns schedule of the ring walks (A/B)

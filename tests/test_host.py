@@ -362,3 +362,44 @@ def test_field_layout_validation_without_a_gpu():
         Field(Lattice4D(4, 4, 4, 3), "vec", layout="eo")
     with pytest.raises(ValueError, match="layout"):
         Field(Lattice4D(4, 4, 4, 4), "vec", layout="aos")
+
+
+@pytest.mark.parametrize("columns", [0, 1])
+def test_walk_schedule_covers_every_block_slice_exactly_once(columns):
+    """The persistent t-walks' work-item schedule (csrc/sweep_common.cuh pick_schedule / schedule_item,
+    through su3g_walk_schedule): for both the uniform and the columns form, the items partition
+    blocks x slices exactly, whole-column items come first, and the columns form never takes more
+    rounds of CTAs (weighted by item length + prologue) than the uniform one it replaces."""
+    lib = _lib.load()
+    rng = np.random.default_rng(1309)
+    cases = [(768, 48, 148), (1024, 16, 296), (1024, 16, 148), (1024, 14, 296), (256, 32, 592), (320, 3, 148),
+             (1, 1, 148), (148, 7, 148), (149, 5, 148)]
+    cases += [(int(rng.integers(1, 1500)), int(rng.integers(1, 130)), int(rng.choice([148, 296, 444, 592])))
+              for _ in range(40)]
+    blk, n_full = ctypes.c_int64(), ctypes.c_int64()
+    t0, t1, chunk = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+
+    def cost(nblocks, L, G, cols, prologue):
+        n = lib.su3g_walk_schedule(nblocks, L, G, int(prologue * 10), cols, -1, None, None, None,
+                                   ctypes.byref(n_full), ctypes.byref(chunk))
+        rounds_full = n_full.value // G
+        rest = n - n_full.value
+        return rounds_full * (L + prologue) + -(-rest // G) * (chunk.value + prologue) if rest else rounds_full * (L + prologue)
+
+    for nblocks, L, G in cases:
+        n = lib.su3g_walk_schedule(nblocks, L, G, 5, columns, -1, None, None, None, ctypes.byref(n_full),
+                                   ctypes.byref(chunk))
+        assert n > 0 and 1 <= chunk.value <= L and 0 <= n_full.value <= nblocks, (nblocks, L, G)
+        assert n_full.value % G == 0 and (columns or n_full.value == 0)
+        seen = np.zeros((nblocks, L), dtype=np.int32)
+        for item in range(n):
+            assert lib.su3g_walk_schedule(nblocks, L, G, 5, columns, item, ctypes.byref(blk), ctypes.byref(t0),
+                                          ctypes.byref(t1), None, None) == n
+            assert 0 <= blk.value < nblocks and 0 <= t0.value < t1.value <= L, (nblocks, L, G, item)
+            if item < n_full.value:
+                assert (blk.value, t0.value, t1.value) == (item, 0, L)
+            seen[blk.value, t0.value:t1.value] += 1
+        assert (seen == 1).all(), (nblocks, L, G, columns)
+        if columns:
+            assert cost(nblocks, L, G, 1, 0.5) <= cost(nblocks, L, G, 0, 0.5) + 1e-9, (nblocks, L, G)
+    assert lib.su3g_walk_schedule(0, 4, 148, 5, 1, -1, None, None, None, None, None) == -1
